@@ -1,0 +1,208 @@
+/*
+ * epk.h -- C ABI of the B200-native EpiCache block-prefill eviction step.
+ *
+ * This is the drop-in boundary.  Everything below the
+ * boundary is sm_100a CUDA (paper_2509_17396_b200/csrc/); everything above it
+ * is host code that mirrors the reference epikv C++ API
+ * (include/epikv/epikv_gpu.hpp for C++, paper_2509_17396_b200/ for Python).
+ *
+ * Signatures use plain pointers and sizes only.  Device pointers are marked
+ * [dev], host pointers [host].  Every call is enqueued on the context's stream
+ * and returns an EPK_* status; epk_last_error() holds the thread's last
+ * message.  Functions documented "synchronous" block until the stream drains
+ * because their result (an error the reference throws, a host count) is
+ * data-dependent.  The library never allocates inside a call except the
+ * context's grow-only workspace (reserve it with epk_ctx_reserve before CUDA
+ * graph capture).
+ *
+ * Reference interfaces replaced (file:line under /root/reference/proj/include/epikv):
+ *   epk_score            score_with_prompt (scoring.hpp:80) fused with the
+ *                        attention-weight loop of forward (toymodel.hpp:327-391)
+ *   epk_score_grids      score_with_prompt (scoring.hpp:80) on given grids
+ *   epk_select_pooled    evict_to_budget selection (kvcache.hpp:142-190)
+ *   epk_select_per_head  top_k_indices (numerics.hpp:111-125) per kv-head
+ *   epk_compact          evict_to_budget output loop (kvcache.hpp:192-199)
+ *   epk_append           append_to_cache (toymodel.hpp:428-443)
+ *   epk_evict_step       one block step of block_prefill (blockprefill.hpp:420-444):
+ *                        score -> per-layer evict, all layers
+ *   epk_kmeans*          kmeans (clustering.hpp:148-260)
+ *   epk_key_cosine_sigma measure_sensitivity reduction (allocation.hpp:80-100)
+ */
+#ifndef EPK_EPK_H
+#define EPK_EPK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (C++ shim maps them back to the reference exceptions) --- */
+#define EPK_OK 0
+#define EPK_ERR_ARG (-1)          /* bad argument (epikv::Error)                    */
+#define EPK_ERR_PIN_OVERFLOW (-2) /* pinned entries exceed budget (epikv::Error,    */
+                                  /*   kvcache.hpp:175-178)                          */
+#define EPK_ERR_DIM (-3)          /* shape mismatch (epikv::DimensionError)         */
+#define EPK_ERR_ZERO_NORM (-4)    /* epikv::ZeroNormError                           */
+#define EPK_ERR_EMPTY_PROMPT (-6) /* score_with_prompt: empty prompt (scoring.hpp:82) */
+#define EPK_ERR_CUDA (-7)         /* CUDA runtime / launch failure                  */
+#define EPK_ERR_UNSUPPORTED (-8)  /* shape outside what the kernels support         */
+
+/* ---- enums ---------------------------------------------------------------- */
+#define EPK_F32 0
+#define EPK_BF16 1
+#define EPK_F64 2
+
+#define EPK_AGG_AVG 0 /* Aggregation::Avg (scoring.hpp:35) */
+#define EPK_AGG_MAX 1 /* Aggregation::Max, the default      */
+
+#define EPK_SCORE_EXACT_F32 0 /* CUDA-core fp32, EPK-F32 v1 op order (bit-exact vs oracle) */
+#define EPK_SCORE_TC_BF16 1   /* tcgen05/TMEM tensor-core scorer, bf16 inputs, fp32 accum  */
+
+typedef struct epk_ctx epk_ctx;
+
+/*
+ * A layered CSR cache ("episode cache"), all layers in one allocation.
+ * Layer l owns rows [layer_base[l], layer_base[l+1]) of k/v/pos.  Inside the
+ * layer, kv-head h owns the REGION [head_off[h], head_off[h+1]) (layer-relative
+ * rows); its live entries are the first head_len[h] rows of the region,
+ * position-sorted (the per-head KVEntry list of kvcache.hpp:38-53).  Rows
+ * after head_len[h] are free slack that epk_append fills with the next block.
+ *   k, v     [dev]  [rows][head_dim] of dtype, row-major, 16-byte aligned rows
+ *   pos      [dev]  [rows] int32 token positions
+ *   head_off [dev]  [layers][kv_heads+1] int32 (data dependent after eviction)
+ *   head_len [dev]  [layers][kv_heads]   int32
+ *   layer_base [host] [layers+1] int64 capacity layout (layer_base[layers] = rows)
+ */
+typedef struct epk_cache_desc {
+    int32_t layers;
+    int32_t kv_heads;
+    int32_t head_dim;
+    int32_t dtype;
+    void* k;
+    void* v;
+    int32_t* pos;
+    int32_t* head_off;
+    int32_t* head_len;
+    const int64_t* layer_base;
+} epk_cache_desc;
+
+/* ---- context ---------------------------------------------------------------- */
+int epk_ctx_create(int device, void* cuda_stream, epk_ctx** out);
+int epk_ctx_destroy(epk_ctx* ctx);
+int epk_ctx_set_stream(epk_ctx* ctx, void* cuda_stream);
+int epk_ctx_reserve(epk_ctx* ctx, int64_t workspace_bytes);
+int epk_ctx_synchronize(epk_ctx* ctx);
+/* Deferred device-side errors (pin overflow inside epk_evict_step): returns the
+ * first EPK_* error raised since the last call and clears it.  Synchronous. */
+int epk_ctx_poll_error(epk_ctx* ctx);
+const char* epk_last_error(void);
+const char* epk_status_string(int status);
+int epk_version(void);
+/* Number of kernels this library launched on the context since creation. */
+int64_t epk_ctx_launch_count(epk_ctx* ctx);
+
+/* ---- K1 / K1': fused patched-prompt scoring --------------------------------- *
+ * scores[layer_base[l] + r] = score of live row r of layer l (fp32 [dev]).
+ *   q_prompt [dev] [layers][q_heads][prompt_len][head_dim]  (dtype of cache)
+ *   k_prompt [dev] [layers][kv_heads][prompt_len][head_dim]
+ * mode EPK_SCORE_EXACT_F32 needs dtype F32; EPK_SCORE_TC_BF16 needs dtype BF16
+ * and head_dim 128.  n_max_per_head [host] bounds every head's live count
+ * (grid sizing only).  Asynchronous. */
+int epk_score(epk_ctx* ctx, const epk_cache_desc* cache, const void* q_prompt,
+              const void* k_prompt, int32_t q_heads, int32_t prompt_len, int32_t aggregation,
+              int32_t mode, int64_t n_max_per_head, float* scores);
+
+/* score_with_prompt on explicit fp64 attention grids for ONE layer.
+ *   grids [dev] concatenated per query head qh: prompt_len x (n_h + prompt_len),
+ *   n_h = head_off[h+1]-head_off[h] with h = qh / (q_heads/kv_heads)
+ *   head_off [host] [kv_heads+1]; scores [dev] fp64 [head_off[kv_heads]].
+ * Bit-exact with the reference (sequential window sum). Asynchronous. */
+int epk_score_grids(epk_ctx* ctx, int32_t q_heads, int32_t kv_heads, int32_t prompt_len,
+                    const int64_t* head_off, const double* grids, int32_t aggregation,
+                    double* scores);
+
+/* ---- K2: selection -------------------------------------------------------- *
+ * Pooled selection of evict_to_budget for every layer of `cache`:
+ * keep[layer_base[l]+r] = 1 iff row r is retained.  Per layer: under budget
+ * (live <= kv_heads*budget[l]) keeps everything; else pins (sorted positions,
+ * [dev]) are kept and the best kv_heads*budget[l]-pinned_live candidates by
+ * (score desc, position asc, head asc) are kept.  scores are fp32 or fp64
+ * (score_dtype) in cache row order.  kept_per_layer [dev, optional] int32 [layers].
+ * Pin overflow raises EPK_ERR_PIN_OVERFLOW (synchronous check when
+ * `synchronous` != 0, else deferred to epk_ctx_poll_error). */
+int epk_select_pooled(epk_ctx* ctx, const epk_cache_desc* cache, const void* scores,
+                      int32_t score_dtype, const int64_t* layer_budgets, const int32_t* pins,
+                      int32_t n_pins, uint8_t* keep, int32_t* kept_per_layer, int32_t synchronous);
+
+/* Per-head top-k (top_k_indices semantics, ties to the lower row). */
+int epk_select_per_head(epk_ctx* ctx, const epk_cache_desc* cache, const void* scores,
+                        int32_t score_dtype, const int64_t* k_per_layer, uint8_t* keep);
+
+/* ---- K3: compaction ----------------------------------------------------- *
+ * Stable gather of the kept rows (K, V, pos) of `in` into `out` (same layers,
+ * heads, dim, dtype; out->layer_base is out's capacity layout).  Each head of
+ * `out` is followed by `slack` free rows for the next block's append;
+ * out->head_off is written on the device.  Asynchronous. */
+int epk_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out,
+                const uint8_t* keep, int32_t slack);
+
+/* ---- append_to_cache ------------------------------------------------------ *
+ * Writes a block of new rows into the slack after each head:
+ *   k_new, v_new [dev] [layers][kv_heads][len][head_dim], positions [dev] [len]
+ * and advances head_off so the heads stay contiguous (the gap after the last
+ * row of head h must be >= len; the caller sized it with `slack`).  Async. */
+int epk_append(epk_ctx* ctx, const epk_cache_desc* cache, const void* k_new, const void* v_new,
+               const int32_t* positions, int32_t len, int32_t slack);
+
+/* ---- fused block step ------------------------------------------------------ *
+ * score (mode) -> pooled select -> compact, for all layers, in -> out.
+ * scores_ws [dev, optional] fp32 [in rows] receives the scores.
+ * kept_per_layer [dev, optional] int32 [layers].  Asynchronous; pin overflow
+ * is deferred to epk_ctx_poll_error. */
+int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out,
+                   const void* q_prompt, const void* k_prompt, int32_t q_heads,
+                   int32_t prompt_len, const int64_t* layer_budgets, const int32_t* pins,
+                   int32_t n_pins, int32_t aggregation, int32_t mode, int64_t n_max_per_head,
+                   int32_t out_slack, float* scores_ws, int32_t* kept_per_layer);
+
+/* ---- K4: k-means (fp64, bit-exact vs clustering.hpp:148-260) -------------- *
+ * points [dev] [n][dim] fp64.  Device kernels: */
+int epk_kmeans_assign(epk_ctx* ctx, const double* points, int64_t n, int64_t dim,
+                      const double* centroids, int64_t k, int64_t* assign, double* best_d2);
+/* sums [dev] [k][dim] = sum over points i in index order with assign[i]==c
+ * (accumulated ON TOP of the incoming sums when accumulate != 0, the ordered
+ * chain used for sharded points), counts [dev] int64 [k] likewise. */
+int epk_kmeans_partial_sums(epk_ctx* ctx, const double* points, int64_t n, int64_t dim,
+                            const int64_t* assign, int64_t k, double* sums, int64_t* counts,
+                            int32_t accumulate);
+int epk_kmeans_finalize(epk_ctx* ctx, const double* sums, const int64_t* counts, int64_t k,
+                        int64_t dim, double* centroids);
+int epk_kmeans_sq_dist(epk_ctx* ctx, const double* points, int64_t n, int64_t dim,
+                       const double* centroids, const int64_t* assign, double* d2);
+/* Whole kmeans (k-means++ seeding with the reference RNG stream on the host,
+ * Lloyd on the device).  Synchronous.  assign_out, centroids_out, sse_out [host];
+ * sse_out has room for max_iters values. */
+int epk_kmeans(epk_ctx* ctx, const double* points, int64_t n, int64_t dim, int64_t k,
+               uint64_t seed, int64_t max_iters, int64_t* assign_out, double* centroids_out,
+               int64_t* iterations_out, double* sse_out);
+
+/* ---- K5: layer sensitivity ------------------------------------------------ *
+ * sigma[l] = mean over (h, t) of cosine(k_full, k_block), zero-norm pairs
+ * skipped (allocation.hpp:80-100).  k_full, k_block [dev] [layers][kv_heads][ntok][dim]
+ * of dtype (F32, BF16 or F64); sigma [dev] fp64 [layers]; skipped [dev] int64 [1].
+ * Asynchronous. */
+int epk_key_cosine_sigma(epk_ctx* ctx, const void* k_full, const void* k_block, int32_t dtype,
+                         int32_t layers, int32_t kv_heads, int64_t ntok, int32_t dim,
+                         double* sigma, int64_t* skipped);
+
+/* ---- diagnostics ---------------------------------------------------------- *
+ * y[i] = epk_expf(x[i]) as the EPK-F32 v1 kernels compute it ([dev] fp32),
+ * for the bitwise host/device parity test. */
+int epk_debug_expf(epk_ctx* ctx, const float* x, float* y, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EPK_EPK_H */

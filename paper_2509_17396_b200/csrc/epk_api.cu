@@ -1,0 +1,494 @@
+// epk_api.cu -- the C ABI (include/epk/epk.h): argument checking, context,
+// workspace, and the host orchestration that must stay on the host (the
+// k-means++ seeding and empty-cluster repair consume the reference RNG
+// stream, clustering.hpp:158-191,213-232).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "epk_internal.cuh"
+
+namespace epk {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+    return EPK_ERR_CUDA;
+}
+
+int ws_require(epk_ctx* ctx, int64_t bytes) {
+    if (bytes <= ctx->ws_bytes) return EPK_OK;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (ctx->stream) cudaStreamIsCapturing(ctx->stream, &st);
+    if (st != cudaStreamCaptureStatusNone)
+        return fail(EPK_ERR_ARG, "workspace must be reserved (epk_ctx_reserve) before graph capture");
+    if (ctx->ws) {
+        EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        EPK_CUDA_CHECK(cudaFree(ctx->ws));
+        ctx->ws = nullptr;
+        ctx->ws_bytes = 0;
+    }
+    const int64_t grow = align_up(bytes + bytes / 4, 1 << 20);
+    EPK_CUDA_CHECK(cudaMalloc(&ctx->ws, size_t(grow)));
+    ctx->ws_bytes = grow;
+    return EPK_OK;
+}
+
+int make_layer_table(const epk_cache_desc* c, LayerTable* t) {
+    if (!c) return fail(EPK_ERR_ARG, "null cache descriptor");
+    if (c->layers < 1 || c->layers > kMaxLayers) return fail(EPK_ERR_UNSUPPORTED, "layers must be in [1, 128]");
+    if (c->kv_heads < 1) return fail(EPK_ERR_ARG, "kv_heads must be >= 1");
+    if (!c->layer_base) return fail(EPK_ERR_ARG, "layer_base is null");
+    for (int l = 0; l <= c->layers; ++l) {
+        t->base[l] = c->layer_base[l];
+        if (l > 0 && t->base[l] < t->base[l - 1]) return fail(EPK_ERR_ARG, "layer_base must be non-decreasing");
+    }
+    for (int l = c->layers + 1; l <= kMaxLayers; ++l) t->base[l] = t->base[c->layers];
+    return EPK_OK;
+}
+
+int launch_select(epk_ctx*, const epk_cache_desc*, const void*, int, const int64_t*, const int32_t*, int, uint8_t*,
+                  int32_t*, int);
+int launch_compact(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*, int);
+int launch_append(epk_ctx*, const epk_cache_desc*, const void*, const void*, const int32_t*, int);
+int launch_score_f32(epk_ctx*, const epk_cache_desc*, const float*, const float*, int, int, int, int64_t, float*);
+int launch_score_tc(epk_ctx*, const epk_cache_desc*, const void*, const void*, int, int, int, int64_t, float*);
+int launch_score_grids(epk_ctx*, int, int, int, const int64_t*, const double*, int, double*);
+int launch_expf_probe(epk_ctx*, const float*, float*, int64_t);
+int launch_km_dist(epk_ctx*, const double*, int64_t, int64_t, const double*, int64_t, double*);
+int launch_km_assign(epk_ctx*, const double*, int64_t, int64_t, const double*, int64_t, int64_t*, double*);
+int launch_km_sums(epk_ctx*, const double*, int64_t, int64_t, const int64_t*, int64_t, double*, int64_t*, int);
+int launch_km_finalize(epk_ctx*, const double*, const int64_t*, int64_t, int64_t, double*);
+int launch_km_sqdist(epk_ctx*, const double*, int64_t, int64_t, const double*, const int64_t*, double*);
+int launch_key_cosine(epk_ctx*, const void*, const void*, int, int, int, int64_t, int, double*, int64_t*);
+
+static int check_ctx(epk_ctx* ctx) {
+    if (!ctx) return fail(EPK_ERR_ARG, "null context");
+    int dev = -1;
+    EPK_CUDA_CHECK(cudaGetDevice(&dev));
+    if (dev != ctx->device) EPK_CUDA_CHECK(cudaSetDevice(ctx->device));
+    return EPK_OK;
+}
+
+static int check_cache(const epk_cache_desc* c) {
+    if (!c) return fail(EPK_ERR_ARG, "null cache descriptor");
+    if (c->dtype != EPK_F32 && c->dtype != EPK_BF16 && c->dtype != EPK_F64) return fail(EPK_ERR_ARG, "bad cache dtype");
+    if (c->head_dim < 1) return fail(EPK_ERR_ARG, "head_dim must be >= 1");
+    if (!c->head_off || !c->head_len || !c->pos) return fail(EPK_ERR_ARG, "cache head_off/head_len/pos null");
+    if (c->layers < 1 || c->layers > kMaxLayers) return fail(EPK_ERR_UNSUPPORTED, "layers must be in [1, 128]");
+    return EPK_OK;
+}
+
+// ---- host mirror of epikv::Rng (numerics.hpp:146-183) used by the seeding ----
+struct HostRng {
+    std::mt19937_64 gen;
+    explicit HostRng(uint64_t s) : gen(s) {}
+    double uniform() { return double(gen() >> 11) * 0x1.0p-53; }
+    int64_t uniform_index(int64_t n) {
+        return int64_t((static_cast<unsigned __int128>(gen()) * uint64_t(n)) >> 64);
+    }
+};
+
+}  // namespace epk
+
+using namespace epk;
+
+extern "C" {
+
+const char* epk_last_error(void) { return g_last_error.c_str(); }
+
+const char* epk_status_string(int s) {
+    switch (s) {
+        case EPK_OK: return "ok";
+        case EPK_ERR_ARG: return "invalid argument";
+        case EPK_ERR_PIN_OVERFLOW: return "pinned entries exceed layer budget";
+        case EPK_ERR_DIM: return "dimension mismatch";
+        case EPK_ERR_ZERO_NORM: return "zero-norm input";
+        case EPK_ERR_EMPTY_PROMPT: return "empty prompt";
+        case EPK_ERR_CUDA: return "CUDA error";
+        case EPK_ERR_UNSUPPORTED: return "unsupported shape";
+        default: return "unknown status";
+    }
+}
+
+int epk_version(void) { return 10000; }
+
+int epk_ctx_create(int device, void* stream, epk_ctx** out) {
+    if (!out) return fail(EPK_ERR_ARG, "null out pointer");
+    int n = 0;
+    EPK_CUDA_CHECK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return fail(EPK_ERR_ARG, "bad device ordinal");
+    EPK_CUDA_CHECK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    EPK_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(EPK_ERR_UNSUPPORTED, std::string("needs an sm_100 (B200) device, got ") + prop.name);
+    epk_ctx* ctx = new epk_ctx();
+    ctx->device = device;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    ctx->num_sms = prop.multiProcessorCount;
+    cudaError_t e = cudaMalloc(&ctx->err_flag, sizeof(int));
+    if (e != cudaSuccess) {
+        delete ctx;
+        return cuda_fail(e, "cudaMalloc(err_flag)");
+    }
+    e = cudaMemset(ctx->err_flag, 0, sizeof(int));
+    if (e != cudaSuccess) {
+        cudaFree(ctx->err_flag);
+        delete ctx;
+        return cuda_fail(e, "cudaMemset(err_flag)");
+    }
+    *out = ctx;
+    return EPK_OK;
+}
+
+int epk_ctx_destroy(epk_ctx* ctx) {
+    if (!ctx) return EPK_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    else cudaDeviceSynchronize();
+    if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->step_buf) cudaFree(ctx->step_buf);
+    if (ctx->err_flag) cudaFree(ctx->err_flag);
+    delete ctx;
+    return EPK_OK;
+}
+
+int epk_ctx_set_stream(epk_ctx* ctx, void* stream) {
+    if (!ctx) return fail(EPK_ERR_ARG, "null context");
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    return EPK_OK;
+}
+
+int epk_ctx_reserve(epk_ctx* ctx, int64_t bytes) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    return ws_require(ctx, bytes);
+}
+
+int epk_ctx_synchronize(epk_ctx* ctx) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    return EPK_OK;
+}
+
+int epk_ctx_poll_error(epk_ctx* ctx) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    int v = 0;
+    EPK_CUDA_CHECK(cudaMemcpyAsync(&v, ctx->err_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (v != 0) {
+        EPK_CUDA_CHECK(cudaMemsetAsync(ctx->err_flag, 0, sizeof(int), ctx->stream));
+        EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (v == EPK_ERR_PIN_OVERFLOW) return fail(v, "evict_to_budget: pinned entries exceed layer budget");
+        return fail(v, "device-side capacity check failed (slack or output buffer too small)");
+    }
+    return EPK_OK;
+}
+
+int64_t epk_ctx_launch_count(epk_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int epk_score(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const void* kp, int32_t q_heads,
+              int32_t prompt_len, int32_t aggregation, int32_t mode, int64_t n_max, float* scores) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(c))) return rc;
+    if (prompt_len <= 0) return fail(EPK_ERR_EMPTY_PROMPT, "score_with_prompt: empty prompt");
+    if (q_heads < c->kv_heads || q_heads % c->kv_heads != 0)
+        return fail(EPK_ERR_DIM, "score_with_prompt: attention grid shape mismatch");
+    if (!q || !kp || !scores) return fail(EPK_ERR_ARG, "score: null pointer");
+    if (aggregation != EPK_AGG_MAX && aggregation != EPK_AGG_AVG) return fail(EPK_ERR_ARG, "bad aggregation");
+    if (mode == EPK_SCORE_EXACT_F32)
+        return launch_score_f32(ctx, c, static_cast<const float*>(q), static_cast<const float*>(kp), q_heads,
+                                prompt_len, aggregation == EPK_AGG_MAX, n_max, scores);
+    if (mode == EPK_SCORE_TC_BF16)
+        return launch_score_tc(ctx, c, q, kp, q_heads, prompt_len, aggregation == EPK_AGG_MAX, n_max, scores);
+    return fail(EPK_ERR_ARG, "bad score mode");
+}
+
+int epk_score_grids(epk_ctx* ctx, int32_t q_heads, int32_t kv_heads, int32_t prompt_len, const int64_t* head_off,
+                    const double* grids, int32_t aggregation, double* scores) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (!head_off) return fail(EPK_ERR_ARG, "null head_off");
+    return launch_score_grids(ctx, q_heads, kv_heads, prompt_len, head_off, grids, aggregation == EPK_AGG_MAX,
+                              scores);
+}
+
+int epk_select_pooled(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int32_t score_dtype,
+                      const int64_t* budgets, const int32_t* pins, int32_t n_pins, uint8_t* keep, int32_t* kept,
+                      int32_t synchronous) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(c))) return rc;
+    if (!scores || !budgets || !keep) return fail(EPK_ERR_ARG, "select: null pointer");
+    if (n_pins < 0) return fail(EPK_ERR_ARG, "select: negative pin count");
+    rc = launch_select(ctx, c, scores, score_dtype, budgets, pins, n_pins, keep, kept, 0);
+    if (rc) return rc;
+    if (synchronous) return epk_ctx_poll_error(ctx);
+    return EPK_OK;
+}
+
+int epk_select_per_head(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int32_t score_dtype,
+                        const int64_t* k_per_layer, uint8_t* keep) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(c))) return rc;
+    if (!scores || !k_per_layer || !keep) return fail(EPK_ERR_ARG, "select: null pointer");
+    return launch_select(ctx, c, scores, score_dtype, k_per_layer, nullptr, 0, keep, nullptr, 1);
+}
+
+int epk_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const uint8_t* keep,
+                int32_t slack) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(in)) || (rc = check_cache(out))) return rc;
+    if (!keep) return fail(EPK_ERR_ARG, "compact: null keep");
+    return launch_compact(ctx, in, out, keep, slack);
+}
+
+int epk_append(epk_ctx* ctx, const epk_cache_desc* c, const void* k_new, const void* v_new, const int32_t* positions,
+               int32_t len, int32_t slack) {
+    (void)slack;
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(c))) return rc;
+    if (!k_new || !v_new || !positions) return fail(EPK_ERR_ARG, "append: null pointer");
+    return launch_append(ctx, c, k_new, v_new, positions, len);
+}
+
+int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const void* q,
+                   const void* kp, int32_t q_heads, int32_t prompt_len, const int64_t* budgets, const int32_t* pins,
+                   int32_t n_pins, int32_t aggregation, int32_t mode, int64_t n_max, int32_t out_slack,
+                   float* scores_ws, int32_t* kept) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(in)) || (rc = check_cache(out))) return rc;
+    const int64_t rows = in->layer_base[in->layers];
+    // Workspace layout: [scores f32 rows][keep u8 rows] then the kernels' own
+    // scratch (they carve from the start, so give them a separate region).
+    float* scores = scores_ws;
+    uint8_t* keep = nullptr;
+    // Step buffers (scores, keep mask) live in their own allocation so the
+    // kernels' workspace growth never aliases them.
+    const int64_t need = align_up(rows * 4, 256) + align_up(rows, 256);
+    if (need > ctx->step_bytes) {
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(ctx->stream, &st);
+        if (st != cudaStreamCaptureStatusNone) return fail(EPK_ERR_ARG, "run one step before capturing a graph");
+        if (ctx->step_buf) {
+            EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            EPK_CUDA_CHECK(cudaFree(ctx->step_buf));
+            ctx->step_buf = nullptr;
+            ctx->step_bytes = 0;
+        }
+        EPK_CUDA_CHECK(cudaMalloc(&ctx->step_buf, size_t(need)));
+        ctx->step_bytes = need;
+    }
+    if (!scores) scores = static_cast<float*>(ctx->step_buf);
+    keep = static_cast<uint8_t*>(ctx->step_buf) + align_up(rows * 4, 256);
+    rc = epk_score(ctx, in, q, kp, q_heads, prompt_len, aggregation, mode, n_max, scores);
+    if (rc) return rc;
+    rc = launch_select(ctx, in, scores, EPK_F32, budgets, pins, n_pins, keep, kept, 0);
+    if (rc) return rc;
+    return launch_compact(ctx, in, out, keep, out_slack);
+}
+
+// ---- K4 ---------------------------------------------------------------------
+int epk_kmeans_assign(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, const double* cent, int64_t k,
+                      int64_t* assign, double* best_d2) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (n < 1 || dim < 1 || k < 1) return fail(EPK_ERR_ARG, "kmeans_assign: empty input");
+    return launch_km_assign(ctx, pts, n, dim, cent, k, assign, best_d2);
+}
+
+int epk_kmeans_partial_sums(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, const int64_t* assign, int64_t k,
+                            double* sums, int64_t* counts, int32_t accumulate) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    return launch_km_sums(ctx, pts, n, dim, assign, k, sums, counts, accumulate);
+}
+
+int epk_kmeans_finalize(epk_ctx* ctx, const double* sums, const int64_t* counts, int64_t k, int64_t dim,
+                        double* cent) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    return launch_km_finalize(ctx, sums, counts, k, dim, cent);
+}
+
+int epk_kmeans_sq_dist(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, const double* cent,
+                       const int64_t* assign, double* d2) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    return launch_km_sqdist(ctx, pts, n, dim, cent, assign, d2);
+}
+
+int epk_kmeans(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, int64_t k, uint64_t seed, int64_t max_iters,
+               int64_t* assign_out, double* cent_out, int64_t* iters_out, double* sse_out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (k < 1) return fail(EPK_ERR_ARG, "kmeans: cluster count must be >= 1");
+    if (n < k)
+        return fail(EPK_ERR_ARG, "kmeans: fewer points (" + std::to_string(n) + ") than clusters (" +
+                                     std::to_string(k) + ")");
+    cudaStream_t s = ctx->stream;
+    double *d_cent = nullptr, *d_sums = nullptr, *d_d2 = nullptr;
+    int64_t *d_assign = nullptr, *d_counts = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(d_cent);
+        cudaFree(d_sums);
+        cudaFree(d_d2);
+        cudaFree(d_assign);
+        cudaFree(d_counts);
+    };
+#define KM_CUDA(x)                                  \
+    do {                                            \
+        cudaError_t _e = (x);                       \
+        if (_e != cudaSuccess) {                    \
+            cleanup();                              \
+            return cuda_fail(_e, #x);               \
+        }                                           \
+    } while (0)
+#define KM_RC(x)           \
+    do {                   \
+        int _r = (x);      \
+        if (_r) {          \
+            cleanup();     \
+            return _r;     \
+        }                  \
+    } while (0)
+    KM_CUDA(cudaMalloc(&d_cent, size_t(k * dim) * 8));
+    KM_CUDA(cudaMalloc(&d_sums, size_t(k * dim) * 8));
+    KM_CUDA(cudaMalloc(&d_d2, size_t(n) * 8));
+    KM_CUDA(cudaMalloc(&d_assign, size_t(n) * 8));
+    KM_CUDA(cudaMalloc(&d_counts, size_t(k) * 8));
+
+    // k-means++ seeding (clustering.hpp:160-191): distances on the device,
+    // the running min, the sequential total and the draw on the host.
+    HostRng rng(seed);
+    std::vector<int64_t> chosen_idx;
+    chosen_idx.push_back(rng.uniform_index(n));
+    KM_CUDA(cudaMemcpyAsync(d_cent, pts + chosen_idx[0] * dim, size_t(dim) * 8, cudaMemcpyDeviceToDevice, s));
+    std::vector<double> best(static_cast<size_t>(n), std::numeric_limits<double>::infinity());
+    std::vector<double> dd(static_cast<size_t>(n));
+    int64_t have = 1;
+    while (have < k) {
+        KM_RC(launch_km_dist(ctx, pts, n, dim, d_cent + (have - 1) * dim, 1, d_d2));
+        KM_CUDA(cudaMemcpyAsync(dd.data(), d_d2, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+        KM_CUDA(cudaStreamSynchronize(s));
+        double total = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            best[size_t(i)] = std::min(best[size_t(i)], dd[size_t(i)]);
+            total += best[size_t(i)];
+        }
+        int64_t chosen = 0;
+        if (total > 0.0) {
+            const double target = rng.uniform() * total;
+            double acc = 0.0;
+            chosen = n - 1;
+            for (int64_t i = 0; i < n; ++i) {
+                acc += best[size_t(i)];
+                if (acc > target) {
+                    chosen = i;
+                    break;
+                }
+            }
+        } else {
+            chosen = rng.uniform_index(n);
+        }
+        KM_CUDA(cudaMemcpyAsync(d_cent + have * dim, pts + chosen * dim, size_t(dim) * 8, cudaMemcpyDeviceToDevice, s));
+        ++have;
+    }
+
+    // Lloyd iterations (clustering.hpp:195-255).
+    std::vector<int64_t> assign(static_cast<size_t>(n), 0);
+    std::vector<int64_t> prev(static_cast<size_t>(n), 0);
+    std::vector<int64_t> counts(static_cast<size_t>(k));
+    int64_t iters = 0;
+    for (int64_t iter = 0; iter < max_iters; ++iter) {
+        KM_RC(launch_km_assign(ctx, pts, n, dim, d_cent, k, d_assign, nullptr));
+        KM_CUDA(cudaMemcpyAsync(assign.data(), d_assign, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+        KM_CUDA(cudaStreamSynchronize(s));
+        bool changed = false;
+        for (int64_t i = 0; i < n; ++i)
+            if (assign[size_t(i)] != prev[size_t(i)]) changed = true;
+        std::fill(counts.begin(), counts.end(), 0);
+        for (int64_t a : assign) ++counts[size_t(a)];
+        bool repaired = false;
+        for (int64_t c = 0; c < k; ++c) {
+            if (counts[size_t(c)] > 0) continue;
+            // distances to the current centroids under the current assignment
+            KM_CUDA(cudaMemcpyAsync(d_assign, assign.data(), size_t(n) * 8, cudaMemcpyHostToDevice, s));
+            KM_RC(launch_km_sqdist(ctx, pts, n, dim, d_cent, d_assign, d_d2));
+            KM_CUDA(cudaMemcpyAsync(dd.data(), d_d2, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+            KM_CUDA(cudaStreamSynchronize(s));
+            int64_t victim = 0;
+            double worst = -1.0;
+            for (int64_t i = 0; i < n; ++i) {
+                if (counts[size_t(assign[size_t(i)])] <= 1) continue;
+                if (dd[size_t(i)] > worst) {
+                    worst = dd[size_t(i)];
+                    victim = i;
+                }
+            }
+            --counts[size_t(assign[size_t(victim)])];
+            assign[size_t(victim)] = c;
+            ++counts[size_t(c)];
+            changed = true;
+            repaired = true;
+        }
+        if (repaired) KM_CUDA(cudaMemcpyAsync(d_assign, assign.data(), size_t(n) * 8, cudaMemcpyHostToDevice, s));
+        KM_RC(launch_km_sums(ctx, pts, n, dim, d_assign, k, d_sums, d_counts, 0));
+        KM_RC(launch_km_finalize(ctx, d_sums, d_counts, k, dim, d_cent));
+        iters = iter + 1;
+        KM_RC(launch_km_sqdist(ctx, pts, n, dim, d_cent, d_assign, d_d2));
+        KM_CUDA(cudaMemcpyAsync(dd.data(), d_d2, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+        KM_CUDA(cudaStreamSynchronize(s));
+        double sse = 0.0;
+        for (int64_t i = 0; i < n; ++i) sse += dd[size_t(i)];
+        if (sse_out) sse_out[iter] = sse;
+        prev = assign;
+        if (!changed) break;
+    }
+    std::memcpy(assign_out, assign.data(), size_t(n) * 8);
+    KM_CUDA(cudaMemcpyAsync(cent_out, d_cent, size_t(k * dim) * 8, cudaMemcpyDeviceToHost, s));
+    KM_CUDA(cudaStreamSynchronize(s));
+    *iters_out = iters;
+    cleanup();
+#undef KM_CUDA
+#undef KM_RC
+    return EPK_OK;
+}
+
+// ---- K5 ---------------------------------------------------------------------
+int epk_key_cosine_sigma(epk_ctx* ctx, const void* kf, const void* kb, int32_t dtype, int32_t layers, int32_t H,
+                         int64_t ntok, int32_t dim, double* sigma, int64_t* skipped) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (layers < 1 || H < 1 || ntok < 1 || dim < 1) return fail(EPK_ERR_ARG, "key_cosine: empty input");
+    if (dtype != EPK_F32 && dtype != EPK_BF16 && dtype != EPK_F64) return fail(EPK_ERR_ARG, "key_cosine: bad dtype");
+    return launch_key_cosine(ctx, kf, kb, dtype, layers, H, ntok, dim, sigma, skipped);
+}
+
+// ---- diagnostics ---------------------------------------------------------------
+int epk_debug_expf(epk_ctx* ctx, const float* x, float* y, int64_t n) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    return launch_expf_probe(ctx, x, y, n);
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// epk_internal.cuh -- shared device/host helpers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstring>
+#include <string>
+
+#include "epk/epk.h"
+
+struct epk_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    void* ws = nullptr;  // grow-only workspace
+    int64_t ws_bytes = 0;
+    void* step_buf = nullptr;  // epk_evict_step scores + keep mask
+    int64_t step_bytes = 0;
+    int* err_flag = nullptr;  // deferred device-side error code (device int)
+    int64_t launches = 0;
+    int num_sms = 148;
+};
+
+namespace epk {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+// Workspace carve-up: returns a pointer into ctx->ws (grows the workspace when
+// needed; growing is not allowed while the stream is being captured).
+int ws_require(epk_ctx* ctx, int64_t bytes);
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct WsCarver {
+    char* base;
+    int64_t off = 0;
+    explicit WsCarver(void* b) : base(static_cast<char*>(b)) {}
+    template <typename T>
+    T* take(int64_t count) {
+        off = align_up(off, 256);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += count * int64_t(sizeof(T));
+        return p;
+    }
+};
+
+inline int dtype_size(int dt) { return dt == EPK_F64 ? 8 : (dt == EPK_F32 ? 4 : 2); }
+
+#define EPK_CUDA_CHECK(expr)                                      \
+    do {                                                          \
+        cudaError_t _e = (expr);                                  \
+        if (_e != cudaSuccess) return ::epk::cuda_fail(_e, #expr); \
+    } while (0)
+
+#define EPK_LAUNCH_CHECK(ctx)                                                \
+    do {                                                                     \
+        (ctx)->launches++;                                                   \
+        cudaError_t _e = cudaGetLastError();                                 \
+        if (_e != cudaSuccess) return ::epk::cuda_fail(_e, "kernel launch"); \
+    } while (0)
+
+// Layer table passed by value to kernels (host layer_base copied in).
+constexpr int kMaxLayers = 128;
+struct LayerTable {
+    int64_t base[kMaxLayers + 1];
+};
+
+int make_layer_table(const epk_cache_desc* c, LayerTable* t);
+
+// ---------------------------------------------------------------------------
+// Order-preserving score keys.  Selection sorts ascending on
+//   (desc_key(score), position, head)
+// desc_key maps larger scores to smaller keys; -0.0 is canonicalised to +0.0
+// because the reference compares with != (kvcache.hpp:182), under which
+// -0.0 == +0.0 and the tie falls through to the position.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline uint32_t desc_key(float s) {
+    uint32_t u;
+#ifdef __CUDA_ARCH__
+    u = __float_as_uint(s);
+#else
+    memcpy(&u, &s, 4);
+#endif
+    if (u == 0x80000000u) u = 0;
+    const uint32_t ord = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ~ord;
+}
+
+__host__ __device__ inline uint64_t desc_key(double s) {
+    uint64_t u;
+#ifdef __CUDA_ARCH__
+    u = static_cast<uint64_t>(__double_as_longlong(s));
+#else
+    memcpy(&u, &s, 8);
+#endif
+    if (u == 0x8000000000000000ull) u = 0;
+    const uint64_t ord = (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+    return ~ord;
+}
+
+}  // namespace epk

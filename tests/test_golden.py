@@ -1,0 +1,64 @@
+"""The oracle against golden fixtures generated from the reference itself
+(tests/golden/make_golden.py).  Runs anywhere (no /root/reference needed)."""
+import os
+
+import numpy as np
+import pytest
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_v1.npz")
+
+
+@pytest.fixture(scope="module")
+def g():
+    return np.load(GOLDEN)
+
+
+def test_evict_fixtures(orc, g):
+    for i in range(int(g["ev_count"])):
+        st, keep = orc.evict_layer(g[f"ev{i}_head_off"], g[f"ev{i}_pos"], g[f"ev{i}_scores"], int(g[f"ev{i}_budget"]),
+                                   set(g[f"ev{i}_pins"].tolist()))
+        if int(g[f"ev{i}_status"]) == -2:
+            assert st == -2
+        else:
+            assert np.array_equal(keep, g[f"ev{i}_keep"]), i
+
+
+def test_score_fixtures_bitwise(orc, g):
+    for i in range(int(g["sc_count"])):
+        for agg in (1, 0):
+            s = orc.score_layer_f64(g[f"sc{i}_q"], g[f"sc{i}_k"], g[f"sc{i}_kp"], g[f"sc{i}_head_off"], bool(agg))
+            assert np.array_equal(s, g[f"sc{i}_{agg}_scores"]), (i, agg)
+
+
+def test_kmeans_fixtures_bitwise(orc, g):
+    for i in range(int(g["km_count"])):
+        a, c, it, sse = orc.kmeans(g[f"km{i}_pts"], int(g[f"km{i}_k"]), int(g[f"km{i}_seed"]))
+        assert np.array_equal(a, g[f"km{i}_assign"]) and np.array_equal(c, g[f"km{i}_cent"])
+        assert it == int(g[f"km{i}_iters"]) and np.array_equal(sse, g[f"km{i}_sse"])
+
+
+def test_allocate_fixtures(orc, g):
+    for i in range(int(g["al_count"])):
+        b, w = orc.allocate(g[f"al{i}_s"], int(g[f"al{i}_M"]), float(g[f"al{i}_alpha"]))
+        assert np.array_equal(b, g[f"al{i}_b"]) and np.array_equal(w, g[f"al{i}_w"])
+
+
+def test_sensitivity_fixture(orc, g):
+    sigma, skipped = orc.sensitivity(g["sens_kf"], g["sens_kb"])
+    assert np.array_equal(sigma, g["sens_sigma"]) and skipped == int(g["sens_skipped"])
+
+
+def test_trace_fixture(g):
+    assert g["bp_c2_series"].tolist() == [3, 1, 4, 1, 4, 1]
+    assert g["bp_alloc_counts"].tolist() == [4, 12]
+
+
+def test_expf_contract(orc):
+    """EPK-F32 v1 exp: <= 1 ulp from the correctly rounded value on the
+    softmax domain, exact 1 at 0, 0 below -103.97."""
+    x = np.linspace(-87.0, 0.0, 400001).astype(np.float32)
+    y = orc.expf(x)
+    cr = np.exp(x.astype(np.float64)).astype(np.float32)
+    assert np.max(np.abs(y.view(np.int32).astype(np.int64) - cr.view(np.int32))) <= 1
+    assert orc.expf(np.array([0.0], np.float32))[0] == 1.0
+    assert orc.expf(np.array([-104.0], np.float32))[0] == 0.0

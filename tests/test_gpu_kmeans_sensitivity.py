@@ -1,0 +1,76 @@
+"""K4 (k-means) bit-exact vs the reference fixtures/oracle; K5 (sensitivity)
+vs the reference's measure_sensitivity; allocate vs the reference."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_v1.npz")
+
+
+def test_kmeans_golden_bitwise(gpu):
+    g = np.load(GOLDEN)
+    for i in range(int(g["km_count"])):
+        r = gpu.kmeans(g[f"km{i}_pts"], int(g[f"km{i}_k"]), int(g[f"km{i}_seed"]))
+        assert r.assignments == g[f"km{i}_assign"].tolist()
+        assert np.array_equal(r.centroids, g[f"km{i}_cent"])
+        assert r.iterations == int(g[f"km{i}_iters"])
+        assert np.array_equal(np.array(r.sse_per_iteration), g[f"km{i}_sse"])
+
+
+@pytest.mark.parametrize("n,dim,k,seed", [(2048, 256, 4, 1), (2048, 1024, 8, 2), (300, 3, 7, 9)])
+def test_kmeans_vs_oracle(gpu, orc, n, dim, k, seed):
+    rng = np.random.default_rng(seed)
+    centers = rng.standard_normal((k, dim)) * 3
+    pts = centers[rng.integers(0, k, n)] + rng.standard_normal((n, dim))
+    r = gpu.kmeans(pts, k, seed)
+    a, c, it, sse = orc.kmeans(pts, k, seed)
+    assert r.assignments == a.tolist() and np.array_equal(r.centroids, c) and r.iterations == it
+    assert np.array_equal(np.array(r.sse_per_iteration), sse)
+
+
+def test_kmeans_repair_and_edges(gpu, orc):
+    pts = np.repeat(np.random.default_rng(0).standard_normal((3, 4)), 5, axis=0)
+    pts = np.concatenate([pts, pts[:1]])
+    r = gpu.kmeans(pts, 6, 3)
+    a, c, it, sse = orc.kmeans(pts, 6, 3)
+    assert r.assignments == a.tolist() and np.array_equal(r.centroids, c)
+    with pytest.raises(gpu.Error, match="fewer points"):
+        gpu.kmeans(pts[:2], 3, 1)
+    with pytest.raises(gpu.Error, match="cluster count"):
+        gpu.kmeans(pts, 0, 1)
+    one = gpu.kmeans(pts, 1, 4)  # E = 1: the plain mean
+    assert np.allclose(one.centroids[0], pts.mean(0))
+
+
+def test_sensitivity_golden(gpu):
+    g = np.load(GOLDEN)
+    kf = torch.as_tensor(g["sens_kf"], device="cuda")
+    kb = torch.as_tensor(g["sens_kb"], device="cuda")
+    prof = gpu.sensitivity_from_keys(kf, kb)
+    assert np.allclose(prof.sigma, g["sens_sigma"], rtol=0, atol=1e-12)
+    assert prof.skipped_zero_norm == int(g["sens_skipped"])
+
+
+def test_sensitivity_bf16_large_vs_oracle(gpu, orc):
+    torch.manual_seed(0)
+    L, H, N, d = 4, 8, 4096, 128
+    kf = torch.randn(L, H, N, d, device="cuda").bfloat16()
+    kb = (kf.float() + 0.3 * torch.randn_like(kf.float())).bfloat16()
+    kb[1, 2, 5] = 0  # a zero-norm pair is skipped
+    prof = gpu.sensitivity_from_keys(kf, kb)
+    sig, sk = orc.sensitivity(kf.double().cpu().numpy(), kb.double().cpu().numpy())
+    assert np.allclose(prof.sigma, sig, rtol=0, atol=1e-12) and prof.skipped_zero_norm == sk == 1
+
+
+def test_allocate_golden(gpu):
+    g = np.load(GOLDEN)
+    for i in range(int(g["al_count"])):
+        prof = gpu.SensitivityProfile(sigma=[1 - s for s in g[f"al{i}_s"]], sensitivity=g[f"al{i}_s"].tolist())
+        a = gpu.allocate(prof, int(g[f"al{i}_M"]), float(g[f"al{i}_alpha"]))
+        assert a.layer_budgets == g[f"al{i}_b"].tolist()
+        assert a.weights == g[f"al{i}_w"].tolist()
+        assert a.total() == len(a.layer_budgets) * int(g[f"al{i}_M"])
