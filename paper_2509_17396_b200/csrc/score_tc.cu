@@ -87,7 +87,7 @@ struct P1Item {
     int64_t krow0;   // first K row of the head (global)
     int cache_t0, cache_t1;
     int prompt_tiles;
-    int ntiles() const { return (cache_t1 > cache_t0 ? cache_t1 - cache_t0 : 0) + prompt_tiles; }
+    __device__ int ntiles() const { return (cache_t1 > cache_t0 ? cache_t1 - cache_t0 : 0) + prompt_tiles; }
 };
 
 __device__ __forceinline__ P1Item p1_item(const TcParams& P, int64_t it) {
@@ -314,7 +314,7 @@ __global__ void tc_merge_kernel(const __grid_constant__ TcParams P) {
 struct P2Item {
     int l, h, tile, n_h;
     int64_t krow0;
-    bool live() const { return tile * kTile < n_h; }
+    __device__ bool live() const { return tile * kTile < n_h; }
 };
 
 __device__ __forceinline__ P2Item p2_item(const TcParams& P, int64_t it) {

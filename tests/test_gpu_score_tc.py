@@ -1,0 +1,106 @@
+"""K1 (tcgen05/TMEM tensor-core scorer, bf16 inputs, fp32 accumulate) vs
+the oracle on the same bf16-rounded inputs.
+
+Tolerances (north_star): the bf16 tensor-core path must give retained-set
+overlap >= 99.9% per block step on identical cache state.  The scores
+themselves are checked at 1e-4 relative against the fp64 restatement
+(products of bf16 values are exact in fp32; the residual is fp32
+accumulation order plus ex2/lg2.approx, measured ~1e-6)."""
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import bf16_round, random_layer
+
+pytestmark = pytest.mark.gpu
+
+SCORE_RTOL = 1e-4
+OVERLAP_MIN = 0.999
+
+
+def _run(epk, layers, qs, kps, agg="max", mode="tc_bf16"):
+    H = len(layers[0][0]) - 1
+    cap = [int(ho[-1]) + 1 for ho, _, _, _ in layers]
+    dt = torch.bfloat16 if mode == "tc_bf16" else torch.float32
+    c = epk.EpisodeCache(len(layers), H, 128, cap, dt, "cuda")
+    c.load_layers([(np.diff(ho), pos, k, v) for ho, pos, k, v in layers])
+    q = torch.as_tensor(np.stack(qs), device="cuda").to(dt)
+    kp = torch.as_tensor(np.stack(kps), device="cuda").to(dt)
+    sc = epk.score_with_prompt(c, q, kp, agg, mode=mode).cpu().numpy()
+    return c, [sc[int(c.layer_base[l]):int(c.layer_base[l]) + len(layers[l][1])] for l in range(len(layers))]
+
+
+def _inputs(rng, L, Hq, H, p, counts):
+    layers, qs, kps = [], [], []
+    for _ in range(L):
+        ho, pos, k, v = random_layer(rng, H, counts, 128, dtype=np.float32)
+        layers.append((ho, pos, bf16_round(k), bf16_round(v)))
+        qs.append(bf16_round(rng.standard_normal((Hq, p, 128)).astype(np.float32)))
+        kps.append(bf16_round(rng.standard_normal((H, p, 128)).astype(np.float32)))
+    return layers, qs, kps
+
+
+@pytest.mark.parametrize("agg", ["max", "avg"])
+@pytest.mark.parametrize("cfg", [
+    (1, 3, 1, 128, [1000]),           # one head, G*p = 384 (3 query chunks, resident)
+    (2, 24, 8, 64, [300] * 8),        # Llama GQA, p = 64
+    (1, 4, 4, 1, [0, 129, 5, 256]),   # p = 1, empty head, partial tiles
+    (1, 12, 2, 200, [700, 333]),      # two prompt tiles, G*p = 1200 (streamed Q)
+    (1, 28, 4, 128, [2100, 1900, 17, 4096]),  # Qwen GQA (G = 7, NQ = 7)
+])
+def test_tc_scores_vs_fp64_oracle(gpu, orc, cfg, agg):
+    L, Hq, H, p, counts = cfg
+    rng = np.random.default_rng(sum(counts) + p + Hq)
+    layers, qs, kps = _inputs(rng, L, Hq, H, p, counts)
+    _, got = _run(gpu, layers, qs, kps, agg)
+    for l, (ho, pos, k, v) in enumerate(layers):
+        if len(pos) == 0:
+            continue
+        exp = orc.score_layer_f64(qs[l].astype(np.float64), k.astype(np.float64), kps[l].astype(np.float64), ho,
+                                  agg == "max")
+        rel = np.abs(got[l].astype(np.float64) - exp) / exp
+        assert rel.max() < SCORE_RTOL, (l, rel.max())
+
+
+def test_tc_retained_overlap_cfg2_layer(gpu, orc):
+    """cfg2 layer shape (8 heads x 10,240 live entries, G = 3, p = 128, M = 8,192):
+    the bf16 tensor-core selection keeps >= 99.9% of the fp64 oracle's set."""
+    rng = np.random.default_rng(2)
+    layers, qs, kps = _inputs(rng, 1, 24, 8, 128, [10240] * 8)
+    c, got = _run(gpu, layers, qs, kps)
+    ho, pos, k, v = layers[0]
+    # fp64 reference scores via the exact GPU path on the same values is
+    # too slow to restate on CPU at this size; use the fp32 parity kernel
+    # (bit-exact with the oracle, within 1e-5 of fp64) as the reference.
+    _, ref32 = _run(gpu, layers, qs, kps, mode="exact_f32")
+    rel = np.abs(got[0] - ref32[0]) / ref32[0]
+    assert rel.max() < SCORE_RTOL, rel.max()
+    M = 8192
+    _, keep_ref = orc.evict_layer(ho, pos, ref32[0].astype(np.float64), M)
+    _, keep_tc = orc.evict_layer(ho, pos, got[0].astype(np.float64), M)
+    inter = np.logical_and(keep_ref, keep_tc).sum()
+    recall = inter / keep_ref.sum()
+    assert recall >= OVERLAP_MIN, recall
+
+
+def test_tc_fused_step_overlap(gpu, orc):
+    """The whole tensor-core step (score -> select -> compact) against the
+    oracle chain on the same state: retained overlap >= 99.9% per layer."""
+    from paper_2509_17396_b200.step import evict_step
+    rng = np.random.default_rng(4)
+    L, Hq, H, p, M = 3, 24, 8, 128, 1024
+    layers, qs, kps = _inputs(rng, L, Hq, H, p, [1280] * H)
+    cap = [int(ho[-1]) + 256 * H for ho, _, _, _ in layers]
+    cin = gpu.EpisodeCache(L, H, 128, cap, torch.bfloat16, "cuda")
+    cin.load_layers([(np.diff(ho), pos, k, v) for ho, pos, k, v in layers])
+    cout = gpu.EpisodeCache(L, H, 128, cap, torch.bfloat16, "cuda")
+    evict_step(cin, cout, torch.as_tensor(np.stack(qs), device="cuda").bfloat16(),
+               torch.as_tensor(np.stack(kps), device="cuda").bfloat16(), [M] * L, slack=256)
+    for l, (ho, pos, k, v) in enumerate(layers):
+        s = orc.score_layer_f64(qs[l].astype(np.float64), k.astype(np.float64), kps[l].astype(np.float64), ho, True)
+        _, keep = orc.evict_layer(ho, pos, s, M)
+        got = cout.retained_positions()[l]
+        ref = [pos[ho[h]:ho[h + 1]][keep[ho[h]:ho[h + 1]]].tolist() for h in range(H)]
+        inter = sum(len(set(a) & set(b)) for a, b in zip(got, ref))
+        assert sum(len(a) for a in got) == H * M
+        assert inter / (H * M) >= OVERLAP_MIN
