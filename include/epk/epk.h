@@ -102,6 +102,12 @@ const char* epk_status_string(int status);
 int epk_version(void);
 /* Number of kernels this library launched on the context since creation. */
 int64_t epk_ctx_launch_count(epk_ctx* ctx);
+/* Live per-kernel timing: while enabled, every kernel launch is bracketed by
+ * CUDA events on the context stream.  Enabling clears the record.
+ * epk_ctx_profile_read(ctx, -1, ...) synchronises and returns the record
+ * count; index >= 0 returns the kernel name (<= 31 chars) and milliseconds. */
+int epk_ctx_profile(epk_ctx* ctx, int32_t enable);
+int64_t epk_ctx_profile_read(epk_ctx* ctx, int64_t index, char* name_out, float* ms_out);
 
 /* ---- K1 / K1': fused patched-prompt scoring --------------------------------- *
  * scores[layer_base[l] + r] = score of live row r of layer l (fp32 [dev]).

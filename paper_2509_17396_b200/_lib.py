@@ -51,6 +51,8 @@ _SIGS = {
     "epk_status_string": (C.c_char_p, [C.c_int]),
     "epk_version": (C.c_int, []),
     "epk_ctx_launch_count": (i64, [vp]),
+    "epk_ctx_profile": (C.c_int, [vp, i32]),
+    "epk_ctx_profile_read": (i64, [vp, i64, C.c_char_p, C.POINTER(C.c_float)]),
     "epk_score": (C.c_int, [vp, C.POINTER(CacheDesc), vp, vp, i32, i32, i32, i32, i64, vp]),
     "epk_score_grids": (C.c_int, [vp, i32, i32, i32, vp, vp, i32, vp]),
     "epk_select_pooled": (C.c_int, [vp, C.POINTER(CacheDesc), vp, i32, vp, vp, i32, vp, vp, i32]),

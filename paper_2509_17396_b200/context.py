@@ -41,6 +41,22 @@ class Context:
     def launches(self) -> int:
         return int(_lib.load().epk_ctx_launch_count(self.handle))
 
+    def profile(self, enable: bool) -> None:
+        """Bracket every kernel launch with CUDA events (live per-kernel timing)."""
+        _lib.call("epk_ctx_profile", self.handle, int(enable))
+
+    def profile_records(self) -> list[tuple[str, float]]:
+        """[(kernel name, ms)] recorded since profile(True); synchronises."""
+        lib = _lib.load()
+        n = int(lib.epk_ctx_profile_read(self.handle, -1, None, None))
+        out = []
+        name = C.create_string_buffer(32)
+        ms = C.c_float()
+        for i in range(max(n, 0)):
+            lib.epk_ctx_profile_read(self.handle, i, name, C.byref(ms))
+            out.append((name.value.decode(), float(ms.value)))
+        return out
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             _lib.load().epk_ctx_destroy(self.handle)

@@ -286,10 +286,13 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     P.chunk_cnt = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
     P.chunk_prefix = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
     dim3 grid(P.max_chunks, in->layers);
+    EPK_PROF(ctx, "compact_count");
     compact_count_kernel<<<grid, kCompactThreads, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
+    EPK_PROF(ctx, "compact_plan");
     compact_plan_kernel<<<in->layers, 1024, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
+    EPK_PROF(ctx, "compact_gather");
     compact_gather_kernel<<<grid, kCompactThreads, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
@@ -367,9 +370,11 @@ int launch_append(epk_ctx* ctx, const epk_cache_desc* c, const void* k_new, cons
     const int64_t nvec = int64_t(len) * P.row_vec;
     const int bx = int(std::min<int64_t>(64, (nvec + 255) / 256));
     dim3 grid(bx, c->layers * c->kv_heads);
+    EPK_PROF(ctx, "append_copy");
     append_copy_kernel<<<grid, 256, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     const int n = c->layers * c->kv_heads;
+    EPK_PROF(ctx, "append_len");
     append_len_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(c->head_len, c->head_off, c->kv_heads, n, len);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;

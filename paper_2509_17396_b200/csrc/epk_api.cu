@@ -46,6 +46,30 @@ int ws_require(epk_ctx* ctx, int64_t bytes) {
     return EPK_OK;
 }
 
+void prof_begin(epk_ctx* ctx, const char* name) {
+    if (!ctx->profiling) return;
+    epk_prof_rec r;
+    std::snprintf(r.name, sizeof(r.name), "%s", name);
+    cudaEventCreate(&r.start);
+    cudaEventCreate(&r.stop);
+    cudaEventRecord(r.start, ctx->stream);
+    r.stop = r.stop;
+    ctx->prof.push_back(r);
+}
+
+void prof_end(epk_ctx* ctx) {
+    if (!ctx->profiling || ctx->prof.empty()) return;
+    cudaEventRecord(ctx->prof.back().stop, ctx->stream);
+}
+
+static void prof_clear(epk_ctx* ctx) {
+    for (auto& r : ctx->prof) {
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    ctx->prof.clear();
+}
+
 int make_layer_table(const epk_cache_desc* c, LayerTable* t) {
     if (!c) return fail(EPK_ERR_ARG, "null cache descriptor");
     if (c->layers < 1 || c->layers > kMaxLayers) return fail(EPK_ERR_UNSUPPORTED, "layers must be in [1, 128]");
@@ -158,6 +182,7 @@ int epk_ctx_destroy(epk_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
+    prof_clear(ctx);
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->step_buf) cudaFree(ctx->step_buf);
     if (ctx->err_flag) cudaFree(ctx->err_flag);
@@ -200,6 +225,30 @@ int epk_ctx_poll_error(epk_ctx* ctx) {
 }
 
 int64_t epk_ctx_launch_count(epk_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int epk_ctx_profile(epk_ctx* ctx, int32_t enable) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    prof_clear(ctx);
+    ctx->profiling = enable != 0;
+    return EPK_OK;
+}
+
+int64_t epk_ctx_profile_read(epk_ctx* ctx, int64_t index, char* name_out, float* ms_out) {
+    if (!ctx) return -1;
+    if (index < 0) {
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return -1;
+        return int64_t(ctx->prof.size());
+    }
+    if (index >= int64_t(ctx->prof.size())) return -1;
+    const epk_prof_rec& r = ctx->prof[size_t(index)];
+    std::snprintf(name_out, 32, "%s", r.name);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.start, r.stop);
+    *ms_out = ms;
+    return int64_t(ctx->prof.size());
+}
 
 int epk_score(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const void* kp, int32_t q_heads,
               int32_t prompt_len, int32_t aggregation, int32_t mode, int64_t n_max, float* scores) {

@@ -10,6 +10,13 @@
 
 #include "epk/epk.h"
 
+#include <vector>
+
+struct epk_prof_rec {
+    char name[32];
+    cudaEvent_t start, stop;
+};
+
 struct epk_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -20,6 +27,8 @@ struct epk_ctx {
     int* err_flag = nullptr;  // deferred device-side error code (device int)
     int64_t launches = 0;
     int num_sms = 148;
+    bool profiling = false;  // record CUDA events around every kernel launch
+    std::vector<epk_prof_rec> prof;
 };
 
 namespace epk {
@@ -58,9 +67,15 @@ inline int dtype_size(int dt) { return dt == EPK_F64 ? 8 : (dt == EPK_F32 ? 4 : 
 #define EPK_LAUNCH_CHECK(ctx)                                                \
     do {                                                                     \
         (ctx)->launches++;                                                   \
+        ::epk::prof_end(ctx);                                                \
         cudaError_t _e = cudaGetLastError();                                 \
         if (_e != cudaSuccess) return ::epk::cuda_fail(_e, "kernel launch"); \
     } while (0)
+
+// Live per-kernel timing (epk_ctx_profile): events on the launching stream.
+void prof_begin(epk_ctx* ctx, const char* name);
+void prof_end(epk_ctx* ctx);
+#define EPK_PROF(ctx, name) ::epk::prof_begin(ctx, name)
 
 // Layer table passed by value to kernels (host layer_base copied in).
 constexpr int kMaxLayers = 128;

@@ -99,6 +99,7 @@ __global__ void km_sqdist_assigned_kernel(const double* __restrict__ pts, int64_
 int launch_km_dist(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, const double* cent, int64_t k,
                    double* D) {
     const int64_t tot = n * k;
+    EPK_PROF(ctx, "km_dist");
     km_dist_kernel<<<unsigned((tot + 127) / 128), 128, 0, ctx->stream>>>(pts, n, dim, cent, k, D);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
@@ -111,6 +112,7 @@ int launch_km_assign(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, co
     double* D = static_cast<double*>(ctx->ws);
     rc = launch_km_dist(ctx, pts, n, dim, cent, k, D);
     if (rc) return rc;
+    EPK_PROF(ctx, "km_argmin");
     km_argmin_kernel<<<unsigned((n + 255) / 256), 256, 0, ctx->stream>>>(D, n, k, assign, best_d2);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
@@ -118,9 +120,11 @@ int launch_km_assign(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, co
 
 int launch_km_sums(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, const int64_t* assign, int64_t k,
                    double* sums, int64_t* counts, int accumulate) {
+    EPK_PROF(ctx, "km_sums");
     km_sums_kernel<<<unsigned((k * dim + 127) / 128), 128, 0, ctx->stream>>>(pts, n, dim, assign, k, sums,
                                                                             accumulate);
     EPK_LAUNCH_CHECK(ctx);
+    EPK_PROF(ctx, "km_counts");
     km_counts_kernel<<<unsigned((k + 31) / 32), 32, 0, ctx->stream>>>(assign, n, k, counts, accumulate);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
@@ -128,6 +132,7 @@ int launch_km_sums(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, cons
 
 int launch_km_finalize(epk_ctx* ctx, const double* sums, const int64_t* counts, int64_t k, int64_t dim,
                        double* cent) {
+    EPK_PROF(ctx, "km_finalize");
     km_finalize_kernel<<<unsigned((k * dim + 255) / 256), 256, 0, ctx->stream>>>(sums, counts, k, dim, cent);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
@@ -135,6 +140,7 @@ int launch_km_finalize(epk_ctx* ctx, const double* sums, const int64_t* counts, 
 
 int launch_km_sqdist(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, const double* cent,
                      const int64_t* assign, double* d2) {
+    EPK_PROF(ctx, "km_sqdist");
     km_sqdist_assigned_kernel<<<unsigned((n + 127) / 128), 128, 0, ctx->stream>>>(pts, n, dim, cent, assign, d2);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
@@ -274,6 +280,7 @@ int launch_key_cosine(epk_ctx* ctx, const void* kf, const void* kb, int dtype, i
     int64_t* pskip = carve.take<int64_t>(np);
     int64_t* skl = carve.take<int64_t>(layers);
     dim3 g(bpl, layers);
+    EPK_PROF(ctx, "cosine_partial");
     if (dtype == EPK_F64)
         cosine_partial_kernel<double><<<g, kCosThreads, 0, ctx->stream>>>(
             static_cast<const double*>(kf), static_cast<const double*>(kb), rows, dim, bpl, psum, pcnt, pskip);
@@ -285,8 +292,10 @@ int launch_key_cosine(epk_ctx* ctx, const void* kf, const void* kb, int dtype, i
             static_cast<const __nv_bfloat16*>(kf), static_cast<const __nv_bfloat16*>(kb), rows, dim, bpl, psum,
             pcnt, pskip);
     EPK_LAUNCH_CHECK(ctx);
+    EPK_PROF(ctx, "cosine_final");
     cosine_final_kernel<<<layers, 256, 0, ctx->stream>>>(psum, pcnt, pskip, bpl, sigma, skl);
     EPK_LAUNCH_CHECK(ctx);
+    EPK_PROF(ctx, "cosine_total");
     cosine_skip_total_kernel<<<1, 32, 0, ctx->stream>>>(skl, layers, skipped);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;

@@ -230,11 +230,14 @@ int launch_score_f32(epk_ctx* ctx, const epk_cache_desc* c, const float* q, cons
         P.q = q + int64_t(l) * hq * p * d;
         P.kp = kp + int64_t(l) * H * p * d;
         dim3 g1(unsigned((stride + kT - 1) / kT), unsigned((p + kT - 1) / kT), unsigned(hq));
+        EPK_PROF(ctx, "f32_logits");
         f32_logits_kernel<<<g1, 256, 0, ctx->stream>>>(P);
         EPK_LAUNCH_CHECK(ctx);
+        EPK_PROF(ctx, "f32_rowstat");
         f32_rowstat_kernel<<<unsigned(rows), 256, rs_smem, ctx->stream>>>(P);
         EPK_LAUNCH_CHECK(ctx);
         dim3 g3(unsigned((std::max<int64_t>(n_max, 1) + 255) / 256), unsigned(H));
+        EPK_PROF(ctx, "f32_colscore");
         f32_colscore_kernel<<<g3, 256, 0, ctx->stream>>>(P);
         EPK_LAUNCH_CHECK(ctx);
     }
@@ -242,6 +245,7 @@ int launch_score_f32(epk_ctx* ctx, const epk_cache_desc* c, const float* q, cons
 }
 
 int launch_expf_probe(epk_ctx* ctx, const float* x, float* y, int64_t n) {
+    EPK_PROF(ctx, "expf_probe");
     expf_probe_kernel<<<unsigned((n + 255) / 256), 256, 0, ctx->stream>>>(x, y, n);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
@@ -307,6 +311,7 @@ int launch_score_grids(epk_ctx* ctx, int hq, int H, int p, const int64_t* head_o
     P.scores = scores;
     P.agg_max = agg_max;
     dim3 g(unsigned((std::max<int64_t>(n_max, 1) + 255) / 256), unsigned(H));
+    EPK_PROF(ctx, "grid_score");
     grid_score_kernel<<<g, 256, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;

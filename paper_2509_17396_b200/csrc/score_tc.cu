@@ -589,12 +589,15 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     }
     P.items = int64_t(P.L) * H * P.NQ * P.splits;
     int grid1 = int(std::min<int64_t>(P.items, ctx->num_sms));
+    EPK_PROF(ctx, "p1_rowstats");
     tc_rowstats_kernel<<<grid1, kThreads, smem1, ctx->stream>>>(P, tm_k, tm_q, tm_kp);
     EPK_LAUNCH_CHECK(ctx);
+    EPK_PROF(ctx, "p1_merge");
     tc_merge_kernel<<<unsigned((rows + 255) / 256), 256, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     P.items = int64_t(P.L) * H * P.tiles_max;
     int grid2 = int(std::min<int64_t>(P.items, ctx->num_sms));
+    EPK_PROF(ctx, "p2_colscore");
     tc_colscore_kernel<<<grid2, kThreads, smem2, ctx->stream>>>(P, tm_k, tm_q);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;

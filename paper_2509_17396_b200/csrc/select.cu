@@ -342,6 +342,7 @@ int launch_select(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int
     P.err_flag = ctx->err_flag;
     const int segs = per_head ? c->layers * c->kv_heads : c->layers;
     dim3 grid(segs * kSelCluster), block(kSelThreads);
+    EPK_PROF(ctx, per_head ? "select_per_head" : "select");
     if (score_dtype == EPK_F32)
         select_kernel<float><<<grid, block, 0, ctx->stream>>>(P);
     else
