@@ -207,6 +207,18 @@ int epk_key_cosine_sigma(epk_ctx* ctx, const void* k_full, const void* k_block, 
  * y[i] = epk_expf(x[i]) as the EPK-F32 v1 kernels compute it ([dev] fp32),
  * for the bitwise host/device parity test. */
 int epk_debug_expf(epk_ctx* ctx, const float* x, float* y, int64_t n);
+/* TMA streaming probe: reads rows x 128 bf16 through the scorer's K-tile
+ * producer (box_rows x 64 boxes, `stages`-deep ring, `grid` CTAs) with a
+ * trivial consumer; time it with epk_ctx_profile to size the K ring. */
+int epk_debug_tma_stream(epk_ctx* ctx, const void* k, int64_t rows, int32_t box_rows, int32_t stages,
+                         int32_t grid);
+/* tcgen05 issue-rate probe: `iters` 128 x n x 128 bf16 MMAs per SM (n = 128
+ * or 256) from resident shared memory; drain != 0 adds epilogue warps that
+ * tcgen05.ld every result before its TMEM slot is reused. */
+int epk_debug_mma_rate(epk_ctx* ctx, int32_t n, int32_t iters, int32_t drain);
+/* P1 pipeline without the softmax: TMA-streamed 256-row K stages x nq
+ * resident 128-row chunks, 128 x 256 x 128 MMAs, optional TMEM drain. */
+int epk_debug_mma_stream(epk_ctx* ctx, const void* k, int64_t rows, int32_t nq, int32_t stages, int32_t drain);
 
 #ifdef __cplusplus
 }

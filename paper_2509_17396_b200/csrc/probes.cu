@@ -1,0 +1,320 @@
+// probes.cu -- diagnostics, not on the product path:
+//   epk_debug_tma_stream: TMA streaming bandwidth of the scorer's K-tile
+//     producer with a trivial consumer (sizes the K ring);
+//   epk_debug_mma_rate: tcgen05.mma issue ceiling for 128xN bf16 tiles from
+//     resident shared memory, optionally drained by epilogue warps.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "epk_internal.cuh"
+#include "sm100.cuh"
+
+namespace epk {
+using namespace sm100;
+
+__global__ void __launch_bounds__(64, 1) tma_stream_kernel(const __grid_constant__ CUtensorMap tm, int64_t rows,
+                                                           int box_rows, int stages, unsigned* sink) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int tile_bytes = box_rows * 256;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * tile_bytes);
+    uint64_t* empty = full + stages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int64_t tiles = rows / box_rows;
+    const int64_t per = (tiles + gridDim.x - 1) / gridDim.x;
+    const int64_t t0 = blockIdx.x * per, t1 = min(tiles, t0 + per);
+    if (warp == 0 && lane == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t t = t0; t < t1; ++t) {
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_expect_tx(&full[s], tile_bytes);
+            tma_load_2d(smem + s * tile_bytes, &tm, &full[s], 0, int(t * box_rows));
+            tma_load_2d(smem + s * tile_bytes + tile_bytes / 2, &tm, &full[s], 64, int(t * box_rows));
+            if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        unsigned acc = 0;
+        for (int64_t t = t0; t < t1; ++t) {
+            mbar_wait(&full[s], ph);
+            acc += smem[s * tile_bytes + (t & 255)];
+            mbar_arrive(&empty[s]);
+            if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        if (acc == 0xFFFFFFFFu) *sink = acc;
+    }
+}
+
+int launch_tma_stream(epk_ctx* ctx, const void* base, int64_t rows, int box_rows, int stages, int grid) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    CUtensorMap m;
+    cuuint64_t dims[2] = {128, cuuint64_t(rows)};
+    cuuint64_t strides[1] = {256};
+    cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(EPK_ERR_CUDA, "tensor map");
+    const int smem = 1024 + stages * box_rows * 256 + 2 * stages * 8;
+    EPK_CUDA_CHECK(cudaFuncSetAttribute(tma_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    unsigned* sink = reinterpret_cast<unsigned*>(ctx->err_flag);
+    EPK_PROF(ctx, "tma_stream");
+    tma_stream_kernel<<<grid, 64, smem, ctx->stream>>>(m, rows, box_rows, stages, sink);
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
+// 128 x N x 128 bf16 MMAs (8 K-steps) from resident smem into a ring of
+// TMEM slots; with `drain`, 4 epilogue warps tcgen05.ld each result (64
+// columns at a time) before the slot is reused.
+template <int N>
+__global__ void __launch_bounds__(192, 1) mma_rate_kernel(int iters, int drain, unsigned* sink) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;                  // 128 x 128 bf16 (two swizzled halves)
+    uint8_t* sB = smem + 32768;          // N x 128
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + N * 256);
+    uint64_t* empty = full + 4;
+    uint32_t* holder = reinterpret_cast<uint32_t*>(empty + 4);
+    constexpr int kSlots = 512 / N;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < (32768 + N * 256) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSlots; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(holder, 512);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *holder;
+    constexpr uint32_t idesc = idesc_bf16_f32(128, N);
+    if (warp == 1 && lane == 0) {
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+        for (int it = 0; it < iters; ++it) {
+            const int s = it % kSlots;
+            const uint32_t ph = (it / kSlots) & 1;
+            if (drain) mbar_wait(&empty[s], ph ^ 1);
+            else if (it >= kSlots) mbar_wait(&full[s], ph ^ 1);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t aoff = uint32_t((kk >> 2) * 16384 + (kk & 3) * 32);
+                const uint32_t boff = uint32_t((kk >> 2) * (N * 128) + (kk & 3) * 32);
+                mma_bf16_ss(tmem + uint32_t(s * N), sdesc_k_sw128(a0 + aoff), sdesc_k_sw128(b0 + boff), idesc, kk > 0);
+            }
+            mma_commit(&full[s]);
+        }
+    } else if (warp >= 2 && drain) {
+        const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
+        float acc = 0.f;
+        for (int it = 0; it < iters; ++it) {
+            const int s = it % kSlots;
+            mbar_wait(&full[s], (it / kSlots) & 1);
+            tc_fence_after();
+            for (int c = 0; c < N; c += 64) {
+                float v[64];
+                tmem_ld64(tmem + lane_addr + uint32_t(s * N + c), v);
+                acc += v[0] + v[63];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if (acc == 12345.f) *sink = 1;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+int launch_mma_rate(epk_ctx* ctx, int n, int iters, int drain) {
+    const int smem = 1024 + 32768 + n * 256 + 128;
+    unsigned* sink = reinterpret_cast<unsigned*>(ctx->err_flag);
+    EPK_PROF(ctx, n == 256 ? "mma_rate_n256" : "mma_rate_n128");
+    if (n == 256) {
+        EPK_CUDA_CHECK(cudaFuncSetAttribute(mma_rate_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        mma_rate_kernel<256><<<ctx->num_sms, 192, smem, ctx->stream>>>(iters, drain, sink);
+    } else {
+        EPK_CUDA_CHECK(cudaFuncSetAttribute(mma_rate_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        mma_rate_kernel<128><<<ctx->num_sms, 192, smem, ctx->stream>>>(iters, drain, sink);
+    }
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
+// TMA-streamed 256-row K stages (`stages`-deep ring) feeding `nq` resident
+// 128-row A chunks: per stage nq MMAs of 128 x 256 x 128 into two TMEM slots,
+// drained by 8 epilogue warps (tcgen05.ld, no math).  The P1 pipeline
+// without its softmax epilogue.
+__global__ void __launch_bounds__(320, 1) mma_stream_kernel(const __grid_constant__ CUtensorMap tm, int64_t rows,
+                                                            int nq, int stages, int drain, unsigned* sink) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t q_half = uint32_t(nq) * 128 * 128;
+    uint8_t* sQ = smem;
+    uint8_t* sK = smem + 2 * q_half;
+    const uint32_t k_half = 256 * 128, k_stage = 2 * k_half;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sK + stages * k_stage);
+    uint64_t* empty = full + stages;
+    uint64_t* tfull = empty + stages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < int(2 * q_half / 4); i += blockDim.x) reinterpret_cast<uint32_t*>(sQ)[i] = 0x3c003c00u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 8);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(holder, 512);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *holder;
+    const int64_t tiles = rows / 256;
+    const int64_t per = (tiles + gridDim.x - 1) / gridDim.x;
+    const int64_t t0 = blockIdx.x * per, t1 = min(tiles, t0 + per);
+    if (warp == 0 && lane == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t t = t0; t < t1; ++t) {
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_expect_tx(&full[s], k_stage);
+            tma_load_2d(sK + s * k_stage, &tm, &full[s], 0, int(t * 256));
+            tma_load_2d(sK + s * k_stage + k_half, &tm, &full[s], 64, int(t * 256));
+            if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        int s = 0;
+        uint32_t ph = 0, job = 0;
+        const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK);
+        for (int64_t t = t0; t < t1; ++t) {
+            mbar_wait(&full[s], ph);
+            for (int c = 0; c < nq; ++c) {
+                const int ts = int(job & 1);
+                if (drain) mbar_wait(&tempty[ts], ((job >> 1) & 1) ^ 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t k = uint32_t((kk & 3) * 32), h = uint32_t(kk >> 2);
+                    mma_bf16_ss(tmem + uint32_t(ts * 256), sdesc_k_sw128(q0 + uint32_t(c) * 16384 + h * q_half + k),
+                                sdesc_k_sw128(k0 + uint32_t(s) * k_stage + h * k_half + k), idesc_bf16_f32(128, 256),
+                                kk > 0);
+                }
+                mma_commit(&tfull[ts]);
+                ++job;
+            }
+            mma_commit(&empty[s]);
+            if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp >= 2 && drain) {
+        const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
+        const int half = (warp - 2) >> 2;
+        float acc = 0.f;
+        uint32_t job = 0;
+        for (int64_t t = t0; t < t1; ++t)
+            for (int c = 0; c < nq; ++c, ++job) {
+                const int ts = int(job & 1);
+                mbar_wait(&tfull[ts], (job >> 1) & 1);
+                tc_fence_after();
+                for (int q4 = 0; q4 < 2; ++q4) {
+                    float v[64];
+                    tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + half * 128 + q4 * 64), v);
+                    acc += v[0] + v[63];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[ts]);
+            }
+        if (acc == 12345.f) *sink = 1;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+int launch_mma_stream(epk_ctx* ctx, const void* base, int64_t rows, int nq, int stages, int drain) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    CUtensorMap m;
+    cuuint64_t dims[2] = {128, cuuint64_t(rows)};
+    cuuint64_t strides[1] = {256};
+    cuuint32_t box[2] = {64, 256};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(EPK_ERR_CUDA, "tensor map");
+    const int smem = 1024 + 2 * nq * 128 * 128 + stages * 65536 + 256;
+    EPK_CUDA_CHECK(cudaFuncSetAttribute(mma_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    EPK_PROF(ctx, "mma_stream");
+    mma_stream_kernel<<<ctx->num_sms, 320, smem, ctx->stream>>>(m, rows, nq, stages, drain,
+                                                                reinterpret_cast<unsigned*>(ctx->err_flag));
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
+}  // namespace epk
+
+extern "C" int epk_debug_mma_stream(epk_ctx* ctx, const void* k, int64_t rows, int32_t nq, int32_t stages,
+                                    int32_t drain) {
+    return epk::launch_mma_stream(ctx, k, rows, nq, stages, drain);
+}
+
+extern "C" int epk_debug_mma_rate(epk_ctx* ctx, int32_t n, int32_t iters, int32_t drain) {
+    return epk::launch_mma_rate(ctx, n, iters, drain);
+}
+
+extern "C" int epk_debug_tma_stream(epk_ctx* ctx, const void* base, int64_t rows, int32_t box_rows, int32_t stages,
+                                    int32_t grid) {
+    return epk::launch_tma_stream(ctx, base, rows, box_rows, stages, grid);
+}

@@ -10,27 +10,31 @@
 // grid never exists in memory; K is streamed twice (P1, P2), Q stays in
 // shared memory.
 //
-// One persistent kernel template, two modes.  An ITEM is (layer, kv-head,
-// split of 8 K tiles [, query-chunk group]); the producer streams the item's
-// 128-row K tiles once (TMA, 128-byte swizzle) and, per K tile, the MMA warp
-// issues one 128x128x128 tcgen05.mma per resident 128-row query chunk:
-//   STATS (P1): D[query row][cache col] = Q_c . K_t^T  -> epilogue lanes own a
-//               query row, keep an online (max, sum exp2) -> partial (m, Z)
-//               per (row, split, warpgroup); tc_merge_kernel folds them into
+// One persistent kernel template, two modes; every MMA is 128 x 256 x 128
+// (the shape that keeps tcgen05 at ~94% of issue peak -- 128 x 128 tiles
+// saturate shared-memory operand bandwidth at ~69%, see
+// profiles/mma_rate_r01.txt):
+//   STATS (P1): A = 128-row query chunk (resident), B = 256-row K stage,
+//               D[query row][cache col] -> epilogue lanes own a query row and
+//               keep an online (max, sum exp2) per chunk -> partial (m, Z) per
+//               (row, split, column half); tc_merge_kernel folds them into
 //               lse2 = log2 sum 2^(x - m) + m.
-//   SCORE (P2): D[cache row][query row] = K_t . Q_c^T  -> epilogue lanes own a
-//               cache row, reduce max_r (x c2 - lse2[r]) across the query
-//               chunks -> one exp2 per cache row = its score.
-// TMEM: 4 accumulator slots of 128 fp32 columns; epilogue warpgroup g (4 warps,
-// one per TMEM lane quarter) owns slots {2g, 2g+1} and every other K tile, so
-// two warps per SM sub-partition overlap TMEM loads, FMA and MUFU work.
+//   SCORE (P2): A = 128-row K stage, B = two query chunks (256 query rows),
+//               D[cache row][query row] -> epilogue lanes own a cache row and
+//               reduce max_r (x c2 - lse2[r]) -> one exp2 per cache row.
+// Shared memory keeps Q as [d-half][all query rows] (128-byte swizzled rows,
+// 8-row groups 1024 B apart) so any two consecutive 128-row chunks form one
+// 256-row B operand.  TMEM: two 256-column accumulator slots.
 // Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer, warps 2-9 epilogue.  Items are dealt to CTAs in contiguous ranges,
-// so a CTA loads a head's Q once and reuses it across that head's splits.
+// issuer, warps 2-9 epilogue (warp e: TMEM lane quarter e & 3, column half
+// e >> 2 of every job).  Items = (layer, kv-head, 1024-column split [,
+// query-chunk group]) dealt to CTAs in contiguous ranges, so a CTA loads a
+// head's Q once.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "epk_internal.cuh"
 #include "sm100.cuh"
@@ -40,26 +44,25 @@ namespace epk {
 using namespace sm100;
 
 constexpr int kD = 128;
-constexpr int kTile = 128;
-constexpr int kTileBytes = kTile * kD * 2;  // 32 KB: two 16 KB swizzled d-halves
-constexpr int kHalfBytes = kTileBytes / 2;
-constexpr int kSplitTiles = 8;  // K tiles per item (1024 cache columns)
-constexpr int kQSlots = 4;      // resident query chunks (<= 512 query rows)
+constexpr int kRowB = 128;        // bytes of one d-half row (64 bf16)
+constexpr int kChunk = 128;       // query rows per chunk (MMA M in P1)
+constexpr int kSplitCols = 1024;  // cache columns per item
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr uint32_t kIdesc = idesc_bf16_f32(128, 128);
+constexpr int kMaxQRes = 4;       // resident query chunks (P1: per chunk group)
 
 enum { MODE_STATS = 0, MODE_SCORE = 1 };
 
 struct TcParams {
     LayerTable lt;
     int L, H, Hq, G, p, Gp, NQ;
-    int tiles_max;     // ceil(n_max / 128)
-    int splits;        // ceil(tiles_max / kSplitTiles)
-    int cgroups;       // STATS: query-chunk groups of <= kQSlots chunks
-    int prompt_tiles;  // ceil(p / 128)
-    int qslots;        // resident Q slots allocated in smem
+    int splits;        // ceil(n_max / 1024)
+    int cgroups;       // STATS: query-chunk groups
+    int cg_chunks;     // STATS: chunks per group
+    int krows;         // K stage rows: 256 (STATS) / 128 (SCORE)
     int kstages;       // K ring depth
+    int qcap;          // rows per d-half in the Q region
+    int resident;      // SCORE: all query chunks resident (else streamed pairs)
     const int32_t* head_off;
     const int32_t* head_len;
     float c2;       // d^-1/2 * log2(e)
@@ -71,27 +74,32 @@ struct TcParams {
     int64_t items;
 };
 
-// One 128x128x128 MMA: 8 K-steps of 16 elements (32 bytes) over the two
-// 64-element swizzled halves of each operand.
-__device__ __forceinline__ void mma_tile(uint32_t d_tmem, const uint8_t* a, const uint8_t* b) {
-    const uint32_t a0 = smem_u32(a), b0 = smem_u32(b);
+// D (+)= A * B^T over K = 128: 8 K-steps of 16 across the two 64-wide
+// d-halves.  a_half / b_half: byte distance between the operands' d-halves.
+__device__ __forceinline__ void mma_128xN(uint32_t d_tmem, uint32_t a, uint32_t a_half, uint32_t b, uint32_t b_half,
+                                          uint32_t idesc) {
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-        const uint32_t off = uint32_t((kk >> 2) * kHalfBytes + (kk & 3) * 32);
-        mma_bf16_ss(d_tmem, sdesc_k_sw128(a0 + off), sdesc_k_sw128(b0 + off), kIdesc, kk > 0 ? 1u : 0u);
+        const uint32_t k = uint32_t((kk & 3) * 32);
+        const uint32_t h = uint32_t(kk >> 2);
+        mma_bf16_ss(d_tmem, sdesc_k_sw128(a + h * a_half + k), sdesc_k_sw128(b + h * b_half + k), idesc,
+                    kk > 0 ? 1u : 0u);
     }
 }
 
-__device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int row) {
+// Loads `rows` rows (both d-halves) of a [*, 128] bf16 tensor into a
+// [d-half][rows] region whose halves are `half_bytes` apart.
+__device__ __forceinline__ void load_rows(uint8_t* dst, uint32_t half_bytes, const CUtensorMap* map, uint64_t* bar,
+                                          int row) {
     tma_load_2d(dst, map, bar, 0, row);
-    tma_load_2d(dst + kHalfBytes, map, bar, 64, row);
+    tma_load_2d(dst + half_bytes, map, bar, 64, row);
 }
 
 struct Item {
     int l, h, s, cg;
     int n_h;
-    int64_t krow0;  // first K row of the head (global)
-    int t0, nc, np;  // first cache tile, cache tiles, prompt tiles
+    int64_t krow0;   // first K row of the head (global)
+    int t0, nc, np;  // first cache tile, cache tiles, prompt tiles (tiles of krows)
     int c0, nq;      // first query chunk, chunks
     __device__ int ntiles() const { return nc + np; }
     __device__ int64_t qkey() const { return (int64_t(l) * 4096 + h) * 64 + cg; }
@@ -112,13 +120,14 @@ __device__ __forceinline__ Item decode(const TcParams& P, int64_t it) {
     x.l = int(r / P.H);
     x.n_h = P.head_len[x.l * P.H + x.h];
     x.krow0 = P.lt.base[x.l] + P.head_off[x.l * (P.H + 1) + x.h];
-    const int tiles = (x.n_h + kTile - 1) / kTile;
-    x.t0 = x.s * kSplitTiles;
-    x.nc = max(0, min(tiles, x.t0 + kSplitTiles) - x.t0);
-    x.np = (MODE == MODE_STATS && x.s == P.splits - 1) ? P.prompt_tiles : 0;
+    const int per = kSplitCols / P.krows;
+    const int tiles = (x.n_h + P.krows - 1) / P.krows;
+    x.t0 = x.s * per;
+    x.nc = max(0, min(tiles, x.t0 + per) - x.t0);
+    x.np = (MODE == MODE_STATS && x.s == P.splits - 1) ? (P.p + P.krows - 1) / P.krows : 0;
     if (MODE == MODE_STATS) {
-        x.c0 = x.cg * kQSlots;
-        x.nq = min(kQSlots, P.NQ - x.c0);
+        x.c0 = x.cg * P.cg_chunks;
+        x.nq = min(P.cg_chunks, P.NQ - x.c0);
     } else {
         x.c0 = 0;
         x.nq = P.NQ;
@@ -131,24 +140,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_score_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kp) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned (SWIZZLE_128B atoms), derived from smem_raw by pointer
+    // arithmetic so the compiler keeps shared-space (LDS/STS) addressing.
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t q_half = uint32_t(P.qcap) * kRowB;   // Q d-half stride
+    const uint32_t k_half = uint32_t(P.krows) * kRowB;  // K d-half stride
+    const uint32_t k_stage = 2 * k_half;
     uint8_t* sQ = smem;
-    uint8_t* sK = sQ + P.qslots * kTileBytes;
-    float* s_lse = reinterpret_cast<float*>(sK + P.kstages * kTileBytes);  // SCORE: 2 x NQ*128
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_lse + (MODE == MODE_SCORE ? 2 * P.NQ * kTile : 0));
+    uint8_t* sK = sQ + 2 * q_half;
+    float* s_lse = reinterpret_cast<float*>(sK + P.kstages * k_stage);     // SCORE: NQ*128 lse2
+    float* s_pair = s_lse + (MODE == MODE_SCORE ? P.NQ * kChunk : 0);     // SCORE: 128 half maxima
+    float* s_avg = s_pair + (MODE == MODE_SCORE ? kChunk : 0);            // SCORE avg: G*128 sums
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_avg + (MODE == MODE_SCORE && !P.agg_max ? P.G * kChunk : 0));
     uint64_t* k_full = bars;
     uint64_t* k_empty = k_full + P.kstages;
-    uint64_t* q_full = k_empty + P.kstages;
-    uint64_t* q_empty = q_full + kQSlots;
-    uint64_t* t_full = q_empty + kQSlots;
-    uint64_t* t_empty = t_full + 4;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 4);
+    uint64_t* q_full = k_empty + P.kstages;  // per resident chunk, or per streamed pair slot
+    uint64_t* q_empty = q_full + kMaxQRes;
+    uint64_t* t_full = q_empty + kMaxQRes;
+    uint64_t* t_empty = t_full + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t per = (P.items + gridDim.x - 1) / gridDim.x;
     const int64_t it_beg = int64_t(blockIdx.x) * per;
     const int64_t it_end = min(P.items, it_beg + per);
-    const bool resident = MODE == MODE_STATS || P.NQ <= P.qslots;
+    const bool resident = MODE == MODE_STATS || P.resident;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tm_k);
@@ -158,17 +174,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
         }
-        for (int s = 0; s < kQSlots; ++s) {
+        for (int s = 0; s < kMaxQRes; ++s) {
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
         }
-        for (int s = 0; s < 4; ++s) {
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&t_full[s], 1);
-            mbar_init(&t_empty[s], 4);
+            mbar_init(&t_empty[s], kEpiWarps);
         }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_holder, 512);
+    if (MODE == MODE_SCORE && !P.agg_max)
+        for (int i = threadIdx.x; i < P.G * kChunk; i += blockDim.x) s_avg[i] = 0.f;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -178,8 +196,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {  // ------------------------- TMA producer -------------------------
             int ks = 0;
             uint32_t kph = 0;
-            uint32_t qload[kQSlots] = {0, 0, 0, 0};
-            int64_t key = -1, qjob = 0;
+            uint32_t qload[kMaxQRes] = {0, 0, 0, 0};
+            int64_t key = -1, pj = 0;
+            const int npairs = (P.NQ + 1) / 2;
             for (int64_t it = it_beg; it < it_end; ++it) {
                 const Item x = decode<MODE>(P, it);
                 if (x.ntiles() == 0) continue;
@@ -188,29 +207,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                     key = x.qkey();
                     for (int c = 0; c < x.nq; ++c) {
                         mbar_wait(&q_empty[c], (qload[c] & 1) ^ 1);
-                        mbar_expect_tx(&q_full[c], kTileBytes);
-                        load_tile(sQ + c * kTileBytes, &tm_q, &q_full[c], qrow0 + (x.c0 + c) * kTile);
+                        mbar_expect_tx(&q_full[c], 2 * kChunk * kRowB);
+                        load_rows(sQ + c * kChunk * kRowB, q_half, &tm_q, &q_full[c], qrow0 + (x.c0 + c) * kChunk);
                         ++qload[c];
                     }
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
                     mbar_wait(&k_empty[ks], kph ^ 1);
-                    mbar_expect_tx(&k_full[ks], kTileBytes);
+                    mbar_expect_tx(&k_full[ks], k_stage);
                     if (t < x.nc)
-                        load_tile(sK + ks * kTileBytes, &tm_k, &k_full[ks], int(x.krow0 + int64_t(x.t0 + t) * kTile));
+                        load_rows(sK + ks * k_stage, k_half, &tm_k, &k_full[ks],
+                                  int(x.krow0 + int64_t(x.t0 + t) * P.krows));
                     else
-                        load_tile(sK + ks * kTileBytes, &tm_kp, &k_full[ks],
-                                  (x.l * P.H + x.h) * P.p + (t - x.nc) * kTile);
+                        load_rows(sK + ks * k_stage, k_half, &tm_kp, &k_full[ks],
+                                  (x.l * P.H + x.h) * P.p + (t - x.nc) * P.krows);
                     if (++ks == P.kstages) {
                         ks = 0;
                         kph ^= 1;
                     }
-                    if (!resident) {
-                        for (int c = 0; c < x.nq; ++c, ++qjob) {
-                            const int slot = int(qjob % P.qslots);
+                    if (!resident) {  // SCORE, streamed: query chunk pairs through 2 slots
+                        for (int j = 0; j < npairs; ++j, ++pj) {
+                            const int slot = int(pj & 1);
+                            const int nch = min(2, P.NQ - 2 * j);
                             mbar_wait(&q_empty[slot], (qload[slot] & 1) ^ 1);
-                            mbar_expect_tx(&q_full[slot], kTileBytes);
-                            load_tile(sQ + slot * kTileBytes, &tm_q, &q_full[slot], qrow0 + c * kTile);
+                            mbar_expect_tx(&q_full[slot], nch * 2 * kChunk * kRowB);
+                            for (int cc = 0; cc < nch; ++cc)
+                                load_rows(sQ + (slot * 2 + cc) * kChunk * kRowB, q_half, &tm_q, &q_full[slot],
+                                          qrow0 + (2 * j + cc) * kChunk);
                             ++qload[slot];
                         }
                     }
@@ -221,10 +244,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {  // ------------------------- MMA issuer ---------------------------
             int ks = 0;
             uint32_t kph = 0;
-            uint32_t qload[kQSlots] = {0, 0, 0, 0};
-            uint32_t gj[2] = {0, 0};
-            int64_t key = -1, qjob = 0, tcount = 0;
-            int held = 0;  // resident chunks of the current key
+            uint32_t qload[kMaxQRes] = {0, 0, 0, 0};
+            uint32_t job = 0;
+            int64_t key = -1, pj = 0;
+            int held = 0;
+            const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK);
             for (int64_t it = it_beg; it < it_end; ++it) {
                 const Item x = decode<MODE>(P, it);
                 if (x.ntiles() == 0) continue;
@@ -235,31 +259,51 @@ __global__ void __launch_bounds__(kThreads, 1)
                     held = x.nq;
                     fresh = true;
                 }
-                for (int t = 0; t < x.ntiles(); ++t, ++tcount) {
+                for (int t = 0; t < x.ntiles(); ++t) {
                     mbar_wait(&k_full[ks], kph);
-                    const int g = int(tcount & 1);
-                    for (int c = 0; c < x.nq; ++c) {
-                        int slot = c;
-                        if (!resident) {
-                            slot = int(qjob % P.qslots);
-                            ++qjob;
-                            mbar_wait(&q_full[slot], qload[slot] & 1);
-                            ++qload[slot];
-                        } else if (fresh && t == 0) {
-                            mbar_wait(&q_full[slot], qload[slot] & 1);
-                            ++qload[slot];
+                    const uint32_t kst = k0 + uint32_t(ks) * k_stage;
+                    if (MODE == MODE_STATS) {
+                        for (int c = 0; c < x.nq; ++c) {
+                            if (fresh && t == 0) {
+                                mbar_wait(&q_full[c], qload[c] & 1);
+                                ++qload[c];
+                            }
+                            const int ts = int(job & 1);
+                            mbar_wait(&t_empty[ts], ((job >> 1) & 1) ^ 1);
+                            tc_fence_after();
+                            mma_128xN(tmem + uint32_t(ts * 256), q0 + uint32_t(c * kChunk * kRowB), q_half, kst,
+                                      k_half, idesc_bf16_f32(128, 256));
+                            mma_commit(&t_full[ts]);
+                            ++job;
                         }
-                        const int ts = 2 * g + int(gj[g] & 1);
-                        mbar_wait(&t_empty[ts], ((gj[g] >> 1) & 1) ^ 1);
-                        tc_fence_after();
-                        const uint32_t d = tmem + uint32_t(ts * kTile);
-                        if (MODE == MODE_STATS)
-                            mma_tile(d, sQ + slot * kTileBytes, sK + ks * kTileBytes);
-                        else
-                            mma_tile(d, sK + ks * kTileBytes, sQ + slot * kTileBytes);
-                        mma_commit(&t_full[ts]);
-                        if (!resident) mma_commit(&q_empty[slot]);
-                        ++gj[g];
+                    } else {
+                        for (int j = 0; 2 * j < x.nq; ++j) {
+                            const int nch = min(2, x.nq - 2 * j);
+                            uint32_t qb;
+                            int slot = 0;
+                            if (resident) {
+                                if (fresh && t == 0)
+                                    for (int cc = 0; cc < nch; ++cc) {
+                                        mbar_wait(&q_full[2 * j + cc], qload[2 * j + cc] & 1);
+                                        ++qload[2 * j + cc];
+                                    }
+                                qb = q0 + uint32_t(2 * j * kChunk * kRowB);
+                            } else {
+                                slot = int(pj & 1);
+                                ++pj;
+                                mbar_wait(&q_full[slot], qload[slot] & 1);
+                                ++qload[slot];
+                                qb = q0 + uint32_t(slot * 2 * kChunk * kRowB);
+                            }
+                            const int ts = int(job & 1);
+                            mbar_wait(&t_empty[ts], ((job >> 1) & 1) ^ 1);
+                            tc_fence_after();
+                            mma_128xN(tmem + uint32_t(ts * 256), kst, k_half, qb, q_half,
+                                      idesc_bf16_f32(128, uint32_t(nch * kChunk)));
+                            mma_commit(&t_full[ts]);
+                            if (!resident) mma_commit(&q_empty[slot]);
+                            ++job;
+                        }
                     }
                     mma_commit(&k_empty[ks]);
                     if (++ks == P.kstages) {
@@ -269,49 +313,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else {  // ------------------------- epilogue warpgroups --------------------------
-        const int g = (warp - 2) >> 2;
-        const int quarter = warp & 3;
-        const int r_local = quarter * 32 + lane;  // TMEM lane owned by this thread
+    } else {  // ------------------------- epilogue (8 warps) -------------------------
+        const int e = warp - 2;
+        const int quarter = warp & 3;  // TMEM lanes this warp may read
+        const int half = e >> 2;       // column half of every job
+        const int r_local = quarter * 32 + lane;
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-        const int gtid = (warp - 2 - 4 * g) * 32 + lane;  // 0..127 within the group
-        uint32_t gj = 0;
-        int64_t tcount = 0, lkey = -1;
-        float* my_lse = s_lse + g * P.NQ * kTile;
+        const int etid = e * 32 + lane;
+        uint32_t job = 0;
+        int64_t lkey = -1;
         const float inv_p = 1.0f / float(P.p);
         for (int64_t it = it_beg; it < it_end; ++it) {
             const Item x = decode<MODE>(P, it);
             if (MODE == MODE_STATS) {
-                float m[kQSlots], z[kQSlots];
+                float m[kMaxQRes], z[kMaxQRes];
 #pragma unroll
-                for (int c = 0; c < kQSlots; ++c) {
+                for (int c = 0; c < kMaxQRes; ++c) {
                     m[c] = -INFINITY;
                     z[c] = 0.f;
                 }
-                for (int t = 0; t < x.ntiles(); ++t, ++tcount) {
-                    if (int(tcount & 1) != g) continue;
+                for (int t = 0; t < x.ntiles(); ++t) {
 #pragma unroll
-                    for (int c = 0; c < kQSlots; ++c) {
+                    for (int c = 0; c < kMaxQRes; ++c) {
                         if (c >= x.nq) break;
-                        const int rq = (x.c0 + c) * kTile + r_local;  // query row of the head (g*p + t)
-                        int lim;
+                        const int rq = (x.c0 + c) * kChunk + r_local;  // query row of the head (g*p + t)
+                        int lim;  // valid columns of this job from its first column
                         if (t < x.nc)
-                            lim = x.n_h - (x.t0 + t) * kTile;
+                            lim = x.n_h - (x.t0 + t) * P.krows;
                         else
-                            lim = min(P.p, rq % P.p + 1) - (t - x.nc) * kTile;
-                        const int ts = 2 * g + int(gj & 1);
-                        mbar_wait(&t_full[ts], (gj >> 1) & 1);
+                            lim = min(P.p, rq % P.p + 1) - (t - x.nc) * P.krows;
+                        const int ts = int(job & 1);
+                        mbar_wait(&t_full[ts], (job >> 1) & 1);
                         tc_fence_after();
 #pragma unroll 1
-                        for (int half = 0; half < 2; ++half) {
+                        for (int q4 = 0; q4 < 2; ++q4) {
+                            const int col0 = half * 128 + q4 * 64;
                             float v[64];
-                            tmem_ld64(tmem + lane_addr + uint32_t(ts * kTile + half * 64), v);
-                            if (half == 1) {  // TMEM slot free: the last values are in registers
+                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + col0), v);
+                            if (q4 == 1) {  // the slot's values are all in registers now
                                 tc_fence_before();
                                 __syncwarp();
                                 if (lane == 0) mbar_arrive(&t_empty[ts]);
                             }
-                            const int hl = lim - half * 64;
+                            const int hl = lim - col0;
                             float mx = -INFINITY;
                             if (hl >= 64) {
 #pragma unroll
@@ -341,16 +385,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 z[c] += (s0 + s1) + (s2 + s3);
                             }
                         }
-                        ++gj;
+                        ++job;
                     }
                 }
-                // partial (m, Z) of this warpgroup for each query row of the item
+                // partial (m, Z) of this column half for each query row of the item
 #pragma unroll
-                for (int cc = 0; cc < kQSlots; ++cc) {
+                for (int cc = 0; cc < kMaxQRes; ++cc) {
                     if (cc < x.nq) {
-                        const int rq = (x.c0 + cc) * kTile + r_local;
-                        const int64_t o = ((int64_t(x.l) * P.H + x.h) * (P.NQ * kTile) + rq) * (2 * P.splits) +
-                                          2 * x.s + g;
+                        const int rq = (x.c0 + cc) * kChunk + r_local;
+                        const int64_t o = ((int64_t(x.l) * P.H + x.h) * (P.NQ * kChunk) + rq) * (2 * P.splits) +
+                                          2 * x.s + half;
                         P.part_m[o] = m[cc];
                         P.part_z[o] = z[cc];
                     }
@@ -358,29 +402,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
                 if (x.ntiles() == 0) continue;
                 const int64_t hk = int64_t(x.l) * P.H + x.h;
-                for (int t = 0; t < x.ntiles(); ++t, ++tcount) {
-                    if (int(tcount & 1) != g) continue;
-                    if (hk != lkey) {  // this group's copy of the head's lse2
-                        named_bar_sync(1 + g, 128);
-                        for (int r = gtid; r < P.NQ * kTile; r += 128) my_lse[r] = P.lse2[hk * (P.NQ * kTile) + r];
-                        named_bar_sync(1 + g, 128);
-                        lkey = hk;
-                    }
-                    float best = -INFINITY, acc = 0.f;
-                    for (int c = 0; c < x.nq; ++c) {
-                        const int ts = 2 * g + int(gj & 1);
-                        mbar_wait(&t_full[ts], (gj >> 1) & 1);
+                if (hk != lkey) {  // the head's lse2 (all 8 warps)
+                    named_bar_sync(1, 32 * kEpiWarps);
+                    for (int r = etid; r < P.NQ * kChunk; r += 32 * kEpiWarps)
+                        s_lse[r] = P.lse2[hk * (P.NQ * kChunk) + r];
+                    named_bar_sync(1, 32 * kEpiWarps);
+                    lkey = hk;
+                }
+                for (int t = 0; t < x.ntiles(); ++t) {
+                    float best = -INFINITY;
+                    for (int j = 0; 2 * j < x.nq; ++j) {
+                        const int ncols = min(2, x.nq - 2 * j) * kChunk;  // query rows of the job
+                        const int hw = ncols / 2;                         // columns per warp half
+                        const int ts = int(job & 1);
+                        mbar_wait(&t_full[ts], (job >> 1) & 1);
                         tc_fence_after();
 #pragma unroll 1
-                        for (int half = 0; half < 2; ++half) {
+                        for (int q4 = 0; q4 * 64 < hw; ++q4) {
+                            const int col0 = half * hw + q4 * 64;
                             float v[64];
-                            tmem_ld64(tmem + lane_addr + uint32_t(ts * kTile + half * 64), v);
-                            if (half == 1) {
+                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + col0), v);
+                            if ((q4 + 1) * 64 >= hw) {
                                 tc_fence_before();
                                 __syncwarp();
                                 if (lane == 0) mbar_arrive(&t_empty[ts]);
                             }
-                            const float* lse = my_lse + c * kTile + half * 64;
+                            const int r0 = 2 * j * kChunk + col0;  // first query row of these 64 columns
+                            const float* lse = s_lse + r0;
                             if (P.agg_max) {
                                 float b0 = best, b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
 #pragma unroll
@@ -393,23 +441,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                                 best = fmaxf(fmaxf(b0, b1), fmaxf(b2, b3));
                             } else {
+                                // window sums per query head g, both halves add in smem
+                                float acc = 0.f;
+                                int gcur = r0 / P.p;
 #pragma unroll
                                 for (int i = 0; i < 64; ++i) {
-                                    const int rq = c * kTile + half * 64 + i;
-                                    if (rq < P.Gp) {  // pad rows have lse2 = +inf -> exp2 = 0
-                                        acc += ex2(fmaf(v[i], P.c2, -lse[i]));
-                                        if (rq % P.p == P.p - 1) {
-                                            best = fmaxf(best, acc * inv_p);
+                                    const int rq = r0 + i;
+                                    if (rq < P.Gp) {
+                                        const int gg = rq / P.p;
+                                        if (gg != gcur) {
+                                            atomicAdd(&s_avg[gcur * kChunk + r_local], acc);
                                             acc = 0.f;
+                                            gcur = gg;
                                         }
+                                        acc += ex2(fmaf(v[i], P.c2, -lse[i]));
                                     }
                                 }
+                                if (gcur < P.G) atomicAdd(&s_avg[gcur * kChunk + r_local], acc);
                             }
                         }
-                        ++gj;
+                        ++job;
                     }
-                    const int j = (x.t0 + t) * kTile + r_local;
-                    if (j < x.n_h) P.scores[x.krow0 + j] = P.agg_max ? ex2(best) : best;
+                    // combine the two column halves of each cache row
+                    const int jrow = (x.t0 + t) * P.krows + r_local;
+                    if (P.agg_max) {
+                        if (half == 1) s_pair[r_local] = best;
+                        named_bar_sync(2 + quarter, 64);
+                        if (half == 0 && jrow < x.n_h) P.scores[x.krow0 + jrow] = ex2(fmaxf(best, s_pair[r_local]));
+                        named_bar_sync(2 + quarter, 64);
+                    } else {
+                        named_bar_sync(2 + quarter, 64);
+                        if (half == 0) {
+                            float b = -INFINITY;
+                            for (int gg = 0; gg < P.G; ++gg) {
+                                b = fmaxf(b, s_avg[gg * kChunk + r_local] * inv_p);
+                                s_avg[gg * kChunk + r_local] = 0.f;
+                            }
+                            if (jrow < x.n_h) P.scores[x.krow0 + jrow] = b;
+                        }
+                        named_bar_sync(2 + quarter, 64);
+                    }
                 }
             }
         }
@@ -423,9 +494,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // lse2 per query row = log2 sum_s Z_s 2^(m_s - M) + M over the partials.
 __global__ void tc_merge_kernel(const __grid_constant__ TcParams P) {
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t rows = int64_t(P.L) * P.H * P.NQ * kTile;
+    const int64_t rows = int64_t(P.L) * P.H * P.NQ * kChunk;
     if (idx >= rows) return;
-    const int rq = int(idx % (P.NQ * kTile));
+    const int rq = int(idx % (P.NQ * kChunk));
     if (rq >= P.Gp) {
         P.lse2[idx] = INFINITY;
         return;
@@ -457,12 +528,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-static int make_map(CUtensorMap* m, const void* base, int64_t rows) {
+static int make_map(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
     auto enc = get_encode();
     if (!enc) return fail(EPK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {cuuint64_t(kD), cuuint64_t(std::max<int64_t>(rows, 1))};
     cuuint64_t strides[1] = {cuuint64_t(kD * 2)};
-    cuuint32_t box[2] = {64, cuuint32_t(kTile)};
+    cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
     cuuint32_t es[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -472,20 +543,9 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows) {
 }
 
 static int smem_bytes(const TcParams& P, int mode) {
-    return 1024 + (P.qslots + P.kstages) * kTileBytes + (mode == MODE_SCORE ? 2 * P.NQ * kTile * 4 : 0) +
-           (2 * P.kstages + 2 * kQSlots + 8) * 8 + 16;
-}
-
-static void fit_stages(TcParams& P, int mode, int limit) {
-    P.qslots = std::min(P.NQ, kQSlots);
-    P.kstages = 2;
-    while (P.kstages < 4) {
-        ++P.kstages;
-        if (smem_bytes(P, mode) > limit) {
-            --P.kstages;
-            break;
-        }
-    }
+    return 1024 + 2 * P.qcap * kRowB + P.kstages * 2 * P.krows * kRowB +
+           (mode == MODE_SCORE ? (P.NQ + 1 + (P.agg_max ? 0 : P.G)) * kChunk * 4 : 0) +
+           (2 * P.kstages + 2 * kMaxQRes + 4) * 8 + 16;
 }
 
 int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const void* kp, int hq, int p, int agg_max,
@@ -494,6 +554,7 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     if (c->head_dim != kD) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): head_dim must be 128");
     const int H = c->kv_heads;
     if (hq % H != 0) return fail(EPK_ERR_DIM, "score_with_prompt: attention grid shape mismatch");
+    if (p > 256) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): prompt_len must be <= 256");
     TcParams P;
     int rc = make_layer_table(c, &P.lt);
     if (rc) return rc;
@@ -503,29 +564,21 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     P.G = hq / H;
     P.p = p;
     P.Gp = P.G * p;
-    P.NQ = (P.Gp + kTile - 1) / kTile;
+    P.NQ = (P.Gp + kChunk - 1) / kChunk;
     if (P.NQ > 16) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): group*prompt_len must be <= 2048");
-    P.tiles_max = int(std::max<int64_t>(1, (n_max + kTile - 1) / kTile));
-    P.splits = (P.tiles_max + kSplitTiles - 1) / kSplitTiles;
-    P.cgroups = (P.NQ + kQSlots - 1) / kQSlots;
-    P.prompt_tiles = (p + kTile - 1) / kTile;
+    P.splits = int(std::max<int64_t>(1, (n_max + kSplitCols - 1) / kSplitCols));
     P.head_off = c->head_off;
     P.head_len = c->head_len;
     P.c2 = float((1.0 / std::sqrt(double(kD))) * 1.4426950408889634);
     P.scores = scores;
     P.agg_max = agg_max;
-    const int64_t rows = int64_t(P.L) * H * P.NQ * kTile;
+    const int64_t rows = int64_t(P.L) * H * P.NQ * kChunk;
     rc = ws_require(ctx, rows * 2 * P.splits * 8 + rows * 4 + 4096);
     if (rc) return rc;
     WsCarver carve(ctx->ws);
     P.part_m = carve.take<float>(rows * 2 * P.splits);
     P.part_z = carve.take<float>(rows * 2 * P.splits);
     P.lse2 = carve.take<float>(rows);
-
-    CUtensorMap tm_k, tm_q, tm_kp;
-    if ((rc = make_map(&tm_k, c->k, c->layer_base[c->layers]))) return rc;
-    if ((rc = make_map(&tm_q, q, int64_t(P.L) * hq * p))) return rc;
-    if ((rc = make_map(&tm_kp, kp, int64_t(P.L) * H * p))) return rc;
 
     // Dynamic shared memory limit: the per-block opt-in maximum minus the
     // kernel's static/reserved shared memory.
@@ -542,22 +595,62 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
         EPK_CUDA_CHECK(cudaFuncSetAttribute(tc_score_kernel<MODE_SCORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             limit));
     }
-    // P1: query-chunk groups of <= 4 resident chunks, K ring fills the rest.
-    fit_stages(P, MODE_STATS, limit);
+
+    CUtensorMap tm_k1, tm_k2, tm_q, tm_kp;
+    if ((rc = make_map(&tm_k1, c->k, c->layer_base[c->layers], 256))) return rc;
+    if ((rc = make_map(&tm_k2, c->k, c->layer_base[c->layers], 128))) return rc;
+    if ((rc = make_map(&tm_q, q, int64_t(P.L) * hq * p, kChunk))) return rc;
+    if ((rc = make_map(&tm_kp, kp, int64_t(P.L) * H * p, 256))) return rc;
+
+    // P1: 256-row K stages; query chunks in groups sized so two stages fit.
+    P.krows = 256;
+    P.resident = 1;
+    P.cg_chunks = std::min(P.NQ, kMaxQRes);
+    for (;;) {
+        P.qcap = P.cg_chunks * kChunk;
+        P.kstages = 2;
+        if (smem_bytes(P, MODE_STATS) <= limit || P.cg_chunks == 1) break;
+        --P.cg_chunks;
+    }
+    while (P.kstages < 4) {
+        ++P.kstages;
+        if (smem_bytes(P, MODE_STATS) > limit) {
+            --P.kstages;
+            break;
+        }
+    }
+    if (smem_bytes(P, MODE_STATS) > limit) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
+    P.cgroups = (P.NQ + P.cg_chunks - 1) / P.cg_chunks;
     P.items = int64_t(P.L) * H * P.splits * P.cgroups;
     const int grid1 = int(std::min<int64_t>(P.items, ctx->num_sms));
     EPK_PROF(ctx, "p1_rowstats");
-    tc_score_kernel<MODE_STATS><<<grid1, kThreads, smem_bytes(P, MODE_STATS), ctx->stream>>>(P, tm_k, tm_q, tm_kp);
+    tc_score_kernel<MODE_STATS><<<grid1, kThreads, smem_bytes(P, MODE_STATS), ctx->stream>>>(P, tm_k1, tm_q, tm_kp);
     EPK_LAUNCH_CHECK(ctx);
     EPK_PROF(ctx, "p1_merge");
     tc_merge_kernel<<<unsigned((rows + 255) / 256), 256, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
-    // P2: all query chunks resident when they fit, else streamed through 4 slots.
-    fit_stages(P, MODE_SCORE, limit);
+
+    // P2: 128-row K stages; all query chunks resident when they fit, else
+    // streamed as chunk pairs through two 256-row slots.
+    P.krows = 128;
+    P.resident = P.NQ <= kMaxQRes;
+    P.qcap = P.resident ? P.NQ * kChunk : 4 * kChunk;
+    P.kstages = 1;
+    while (P.kstages < 4) {
+        ++P.kstages;
+        if (smem_bytes(P, MODE_SCORE) > limit) {
+            --P.kstages;
+            break;
+        }
+    }
+    if (P.kstages < 2 || smem_bytes(P, MODE_SCORE) > limit)
+        return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
+    P.cgroups = 1;
+    P.cg_chunks = P.NQ;
     P.items = int64_t(P.L) * H * P.splits;
     const int grid2 = int(std::min<int64_t>(P.items, ctx->num_sms));
     EPK_PROF(ctx, "p2_colscore");
-    tc_score_kernel<MODE_SCORE><<<grid2, kThreads, smem_bytes(P, MODE_SCORE), ctx->stream>>>(P, tm_k, tm_q, tm_kp);
+    tc_score_kernel<MODE_SCORE><<<grid2, kThreads, smem_bytes(P, MODE_SCORE), ctx->stream>>>(P, tm_k2, tm_q, tm_kp);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }
