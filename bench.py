@@ -155,6 +155,7 @@ def run_ours(args, c, rank, world, device, torch, dist):
     from paper_2509_17396_b200.step import StepPlan, evict_step
 
     ctx = epk.default_context(device.index)
+    ctx.set_option(layer_group=args.layer_group, overlap=not args.no_overlap)
     n_h, live, keep = step_sizes(c)
     R = 3
     caches, qs, kps, out = make_inputs(epk, torch, c, R, device, 1234 + rank)
@@ -412,6 +413,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layer-group", type=int, default=0, help="layers per step group (0 = auto, L2-sized)")
+    ap.add_argument("--no-overlap", action="store_true", help="compaction on the main stream")
     args = ap.parse_args()
     c = CONFIGS[args.config]
 

@@ -100,6 +100,15 @@ int epk_ctx_poll_error(epk_ctx* ctx);
 const char* epk_last_error(void);
 const char* epk_status_string(int status);
 int epk_version(void);
+/* Options for epk_evict_step:
+ *   EPK_OPT_LAYER_GROUP  layers scored/selected/compacted per group (0 = auto:
+ *                        the largest group whose K fits in ~40 MB of L2, so
+ *                        the second scoring pass re-reads K from L2)
+ *   EPK_OPT_OVERLAP      1 (default): each group's compaction runs on a second
+ *                        stream, overlapping the next group's scoring */
+#define EPK_OPT_LAYER_GROUP 1
+#define EPK_OPT_OVERLAP 2
+int epk_ctx_set_option(epk_ctx* ctx, int32_t option, int64_t value);
 /* Number of kernels this library launched on the context since creation. */
 int64_t epk_ctx_launch_count(epk_ctx* ctx);
 /* Live per-kernel timing: while enabled, every kernel launch is bracketed by

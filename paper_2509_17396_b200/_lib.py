@@ -52,6 +52,7 @@ _SIGS = {
     "epk_version": (C.c_int, []),
     "epk_ctx_launch_count": (i64, [vp]),
     "epk_ctx_profile": (C.c_int, [vp, i32]),
+    "epk_ctx_set_option": (C.c_int, [vp, i32, i64]),
     "epk_ctx_profile_read": (i64, [vp, i64, C.c_char_p, C.POINTER(C.c_float)]),
     "epk_score": (C.c_int, [vp, C.POINTER(CacheDesc), vp, vp, i32, i32, i32, i32, i64, vp]),
     "epk_score_grids": (C.c_int, [vp, i32, i32, i32, vp, vp, i32, vp]),

@@ -7,21 +7,24 @@
 // block's append_to_cache (toymodel.hpp:428-443) lands in place without
 // moving the cache again.
 //
-// Three launches per call:
-//   count   (layer, chunk) CTAs count kept rows per 2048-row chunk;
-//   plan    one CTA per layer scans the chunk counts and derives the per-head
-//           kept totals -> the output head_off / head_len;
-//   gather  (layer, chunk) CTAs recompute their in-chunk exclusive prefix and
-//           copy K, V (16-byte vectors, 4 in flight per thread) and positions.
+// Three launches per call, all free of shared memory so their small CTAs can
+// co-reside on an SM with a scorer CTA of the next layer group (the step
+// overlaps HBM-bound compaction with tensor/SFU-bound scoring):
+//   count   one warp per 256-row chunk: kept rows in the chunk;
+//   plan    one CTA per layer: exclusive scan of the chunk counts and the kept
+//           count in front of every head region -> output head_off/head_len;
+//   gather  one warp per 256-row chunk: ballot prefix per 32 rows, then
+//           16-byte vector copies of K and V (8 in flight per lane) and the
+//           positions.
+// keep[] must be 0 on gap rows (both select modes guarantee it).
 #include <algorithm>
 
 #include "epk_internal.cuh"
 
 namespace epk {
 
-constexpr int kChunkRows = 2048;
-constexpr int kCompactThreads = 256;
-constexpr int kMaxHeadsC = 64;
+constexpr int kChunkRows = 256;   // rows per warp chunk
+constexpr int kWarpsPerCta = 4;
 
 struct CompactParams {
     LayerTable in_lt;
@@ -48,101 +51,80 @@ struct CompactParams {
 
 __device__ __forceinline__ int head_of_row(const int32_t* off, int H, int64_t r) {
     int lo = 0, hi = H - 1;
-    while (lo < hi) {
+    while (lo < hi) {  // last h with off[h] <= r
         const int mid = (lo + hi + 1) >> 1;
-        if (off[mid] <= r) lo = mid; else hi = mid - 1;
+        if (__ldg(off + mid) <= r) lo = mid; else hi = mid - 1;
     }
     return lo;
 }
 
-template <int NT>
-__device__ __forceinline__ int block_sum(int v, int* red) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    int t = 0;
-    for (int w = 0; w < NT / 32; ++w) t += red[w];
-    return t;
-}
-
-__global__ void __launch_bounds__(kCompactThreads) compact_count_kernel(const __grid_constant__ CompactParams P) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta) compact_count_kernel(const __grid_constant__ CompactParams P) {
     const int layer = blockIdx.y;
-    const int chunk = blockIdx.x;
-    __shared__ int32_t s_off[kMaxHeadsC + 1];
-    __shared__ int32_t s_len[kMaxHeadsC];
-    __shared__ int s_red[kCompactThreads / 32];
-    const int H = P.H;
-    for (int i = threadIdx.x; i <= H; i += blockDim.x) s_off[i] = P.in_off[layer * (H + 1) + i];
-    for (int i = threadIdx.x; i < H; i += blockDim.x) s_len[i] = P.in_len[layer * H + i];
-    __syncthreads();
-    const int64_t rows = s_off[H];
+    const int chunk = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (chunk >= P.max_chunks) return;
+    const int64_t rows = P.in_off[layer * (P.H + 1) + P.H];
     const int64_t r0 = int64_t(chunk) * kChunkRows;
-    if (r0 >= rows) {
-        if (threadIdx.x == 0) P.chunk_cnt[layer * P.max_chunks + chunk] = 0;
-        return;
-    }
-    const int64_t base = P.in_lt.base[layer];
     int c = 0;
-    for (int i = threadIdx.x; i < kChunkRows; i += blockDim.x) {
-        const int64_t r = r0 + i;
-        if (r < rows) {
-            const int h = head_of_row(s_off, H, r);
-            if (r - s_off[h] < s_len[h] && P.keep[base + r]) ++c;
+    if (r0 < rows) {
+        const uint8_t* kp = P.keep + P.in_lt.base[layer];
+#pragma unroll
+        for (int i = 0; i < kChunkRows / 32; ++i) {
+            const int64_t r = r0 + i * 32 + lane;
+            c += (r < rows && kp[r]) ? 1 : 0;
         }
     }
-    c = block_sum<kCompactThreads>(c, s_red);
-    if (threadIdx.x == 0) P.chunk_cnt[layer * P.max_chunks + chunk] = c;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) P.chunk_cnt[layer * P.max_chunks + chunk] = c;
 }
 
 // One CTA per layer: exclusive scan of the chunk counts, then the kept count
-// in front of every head-region start -> output head offsets.
-__global__ void __launch_bounds__(1024) compact_plan_kernel(const __grid_constant__ CompactParams P) {
+// in front of every head-region start -> output head offsets and lengths.
+__global__ void __launch_bounds__(256) compact_plan_kernel(const __grid_constant__ CompactParams P) {
     const int layer = blockIdx.x;
     const int H = P.H;
-    __shared__ int32_t s_off[kMaxHeadsC + 1];
-    __shared__ int32_t s_len[kMaxHeadsC];
-    __shared__ int s_red[32];
-    __shared__ int64_t s_head_prefix[kMaxHeadsC + 1];
-    for (int i = threadIdx.x; i <= H; i += blockDim.x) s_off[i] = P.in_off[layer * (H + 1) + i];
-    for (int i = threadIdx.x; i < H; i += blockDim.x) s_len[i] = P.in_len[layer * H + i];
-    __syncthreads();
-    const int64_t rows = s_off[H];
+    __shared__ int32_t s_warp[8];
+    __shared__ int64_t s_head_prefix[65];
+    const int32_t* off = P.in_off + layer * (H + 1);
+    const int64_t rows = off[H];
     const int nchunks = int((rows + kChunkRows - 1) / kChunkRows);
     const int32_t* cnt = P.chunk_cnt + layer * P.max_chunks;
     int32_t* pre = P.chunk_prefix + layer * P.max_chunks;
-    if (threadIdx.x == 0) {
-        int32_t run = 0;
-        for (int c = 0; c < nchunks; ++c) {
-            pre[c] = run;
-            run += cnt[c];
-        }
+    // block-wide exclusive scan, each thread owns a contiguous run of chunks
+    const int per = (nchunks + blockDim.x - 1) / blockDim.x;
+    const int c0 = threadIdx.x * per, c1 = min(nchunks, c0 + per);
+    int32_t mine = 0;
+    for (int c = c0; c < c1; ++c) mine += cnt[c];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int32_t run = incl - mine;
+    for (int w = 0; w < warp; ++w) run += s_warp[w];
+    for (int c = c0; c < c1; ++c) {
+        pre[c] = run;
+        run += cnt[c];
     }
     __syncthreads();
-    const int64_t base = P.in_lt.base[layer];
-    // kept rows before row x = pre[x / chunk] + kept in [chunk start, x)
-    for (int h = 0; h <= H; ++h) {
-        const int64_t x = s_off[h];
+    const uint8_t* kp = P.keep + P.in_lt.base[layer];
+    for (int h = threadIdx.x; h <= H; h += blockDim.x) {
+        const int64_t x = off[h];
         const int64_t c = x / kChunkRows;
-        int part = 0;
-        for (int64_t r = c * kChunkRows + threadIdx.x; r < x; r += blockDim.x) {
-            const int hh = head_of_row(s_off, H, r);
-            if (r - s_off[hh] < s_len[hh] && P.keep[base + r]) ++part;
+        int64_t v;
+        if (c >= nchunks) {
+            v = int64_t(pre[nchunks - 1]) + cnt[nchunks - 1];
+            if (nchunks == 0) v = 0;
+        } else {
+            v = pre[c];
+            for (int64_t r = c * kChunkRows; r < x; ++r) v += kp[r] ? 1 : 0;
         }
-        part = block_sum<1024>(part, s_red);
-        if (threadIdx.x == 0) {
-            const int64_t before = (c < nchunks ? int64_t(P.chunk_prefix[layer * P.max_chunks + c]) : 0) + part;
-            // x == rows may sit past the last chunk start: count everything.
-            int64_t v = before;
-            if (c >= nchunks) {
-                v = 0;
-                for (int cc = 0; cc < nchunks; ++cc) v += cnt[cc];
-            }
-            s_head_prefix[h] = v;
-        }
-        __syncthreads();
+        s_head_prefix[h] = v;
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
         const int64_t cap = P.out_lt.base[layer + 1] - P.out_lt.base[layer];
         const int64_t need = s_head_prefix[H] + int64_t(P.slack) * H;
@@ -155,104 +137,73 @@ __global__ void __launch_bounds__(1024) compact_plan_kernel(const __grid_constan
     }
 }
 
-__global__ void __launch_bounds__(kCompactThreads) compact_gather_kernel(const __grid_constant__ CompactParams P) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta) compact_gather_kernel(const __grid_constant__ CompactParams P) {
     const int layer = blockIdx.y;
-    const int chunk = blockIdx.x;
-    const int H = P.H;
-    __shared__ int32_t s_off[kMaxHeadsC + 1];
-    __shared__ int32_t s_len[kMaxHeadsC];
-    __shared__ int32_t s_src[kChunkRows];  // in-layer source row
-    __shared__ int32_t s_dst[kChunkRows];  // out-layer destination row
-    __shared__ int s_warp[kCompactThreads / 32];
-    for (int i = threadIdx.x; i <= H; i += blockDim.x) s_off[i] = P.in_off[layer * (H + 1) + i];
-    for (int i = threadIdx.x; i < H; i += blockDim.x) s_len[i] = P.in_len[layer * H + i];
-    __syncthreads();
-    const int64_t rows = s_off[H];
+    const int chunk = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (chunk >= P.max_chunks) return;
+    const int32_t* off = P.in_off + layer * (P.H + 1);
+    const int64_t rows = off[P.H];
     const int64_t r0 = int64_t(chunk) * kChunkRows;
     if (r0 >= rows) return;
     const int64_t in_base = P.in_lt.base[layer];
     const int64_t out_base = P.out_lt.base[layer];
-    const int32_t chunk_pre = P.chunk_prefix[layer * P.max_chunks + chunk];
-
-    // Each thread owns 8 consecutive rows of the chunk.
-    constexpr int kPer = kChunkRows / kCompactThreads;
-    uint32_t bits = 0;
-    int hs[kPer];
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-        const int64_t r = r0 + threadIdx.x * kPer + i;
-        hs[i] = 0;
-        if (r < rows) {
-            const int h = head_of_row(s_off, H, r);
-            hs[i] = h;
-            if (r - s_off[h] < s_len[h] && P.keep[in_base + r]) bits |= 1u << i;
-        }
-    }
-    const int mine = __popc(bits);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int incl = mine;
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    int warp_pre = 0;
-    for (int w = 0; w < warp; ++w) warp_pre += s_warp[w];
-    int total = 0;
-    for (int w = 0; w < kCompactThreads / 32; ++w) total += s_warp[w];
-    int slot = warp_pre + incl - mine;
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-        if (bits & (1u << i)) {
-            const int64_t r = r0 + threadIdx.x * kPer + i;
-            s_src[slot] = int32_t(r);
-            s_dst[slot] = chunk_pre + slot + P.slack * hs[i];
-            ++slot;
-        }
-    }
-    __syncthreads();
-
-    // Positions.
-    for (int j = threadIdx.x; j < total; j += blockDim.x)
-        P.out_pos[out_base + s_dst[j]] = P.in_pos[in_base + s_src[j]];
-
-    // K and V rows: flattened (row, 16-byte column) loop, 4 vectors in flight.
+    const uint8_t* kp = P.keep + in_base;
+    int32_t run = P.chunk_prefix[layer * P.max_chunks + chunk];
     const int rv = P.row_vec;
-    const int64_t nvec = int64_t(total) * rv;
-    constexpr int U = 4;
-    for (int64_t v0 = threadIdx.x; v0 < nvec; v0 += int64_t(blockDim.x) * U) {
-        uint4 ka[U], va[U];
-        int64_t dst[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t v = v0 + int64_t(u) * blockDim.x;
-            if (v < nvec) {
-                const int j = int(v / rv), c = int(v % rv);
-                const int64_t src = (in_base + s_src[j]) * rv + c;
-                dst[u] = (out_base + s_dst[j]) * rv + c;
-                ka[u] = __ldcs(P.in_k + src);
-                va[u] = __ldcs(P.in_v + src);
-            } else {
-                dst[u] = -1;
-            }
+    const int hl = lane >> 4, cl = lane & 15;
+    for (int sc = 0; sc < kChunkRows / 32; ++sc) {
+        const int64_t rs = r0 + sc * 32;
+        if (rs >= rows) break;
+        const int64_t r = rs + lane;
+        const bool k = r < rows && kp[r];
+        const unsigned bal = __ballot_sync(0xffffffffu, k);
+        if (bal == 0) continue;
+        int64_t dst = 0;
+        if (k) {
+            dst = out_base + run + __popc(bal & ((1u << lane) - 1u));
+            if (P.slack) dst += int64_t(P.slack) * head_of_row(off, P.H, r);
+            P.out_pos[dst] = P.in_pos[in_base + r];
         }
+        run += __popc(bal);
+        // copy the kept rows: a half-warp per row, 4 rows per half-warp in flight
+        for (int k0 = 0; k0 < 32; k0 += 8) {
+            uint4 kv[4], vv[4];
+            int64_t dsts[4];
+            bool ok[4];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (dst[u] >= 0) {
-                __stcs(P.out_k + dst[u], ka[u]);
-                __stcs(P.out_v + dst[u], va[u]);
+            for (int u = 0; u < 4; ++u) {
+                const int idx = k0 + 2 * u + hl;
+                ok[u] = (bal >> idx) & 1u;
+                dsts[u] = __shfl_sync(0xffffffffu, dst, idx);
+            }
+            for (int c = cl; c < rv; c += 16) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (ok[u]) {
+                        const int64_t src = (in_base + rs + k0 + 2 * u + hl) * rv + c;
+                        kv[u] = __ldcs(P.in_k + src);
+                        vv[u] = __ldcs(P.in_v + src);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (ok[u]) {
+                        __stcs(P.out_k + dsts[u] * rv + c, kv[u]);
+                        __stcs(P.out_v + dsts[u] * rv + c, vv[u]);
+                    }
+                }
             }
         }
     }
 }
 
-int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out,
-                   const uint8_t* keep, int slack) {
+int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const uint8_t* keep,
+                   int slack) {
     if (in->layers != out->layers || in->kv_heads != out->kv_heads || in->head_dim != out->head_dim ||
         in->dtype != out->dtype)
         return fail(EPK_ERR_DIM, "compact: in/out cache shapes differ");
-    if (in->kv_heads > kMaxHeadsC) return fail(EPK_ERR_UNSUPPORTED, "compact: more than 64 kv heads");
+    if (in->kv_heads > 64) return fail(EPK_ERR_UNSUPPORTED, "compact: more than 64 kv heads");
     const int64_t row_bytes = int64_t(in->head_dim) * dtype_size(in->dtype);
     if (row_bytes % 16 != 0) return fail(EPK_ERR_UNSUPPORTED, "compact: row bytes must be a multiple of 16");
     if (slack < 0) return fail(EPK_ERR_ARG, "compact: negative slack");
@@ -280,20 +231,20 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     P.out_len = out->head_len;
     P.err_flag = ctx->err_flag;
     const int64_t ws = 2 * int64_t(in->layers) * P.max_chunks * 4 + 1024;
-    rc = ws_require(ctx, ws);
+    rc = ws2_require(ctx, ws);
     if (rc) return rc;
-    WsCarver carve(ctx->ws);
+    WsCarver carve(ctx->ws2);
     P.chunk_cnt = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
     P.chunk_prefix = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
-    dim3 grid(P.max_chunks, in->layers);
+    dim3 grid((P.max_chunks + kWarpsPerCta - 1) / kWarpsPerCta, in->layers);
     EPK_PROF(ctx, "compact_count");
-    compact_count_kernel<<<grid, kCompactThreads, 0, ctx->stream>>>(P);
+    compact_count_kernel<<<grid, 32 * kWarpsPerCta, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     EPK_PROF(ctx, "compact_plan");
-    compact_plan_kernel<<<in->layers, 1024, 0, ctx->stream>>>(P);
+    compact_plan_kernel<<<in->layers, 256, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     EPK_PROF(ctx, "compact_gather");
-    compact_gather_kernel<<<grid, kCompactThreads, 0, ctx->stream>>>(P);
+    compact_gather_kernel<<<grid, 32 * kWarpsPerCta, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }

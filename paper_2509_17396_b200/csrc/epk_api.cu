@@ -2,6 +2,7 @@
 // workspace, and the host orchestration that must stay on the host (the
 // k-means++ seeding and empty-cluster repair consume the reference RNG
 // stream, clustering.hpp:158-191,213-232).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -68,6 +69,24 @@ static void prof_clear(epk_ctx* ctx) {
         cudaEventDestroy(r.stop);
     }
     ctx->prof.clear();
+}
+
+int ws2_require(epk_ctx* ctx, int64_t bytes) {
+    if (bytes <= ctx->ws2_bytes) return EPK_OK;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (ctx->stream) cudaStreamIsCapturing(ctx->stream, &st);
+    if (st != cudaStreamCaptureStatusNone)
+        return fail(EPK_ERR_ARG, "workspace must be reserved (run one step) before graph capture");
+    if (ctx->ws2) {
+        EPK_CUDA_CHECK(cudaDeviceSynchronize());
+        EPK_CUDA_CHECK(cudaFree(ctx->ws2));
+        ctx->ws2 = nullptr;
+        ctx->ws2_bytes = 0;
+    }
+    const int64_t grow = align_up(bytes + bytes / 4, 1 << 20);
+    EPK_CUDA_CHECK(cudaMalloc(&ctx->ws2, size_t(grow)));
+    ctx->ws2_bytes = grow;
+    return EPK_OK;
 }
 
 int make_layer_table(const epk_cache_desc* c, LayerTable* t) {
@@ -183,6 +202,13 @@ int epk_ctx_destroy(epk_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
     prof_clear(ctx);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->ws2) cudaFree(ctx->ws2);
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->step_buf) cudaFree(ctx->step_buf);
     if (ctx->err_flag) cudaFree(ctx->err_flag);
@@ -319,6 +345,30 @@ int epk_append(epk_ctx* ctx, const epk_cache_desc* c, const void* k_new, const v
     return launch_append(ctx, c, k_new, v_new, positions, len);
 }
 
+int epk_ctx_set_option(epk_ctx* ctx, int32_t option, int64_t value) {
+    if (!ctx) return fail(EPK_ERR_ARG, "null context");
+    switch (option) {
+        case EPK_OPT_LAYER_GROUP:
+            if (value < 0) return fail(EPK_ERR_ARG, "layer group must be >= 0");
+            ctx->layer_group = int(value);
+            return EPK_OK;
+        case EPK_OPT_OVERLAP:
+            ctx->overlap = value != 0;
+            return EPK_OK;
+        default:
+            return fail(EPK_ERR_ARG, "unknown option");
+    }
+}
+
+static epk_cache_desc layer_view(const epk_cache_desc* c, int l0, int l1) {
+    epk_cache_desc v = *c;
+    v.layers = l1 - l0;
+    v.head_off = c->head_off + int64_t(l0) * (c->kv_heads + 1);
+    v.head_len = c->head_len + int64_t(l0) * c->kv_heads;
+    v.layer_base = c->layer_base + l0;
+    return v;
+}
+
 int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const void* q,
                    const void* kp, int32_t q_heads, int32_t prompt_len, const int64_t* budgets, const int32_t* pins,
                    int32_t n_pins, int32_t aggregation, int32_t mode, int64_t n_max, int32_t out_slack,
@@ -326,18 +376,18 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     int rc = check_ctx(ctx);
     if (rc) return rc;
     if ((rc = check_cache(in)) || (rc = check_cache(out))) return rc;
+    if (in->layers != out->layers) return fail(EPK_ERR_DIM, "evict_step: in/out layer counts differ");
     const int64_t rows = in->layer_base[in->layers];
-    // Workspace layout: [scores f32 rows][keep u8 rows] then the kernels' own
-    // scratch (they carve from the start, so give them a separate region).
-    float* scores = scores_ws;
-    uint8_t* keep = nullptr;
     // Step buffers (scores, keep mask) live in their own allocation so the
     // kernels' workspace growth never aliases them.
     const int64_t need = align_up(rows * 4, 256) + align_up(rows, 256);
-    if (need > ctx->step_bytes) {
+    const bool capturing = [&] {
         cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(ctx->stream, &st);
-        if (st != cudaStreamCaptureStatusNone) return fail(EPK_ERR_ARG, "run one step before capturing a graph");
+        return st != cudaStreamCaptureStatusNone;
+    }();
+    if (need > ctx->step_bytes) {
+        if (capturing) return fail(EPK_ERR_ARG, "run one step before capturing a graph");
         if (ctx->step_buf) {
             EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
             EPK_CUDA_CHECK(cudaFree(ctx->step_buf));
@@ -347,13 +397,55 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
         EPK_CUDA_CHECK(cudaMalloc(&ctx->step_buf, size_t(need)));
         ctx->step_bytes = need;
     }
-    if (!scores) scores = static_cast<float*>(ctx->step_buf);
-    keep = static_cast<uint8_t*>(ctx->step_buf) + align_up(rows * 4, 256);
-    rc = epk_score(ctx, in, q, kp, q_heads, prompt_len, aggregation, mode, n_max, scores);
-    if (rc) return rc;
-    rc = launch_select(ctx, in, scores, EPK_F32, budgets, pins, n_pins, keep, kept, 0);
-    if (rc) return rc;
-    return launch_compact(ctx, in, out, keep, out_slack);
+    float* scores = scores_ws ? scores_ws : static_cast<float*>(ctx->step_buf);
+    uint8_t* keep = static_cast<uint8_t*>(ctx->step_buf) + align_up(rows * 4, 256);
+
+    // Layer groups: small enough that a group's K (read by both scoring
+    // passes) stays in L2 between them.
+    const int L = in->layers;
+    int G = ctx->layer_group;
+    if (G <= 0) {
+        const int64_t k_bytes_per_layer =
+            (rows / std::max(1, L)) * int64_t(in->head_dim) * dtype_size(in->dtype);
+        G = int(std::max<int64_t>(1, (40ll << 20) / std::max<int64_t>(1, k_bytes_per_layer)));
+    }
+    G = std::min(G, L);
+    const bool overlap = ctx->overlap && G < L;
+    if (overlap && !ctx->side) {
+        if (capturing) return fail(EPK_ERR_ARG, "run one step before capturing a graph");
+        EPK_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        EPK_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        EPK_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    }
+    const int64_t qlayer = int64_t(q_heads) * prompt_len * in->head_dim * dtype_size(in->dtype);
+    const int64_t klayer = int64_t(in->kv_heads) * prompt_len * in->head_dim * dtype_size(in->dtype);
+    cudaStream_t main = ctx->stream;
+    for (int l0 = 0; l0 < L; l0 += G) {
+        const int l1 = std::min(L, l0 + G);
+        const epk_cache_desc vin = layer_view(in, l0, l1);
+        const epk_cache_desc vout = layer_view(out, l0, l1);
+        rc = epk_score(ctx, &vin, static_cast<const char*>(q) + l0 * qlayer, static_cast<const char*>(kp) + l0 * klayer,
+                       q_heads, prompt_len, aggregation, mode, n_max, scores);
+        if (rc) return rc;
+        rc = launch_select(ctx, &vin, scores, EPK_F32, budgets + l0, pins, n_pins, keep, kept ? kept + l0 : nullptr, 0);
+        if (rc) return rc;
+        if (overlap) {
+            EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_fork, main));
+            EPK_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            ctx->stream = ctx->side;
+            rc = launch_compact(ctx, &vin, &vout, keep, out_slack);
+            ctx->stream = main;
+            if (rc) return rc;
+        } else {
+            rc = launch_compact(ctx, &vin, &vout, keep, out_slack);
+            if (rc) return rc;
+        }
+    }
+    if (overlap) {
+        EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->side));
+        EPK_CUDA_CHECK(cudaStreamWaitEvent(main, ctx->ev_join, 0));
+    }
+    return EPK_OK;
 }
 
 // ---- K4 ---------------------------------------------------------------------

@@ -20,8 +20,14 @@ struct epk_prof_rec {
 struct epk_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    void* ws = nullptr;  // grow-only workspace
+    void* ws = nullptr;  // grow-only workspace (scoring, selection)
     int64_t ws_bytes = 0;
+    void* ws2 = nullptr;  // grow-only workspace (compaction; may run on `side`)
+    int64_t ws2_bytes = 0;
+    cudaStream_t side = nullptr;  // second stream: compaction overlaps the next layer group's scoring
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int layer_group = 0;  // layers per group in epk_evict_step (0 = auto: group K fits in L2)
+    int overlap = 1;      // run each group's compaction on `side`
     void* step_buf = nullptr;  // epk_evict_step scores + keep mask
     int64_t step_bytes = 0;
     int* err_flag = nullptr;  // deferred device-side error code (device int)
@@ -40,6 +46,7 @@ int cuda_fail(cudaError_t e, const char* what);
 // Workspace carve-up: returns a pointer into ctx->ws (grows the workspace when
 // needed; growing is not allowed while the stream is being captured).
 int ws_require(epk_ctx* ctx, int64_t bytes);
+int ws2_require(epk_ctx* ctx, int64_t bytes);
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 

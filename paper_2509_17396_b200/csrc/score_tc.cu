@@ -34,7 +34,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "epk_internal.cuh"
 #include "sm100.cuh"
@@ -48,7 +50,8 @@ constexpr int kRowB = 128;        // bytes of one d-half row (64 bf16)
 constexpr int kChunk = 128;       // query rows per chunk (MMA M in P1)
 constexpr int kSplitCols = 1024;  // cache columns per item
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kMmaWarps = 2;  // MMA issuers alternate jobs: one issues while the other synchronises
+constexpr int kThreads = 32 * (1 + kMmaWarps + kEpiWarps);
 constexpr int kMaxQRes = 4;       // resident query chunks (P1: per chunk group)
 
 enum { MODE_STATS = 0, MODE_SCORE = 1 };
@@ -72,18 +75,29 @@ struct TcParams {
     float* scores;
     int agg_max;
     int64_t items;
+    unsigned long long* trace;  // diagnostics (EPK_TC_TRACE): CTA 0 timeline records
 };
+
+// Timeline record for CTA 0: per-role private regions of 60000 records,
+// plain stores (no atomics): (event << 56) | clock low 56 bits.
+#define EPK_TRACE(P, role, ev)                                                                          \
+    do {                                                                                                \
+        if ((P).trace && blockIdx.x == 0 && tr_n < 60000)                                               \
+            (P).trace[1 + (role) * 60000 + tr_n++] = (uint64_t(ev) << 56) | (uint64_t(clock64()) & 0xFFFFFFFFFFFFFFull); \
+    } while (0)
 
 // D (+)= A * B^T over K = 128: 8 K-steps of 16 across the two 64-wide
 // d-halves.  a_half / b_half: byte distance between the operands' d-halves.
 __device__ __forceinline__ void mma_128xN(uint32_t d_tmem, uint32_t a, uint32_t a_half, uint32_t b, uint32_t b_half,
                                           uint32_t idesc) {
+    // desc(addr + off) == desc(addr) + (off >> 4): shared addresses < 256 KB
+    // never carry out of the 14-bit start-address field.
+    const uint64_t da = sdesc_k_sw128(a), db = sdesc_k_sw128(b);
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
         const uint32_t k = uint32_t((kk & 3) * 32);
         const uint32_t h = uint32_t(kk >> 2);
-        mma_bf16_ss(d_tmem, sdesc_k_sw128(a + h * a_half + k), sdesc_k_sw128(b + h * b_half + k), idesc,
-                    kk > 0 ? 1u : 0u);
+        mma_bf16_ss(d_tmem, da + ((h * a_half + k) >> 4), db + ((h * b_half + k) >> 4), idesc, kk > 0 ? 1u : 0u);
     }
 }
 
@@ -135,6 +149,76 @@ __device__ __forceinline__ Item decode(const TcParams& P, int64_t it) {
     return x;
 }
 
+// SCORE epilogue on W columns of one cache row (query rows r0 .. r0+W):
+// Max: best = max(best, x c2 - lse2); Avg: per-window sums of 2^(x c2 - lse2)
+// accumulated per query head in shared memory.
+template <int W>
+__device__ __forceinline__ void score_cols(const float (&v)[W], const float* lse, int r0, const TcParams& P,
+                                           float& best, float* s_avg, int r_local) {
+    if (P.agg_max) {
+        float b0 = best, b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < W; i += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(lse + i);
+            b0 = fmaxf(b0, fmaf(v[i], P.c2, -l4.x));
+            b1 = fmaxf(b1, fmaf(v[i + 1], P.c2, -l4.y));
+            b2 = fmaxf(b2, fmaf(v[i + 2], P.c2, -l4.z));
+            b3 = fmaxf(b3, fmaf(v[i + 3], P.c2, -l4.w));
+        }
+        best = fmaxf(fmaxf(b0, b1), fmaxf(b2, b3));
+    } else {
+        float acc = 0.f;
+        int gcur = r0 / P.p;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const int rq = r0 + i;
+            if (rq < P.Gp) {
+                const int gg = rq / P.p;
+                if (gg != gcur) {
+                    atomicAdd(&s_avg[gcur * kChunk + r_local], acc);
+                    acc = 0.f;
+                    gcur = gg;
+                }
+                acc += ex2(fmaf(v[i], P.c2, -lse[i]));
+            }
+        }
+        if (gcur < P.G) atomicAdd(&s_avg[gcur * kChunk + r_local], acc);
+    }
+}
+
+// STATS epilogue on W columns of one query row, `lim` of them valid:
+// online (max, sum 2^(x c2 - max)) update of (m, z).
+template <int W>
+__device__ __forceinline__ void stats_cols(float (&v)[W], int lim, float c2, float& m, float& z) {
+    float mx = -INFINITY;
+    if (lim >= W) {
+#pragma unroll
+        for (int i = 0; i < W; ++i) mx = fmaxf(mx, v[i]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            v[i] = (i < lim) ? v[i] : -INFINITY;
+            mx = fmaxf(mx, v[i]);
+        }
+    }
+    mx *= c2;
+    if (mx > m) {
+        z *= ex2(m - mx);
+        m = mx;
+    }
+    if (m != -INFINITY) {
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int i = 0; i < W; i += 4) {
+            s0 += ex2(fmaf(v[i], c2, -m));
+            s1 += ex2(fmaf(v[i + 1], c2, -m));
+            s2 += ex2(fmaf(v[i + 2], c2, -m));
+            s3 += ex2(fmaf(v[i + 3], c2, -m));
+        }
+        z += (s0 + s1) + (s2 + s3);
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_score_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tm_k,
@@ -165,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t it_beg = int64_t(blockIdx.x) * per;
     const int64_t it_end = min(P.items, it_beg + per);
     const bool resident = MODE == MODE_STATS || P.resident;
+    int tr_n = 0;  // EPK_TRACE record count of this thread
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tm_k);
@@ -172,11 +257,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (MODE == MODE_STATS) tma_prefetch(&tm_kp);
         for (int s = 0; s < P.kstages; ++s) {
             mbar_init(&k_full[s], 1);
-            mbar_init(&k_empty[s], 1);
+            mbar_init(&k_empty[s], kMmaWarps);  // every MMA warp releases every stage
         }
         for (int s = 0; s < kMaxQRes; ++s) {
             mbar_init(&q_full[s], 1);
-            mbar_init(&q_empty[s], 1);
+            mbar_init(&q_empty[s], resident ? kMmaWarps : 1);  // streamed slots belong to one MMA warp
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&t_full[s], 1);
@@ -193,7 +278,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_holder;
 
     if (warp == 0) {
-        if (lane == 0) {  // ------------------------- TMA producer -------------------------
+        const bool leader = elect_one_sync();
+        {  // ------------------------- TMA producer (warp-wide, one lane issues) -----------
             int ks = 0;
             uint32_t kph = 0;
             uint32_t qload[kMaxQRes] = {0, 0, 0, 0};
@@ -207,20 +293,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                     key = x.qkey();
                     for (int c = 0; c < x.nq; ++c) {
                         mbar_wait(&q_empty[c], (qload[c] & 1) ^ 1);
-                        mbar_expect_tx(&q_full[c], 2 * kChunk * kRowB);
-                        load_rows(sQ + c * kChunk * kRowB, q_half, &tm_q, &q_full[c], qrow0 + (x.c0 + c) * kChunk);
+                        if (leader) {
+                            mbar_expect_tx(&q_full[c], 2 * kChunk * kRowB);
+                            load_rows(sQ + c * kChunk * kRowB, q_half, &tm_q, &q_full[c], qrow0 + (x.c0 + c) * kChunk);
+                        }
+                        __syncwarp();
                         ++qload[c];
                     }
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
+                    if (leader) EPK_TRACE(P, 0, 1);
                     mbar_wait(&k_empty[ks], kph ^ 1);
-                    mbar_expect_tx(&k_full[ks], k_stage);
-                    if (t < x.nc)
-                        load_rows(sK + ks * k_stage, k_half, &tm_k, &k_full[ks],
-                                  int(x.krow0 + int64_t(x.t0 + t) * P.krows));
-                    else
-                        load_rows(sK + ks * k_stage, k_half, &tm_kp, &k_full[ks],
-                                  (x.l * P.H + x.h) * P.p + (t - x.nc) * P.krows);
+                    if (leader) EPK_TRACE(P, 0, 2);
+                    if (leader) {
+                        mbar_expect_tx(&k_full[ks], k_stage);
+                        if (t < x.nc)
+                            load_rows(sK + ks * k_stage, k_half, &tm_k, &k_full[ks],
+                                      int(x.krow0 + int64_t(x.t0 + t) * P.krows));
+                        else
+                            load_rows(sK + ks * k_stage, k_half, &tm_kp, &k_full[ks],
+                                      (x.l * P.H + x.h) * P.p + (t - x.nc) * P.krows);
+                    }
+                    __syncwarp();
                     if (++ks == P.kstages) {
                         ks = 0;
                         kph ^= 1;
@@ -230,82 +324,102 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int slot = int(pj & 1);
                             const int nch = min(2, P.NQ - 2 * j);
                             mbar_wait(&q_empty[slot], (qload[slot] & 1) ^ 1);
-                            mbar_expect_tx(&q_full[slot], nch * 2 * kChunk * kRowB);
-                            for (int cc = 0; cc < nch; ++cc)
-                                load_rows(sQ + (slot * 2 + cc) * kChunk * kRowB, q_half, &tm_q, &q_full[slot],
-                                          qrow0 + (2 * j + cc) * kChunk);
+                            if (leader) {
+                                mbar_expect_tx(&q_full[slot], nch * 2 * kChunk * kRowB);
+                                for (int cc = 0; cc < nch; ++cc)
+                                    load_rows(sQ + (slot * 2 + cc) * kChunk * kRowB, q_half, &tm_q, &q_full[slot],
+                                              qrow0 + (2 * j + cc) * kChunk);
+                            }
+                            __syncwarp();
                             ++qload[slot];
                         }
                     }
                 }
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ------------------------- MMA issuer ---------------------------
+    } else if (warp <= kMmaWarps) {
+        // MMA warp mw issues the jobs with (job & 1) == mw into TMEM slot mw;
+        // both walk the same item/tile sequence and both release every K stage.
+        const uint32_t mw = uint32_t(warp - 1);
+        const bool leader = elect_one_sync();
+        {  // ------------------------- MMA issuers (warp-wide, one lane issues) ------------
             int ks = 0;
             uint32_t kph = 0;
             uint32_t qload[kMaxQRes] = {0, 0, 0, 0};
             uint32_t job = 0;
-            int64_t key = -1, pj = 0;
+            int64_t key = -1;
             int held = 0;
             const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK);
+            const bool tr = leader && mw == 0;
             for (int64_t it = it_beg; it < it_end; ++it) {
                 const Item x = decode<MODE>(P, it);
                 if (x.ntiles() == 0) continue;
                 bool fresh = false;
                 if (resident && x.qkey() != key) {
-                    for (int c = 0; c < held; ++c) mma_commit(&q_empty[c]);  // old Q retires with its MMAs
+                    if (leader)
+                        for (int c = 0; c < held; ++c) mma_commit(&q_empty[c]);  // old Q retires with its MMAs
+                    __syncwarp();
                     key = x.qkey();
                     held = x.nq;
                     fresh = true;
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
+                    if (tr) EPK_TRACE(P, 1, 3);
                     mbar_wait(&k_full[ks], kph);
+                    if (tr) EPK_TRACE(P, 1, 4);
                     const uint32_t kst = k0 + uint32_t(ks) * k_stage;
                     if (MODE == MODE_STATS) {
-                        for (int c = 0; c < x.nq; ++c) {
+                        for (int c = 0; c < x.nq; ++c, ++job) {
                             if (fresh && t == 0) {
                                 mbar_wait(&q_full[c], qload[c] & 1);
                                 ++qload[c];
                             }
-                            const int ts = int(job & 1);
+                            if ((job & 1) != mw) continue;
+                            const int ts = int(mw);
                             mbar_wait(&t_empty[ts], ((job >> 1) & 1) ^ 1);
                             tc_fence_after();
-                            mma_128xN(tmem + uint32_t(ts * 256), q0 + uint32_t(c * kChunk * kRowB), q_half, kst,
-                                      k_half, idesc_bf16_f32(128, 256));
-                            mma_commit(&t_full[ts]);
-                            ++job;
+                            if (leader) {
+                                mma_128xN(tmem + uint32_t(ts * 256), q0 + uint32_t(c * kChunk * kRowB), q_half, kst,
+                                          k_half, idesc_bf16_f32(128, 256));
+                                mma_commit(&t_full[ts]);
+                            }
+                            __syncwarp();
                         }
                     } else {
-                        for (int j = 0; 2 * j < x.nq; ++j) {
+                        for (int j = 0; 2 * j < x.nq; ++j, ++job) {
                             const int nch = min(2, x.nq - 2 * j);
+                            if (resident && fresh && t == 0)
+                                for (int cc = 0; cc < nch; ++cc) {
+                                    mbar_wait(&q_full[2 * j + cc], qload[2 * j + cc] & 1);
+                                    ++qload[2 * j + cc];
+                                }
+                            if ((job & 1) != mw) continue;
                             uint32_t qb;
-                            int slot = 0;
+                            const int slot = int(mw);  // streamed pair slot == TMEM slot == this warp
                             if (resident) {
-                                if (fresh && t == 0)
-                                    for (int cc = 0; cc < nch; ++cc) {
-                                        mbar_wait(&q_full[2 * j + cc], qload[2 * j + cc] & 1);
-                                        ++qload[2 * j + cc];
-                                    }
                                 qb = q0 + uint32_t(2 * j * kChunk * kRowB);
                             } else {
-                                slot = int(pj & 1);
-                                ++pj;
                                 mbar_wait(&q_full[slot], qload[slot] & 1);
                                 ++qload[slot];
                                 qb = q0 + uint32_t(slot * 2 * kChunk * kRowB);
                             }
-                            const int ts = int(job & 1);
+                            const int ts = int(mw);
+                            if (tr) EPK_TRACE(P, 1, 5);
                             mbar_wait(&t_empty[ts], ((job >> 1) & 1) ^ 1);
+                            if (tr) EPK_TRACE(P, 1, 6);
                             tc_fence_after();
-                            mma_128xN(tmem + uint32_t(ts * 256), kst, k_half, qb, q_half,
-                                      idesc_bf16_f32(128, uint32_t(nch * kChunk)));
-                            mma_commit(&t_full[ts]);
-                            if (!resident) mma_commit(&q_empty[slot]);
-                            ++job;
+                            if (leader) {
+                                mma_128xN(tmem + uint32_t(ts * 256), kst, k_half, qb, q_half,
+                                          idesc_bf16_f32(128, uint32_t(nch * kChunk)));
+                                mma_commit(&t_full[ts]);
+                                if (!resident) mma_commit(&q_empty[slot]);
+                            }
+                            __syncwarp();
+                            if (tr) EPK_TRACE(P, 1, 7);
                         }
                     }
-                    mma_commit(&k_empty[ks]);
+                    if (leader) mma_commit(&k_empty[ks]);
+                    __syncwarp();
                     if (++ks == P.kstages) {
                         ks = 0;
                         kph ^= 1;
@@ -314,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {  // ------------------------- epilogue (8 warps) -------------------------
-        const int e = warp - 2;
+        const int e = warp - 1 - kMmaWarps;
         const int quarter = warp & 3;  // TMEM lanes this warp may read
         const int half = e >> 2;       // column half of every job
         const int r_local = quarter * 32 + lane;
@@ -345,45 +459,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int ts = int(job & 1);
                         mbar_wait(&t_full[ts], (job >> 1) & 1);
                         tc_fence_after();
-#pragma unroll 1
-                        for (int q4 = 0; q4 < 2; ++q4) {
-                            const int col0 = half * 128 + q4 * 64;
-                            float v[64];
-                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + col0), v);
-                            if (q4 == 1) {  // the slot's values are all in registers now
-                                tc_fence_before();
-                                __syncwarp();
-                                if (lane == 0) mbar_arrive(&t_empty[ts]);
-                            }
-                            const int hl = lim - col0;
-                            float mx = -INFINITY;
-                            if (hl >= 64) {
-#pragma unroll
-                                for (int i = 0; i < 64; ++i) mx = fmaxf(mx, v[i]);
-                            } else {
-#pragma unroll
-                                for (int i = 0; i < 64; ++i) {
-                                    v[i] = (i < hl) ? v[i] : -INFINITY;
-                                    mx = fmaxf(mx, v[i]);
-                                }
-                            }
-                            mx *= P.c2;
-                            if (mx > m[c]) {
-                                z[c] *= ex2(m[c] - mx);
-                                m[c] = mx;
-                            }
-                            if (m[c] != -INFINITY) {
-                                const float mc = m[c];
-                                float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-                                for (int i = 0; i < 64; i += 4) {
-                                    s0 += ex2(fmaf(v[i], P.c2, -mc));
-                                    s1 += ex2(fmaf(v[i + 1], P.c2, -mc));
-                                    s2 += ex2(fmaf(v[i + 2], P.c2, -mc));
-                                    s3 += ex2(fmaf(v[i + 3], P.c2, -mc));
-                                }
-                                z[c] += (s0 + s1) + (s2 + s3);
-                            }
+                        {
+                            float v[128];
+                            tmem_ld128(tmem + lane_addr + uint32_t(ts * 256 + half * 128), v);
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&t_empty[ts]);  // slot free: values are in registers
+                            stats_cols<128>(v, lim - half * 128, P.c2, m[c], z[c]);
                         }
                         ++job;
                     }
@@ -415,53 +497,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int ncols = min(2, x.nq - 2 * j) * kChunk;  // query rows of the job
                         const int hw = ncols / 2;                         // columns per warp half
                         const int ts = int(job & 1);
+                        if (lane == 0 && e == 0) EPK_TRACE(P, 2, 8);
                         mbar_wait(&t_full[ts], (job >> 1) & 1);
+                        if (lane == 0 && e == 0) EPK_TRACE(P, 2, 9);
                         tc_fence_after();
-#pragma unroll 1
-                        for (int q4 = 0; q4 * 64 < hw; ++q4) {
-                            const int col0 = half * hw + q4 * 64;
+                        const int r0 = 2 * j * kChunk + half * hw;  // first query row of this warp's columns
+                        if (hw == 128) {
+                            float v[128];
+                            tmem_ld128(tmem + lane_addr + uint32_t(ts * 256 + half * hw), v);
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&t_empty[ts]);  // slot free: values are in registers
+                            if (lane == 0 && e == 0) EPK_TRACE(P, 2, 10);
+                            score_cols<128>(v, s_lse + r0, r0, P, best, s_avg, r_local);
+                        } else {
                             float v[64];
-                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + col0), v);
-                            if ((q4 + 1) * 64 >= hw) {
-                                tc_fence_before();
-                                __syncwarp();
-                                if (lane == 0) mbar_arrive(&t_empty[ts]);
-                            }
-                            const int r0 = 2 * j * kChunk + col0;  // first query row of these 64 columns
-                            const float* lse = s_lse + r0;
-                            if (P.agg_max) {
-                                float b0 = best, b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
-#pragma unroll
-                                for (int i = 0; i < 64; i += 4) {
-                                    const float4 l4 = *reinterpret_cast<const float4*>(lse + i);
-                                    b0 = fmaxf(b0, fmaf(v[i], P.c2, -l4.x));
-                                    b1 = fmaxf(b1, fmaf(v[i + 1], P.c2, -l4.y));
-                                    b2 = fmaxf(b2, fmaf(v[i + 2], P.c2, -l4.z));
-                                    b3 = fmaxf(b3, fmaf(v[i + 3], P.c2, -l4.w));
-                                }
-                                best = fmaxf(fmaxf(b0, b1), fmaxf(b2, b3));
-                            } else {
-                                // window sums per query head g, both halves add in smem
-                                float acc = 0.f;
-                                int gcur = r0 / P.p;
-#pragma unroll
-                                for (int i = 0; i < 64; ++i) {
-                                    const int rq = r0 + i;
-                                    if (rq < P.Gp) {
-                                        const int gg = rq / P.p;
-                                        if (gg != gcur) {
-                                            atomicAdd(&s_avg[gcur * kChunk + r_local], acc);
-                                            acc = 0.f;
-                                            gcur = gg;
-                                        }
-                                        acc += ex2(fmaf(v[i], P.c2, -lse[i]));
-                                    }
-                                }
-                                if (gcur < P.G) atomicAdd(&s_avg[gcur * kChunk + r_local], acc);
-                            }
+                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + half * hw), v);
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&t_empty[ts]);
+                            if (lane == 0 && e == 0) EPK_TRACE(P, 2, 10);
+                            score_cols<64>(v, s_lse + r0, r0, P, best, s_avg, r_local);
                         }
                         ++job;
                     }
+                    if (lane == 0 && e == 0) EPK_TRACE(P, 2, 11);
                     // combine the two column halves of each cache row
                     const int jrow = (x.t0 + t) * P.krows + r_local;
                     if (P.agg_max) {
@@ -572,6 +632,13 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     P.c2 = float((1.0 / std::sqrt(double(kD))) * 1.4426950408889634);
     P.scores = scores;
     P.agg_max = agg_max;
+    P.trace = nullptr;
+    static unsigned long long* trace_buf = nullptr;
+    if (std::getenv("EPK_TC_TRACE")) {
+        if (!trace_buf) EPK_CUDA_CHECK(cudaMalloc(&trace_buf, 8 * 180001));
+        EPK_CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, 8 * 180001, ctx->stream));
+        P.trace = trace_buf;
+    }
     const int64_t rows = int64_t(P.L) * H * P.NQ * kChunk;
     rc = ws_require(ctx, rows * 2 * P.splits * 8 + rows * 4 + 4096);
     if (rc) return rc;
@@ -619,9 +686,13 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
             break;
         }
     }
+    if (const char* ks = std::getenv("EPK_P1_KSTAGES")) P.kstages = std::max(1, std::min(P.kstages, std::atoi(ks)));
     if (smem_bytes(P, MODE_STATS) > limit) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
     P.cgroups = (P.NQ + P.cg_chunks - 1) / P.cg_chunks;
     P.items = int64_t(P.L) * H * P.splits * P.cgroups;
+    if (std::getenv("EPK_TC_VERBOSE"))
+        fprintf(stderr, "P1: NQ=%d cg_chunks=%d kstages=%d smem=%d limit=%d items=%lld\n", P.NQ, P.cg_chunks,
+                P.kstages, smem_bytes(P, MODE_STATS), limit, (long long)P.items);
     const int grid1 = int(std::min<int64_t>(P.items, ctx->num_sms));
     EPK_PROF(ctx, "p1_rowstats");
     tc_score_kernel<MODE_STATS><<<grid1, kThreads, smem_bytes(P, MODE_STATS), ctx->stream>>>(P, tm_k1, tm_q, tm_kp);
@@ -643,15 +714,28 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
             break;
         }
     }
+    if (const char* ks = std::getenv("EPK_P2_KSTAGES")) P.kstages = std::max(2, std::min(P.kstages, std::atoi(ks)));
     if (P.kstages < 2 || smem_bytes(P, MODE_SCORE) > limit)
         return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
     P.cgroups = 1;
     P.cg_chunks = P.NQ;
     P.items = int64_t(P.L) * H * P.splits;
+    if (std::getenv("EPK_TC_VERBOSE"))
+        fprintf(stderr, "P2: NQ=%d resident=%d kstages=%d smem=%d items=%lld\n", P.NQ, P.resident, P.kstages,
+                smem_bytes(P, MODE_SCORE), (long long)P.items);
     const int grid2 = int(std::min<int64_t>(P.items, ctx->num_sms));
     EPK_PROF(ctx, "p2_colscore");
     tc_score_kernel<MODE_SCORE><<<grid2, kThreads, smem_bytes(P, MODE_SCORE), ctx->stream>>>(P, tm_k2, tm_q, tm_kp);
     EPK_LAUNCH_CHECK(ctx);
+    if (P.trace) {  // dump CTA 0's P2 timeline
+        static std::vector<unsigned long long> h(180001);
+        EPK_CUDA_CHECK(cudaMemcpyAsync(h.data(), trace_buf, 8 * 180001, cudaMemcpyDeviceToHost, ctx->stream));
+        EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (FILE* f = std::fopen(std::getenv("EPK_TC_TRACE"), "wb")) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+    }
     return EPK_OK;
 }
 

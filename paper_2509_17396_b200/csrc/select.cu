@@ -42,6 +42,7 @@ struct SelectParams {
     uint8_t* keep;
     int32_t* kept_per_layer;
     int* err_flag;
+    int key_cap;  // keys of this CTA's slice cached in dynamic shared memory
 };
 
 template <typename ScoreT>
@@ -198,6 +199,8 @@ __global__ void __cluster_dims__(kSelCluster, 1, 1) __launch_bounds__(kSelThread
         pinned_live = s_before;
     }
 
+    if (P.per_head && rank == 0)  // gap rows after the head's live rows: never kept
+        for (int64_t r = seg_end + tid; r < s_off[seg_head + 1]; r += blockDim.x) keep[r] = 0;
     const int64_t limit = P.per_head ? P.budget[layer] : int64_t(H) * P.budget[layer];
     if (n_live <= limit) {
         for (int64_t r = my_begin + tid; r < my_end; r += blockDim.x) keep[r] = is_live(r, head_of(r)) ? 1 : 0;
@@ -219,6 +222,26 @@ __global__ void __cluster_dims__(kSelCluster, 1, 1) __launch_bounds__(kSelThread
         return;
     }
 
+    // ---- this CTA's candidate keys -> shared memory (one global pass) ---------
+    // Non-candidates (gap rows, pinned rows) hold the sentinel ~0, which no
+    // finite or infinite score maps to.
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    KeyT* s_keys = reinterpret_cast<KeyT*>(s_dyn);
+    const KeyT kNone = ~KeyT(0);
+    const int64_t nmine = my_end - my_begin;
+    const bool cached = nmine <= P.key_cap;
+    auto fetch_key = [&](int64_t r) -> KeyT {
+        const int h = head_of(r);
+        if (!is_live(r, h) || (use_pins && is_pinned(P.pins, P.n_pins, pos[r]))) return kNone;
+        return desc_key(scores[r]);
+    };
+    if (cached) {
+#pragma unroll 4
+        for (int64_t i = tid; i < nmine; i += blockDim.x) s_keys[i] = fetch_key(my_begin + i);
+        __syncthreads();
+    }
+    auto key_of = [&](int64_t r) -> KeyT { return cached ? s_keys[r - my_begin] : fetch_key(r); };
+
     // ---- radix select on the score key --------------------------------------
     KeyT prefix = 0, mask = 0;
     int pass = 0;
@@ -230,11 +253,8 @@ __global__ void __cluster_dims__(kSelCluster, 1, 1) __launch_bounds__(kSelThread
             const int64_t r = b0 + lane;
             int digit = 256;
             if (r < my_end) {
-                const int h = head_of(r);
-                if (is_live(r, h) && !(use_pins && is_pinned(P.pins, P.n_pins, pos[r]))) {
-                    const KeyT key = desc_key(scores[r]);
-                    if (((key ^ prefix) & mask) == 0) digit = int((key >> shift) & 0xFF);
-                }
+                const KeyT key = key_of(r);
+                if (key != kNone && ((key ^ prefix) & mask) == 0) digit = int((key >> shift) & 0xFF);
             }
             const unsigned grp = __match_any_sync(0xffffffffu, digit);
             if (digit != 256 && lane == __ffs(grp) - 1) atomicAdd(&hist[digit], uint32_t(__popc(grp)));
@@ -266,10 +286,9 @@ __global__ void __cluster_dims__(kSelCluster, 1, 1) __launch_bounds__(kSelThread
             for (int64_t b0 = my_begin + int64_t(warp) * 32; b0 < my_end; b0 += int64_t(nwarps) * 32) {
                 const int64_t r = b0 + lane;
                 int digit = 256;
-                if (r < my_end) {
+                if (r < my_end && key_of(r) == T) {
                     const int h = head_of(r);
-                    if (is_live(r, h) && !(use_pins && is_pinned(P.pins, P.n_pins, pos[r])) &&
-                        desc_key(scores[r]) == T) {
+                    {
                         const uint64_t tb = P.per_head ? uint64_t(r) : ((uint64_t(uint32_t(pos[r])) << 8) | uint64_t(h));
                         if (((tb ^ tprefix) & tmask) == 0) digit = int((tb >> shift) & 0xFF);
                     }
@@ -295,20 +314,19 @@ __global__ void __cluster_dims__(kSelCluster, 1, 1) __launch_bounds__(kSelThread
 
     // ---- write the keep mask -------------------------------------------------
     for (int64_t r = my_begin + tid; r < my_end; r += blockDim.x) {
-        const int h = head_of(r);
+        const KeyT key = key_of(r);
         uint8_t kf = 0;
-        if (is_live(r, h)) {
-            if (use_pins && is_pinned(P.pins, P.n_pins, pos[r])) {
+        if (key != kNone) {
+            if (key < T) {
                 kf = 1;
-            } else {
-                const KeyT key = desc_key(scores[r]);
-                if (key < T) {
-                    kf = 1;
-                } else if (key == T) {
-                    const uint64_t tb = P.per_head ? uint64_t(r) : ((uint64_t(uint32_t(pos[r])) << 8) | uint64_t(h));
-                    kf = tb <= U ? 1 : 0;
-                }
+            } else if (key == T) {
+                const int h = head_of(r);
+                const uint64_t tb = P.per_head ? uint64_t(r) : ((uint64_t(uint32_t(pos[r])) << 8) | uint64_t(h));
+                kf = tb <= U ? 1 : 0;
             }
+        } else if (use_pins) {
+            const int h = head_of(r);
+            kf = (is_live(r, h) && is_pinned(P.pins, P.n_pins, pos[r])) ? 1 : 0;
         }
         keep[r] = kf;
     }
@@ -342,11 +360,19 @@ int launch_select(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int
     P.err_flag = ctx->err_flag;
     const int segs = per_head ? c->layers * c->kv_heads : c->layers;
     dim3 grid(segs * kSelCluster), block(kSelThreads);
+    constexpr int kKeySmem = 96 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        EPK_CUDA_CHECK(cudaFuncSetAttribute(select_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kKeySmem));
+        EPK_CUDA_CHECK(cudaFuncSetAttribute(select_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kKeySmem));
+        attr = true;
+    }
+    P.key_cap = kKeySmem / (score_dtype == EPK_F32 ? 4 : 8);
     EPK_PROF(ctx, per_head ? "select_per_head" : "select");
     if (score_dtype == EPK_F32)
-        select_kernel<float><<<grid, block, 0, ctx->stream>>>(P);
+        select_kernel<float><<<grid, block, kKeySmem, ctx->stream>>>(P);
     else
-        select_kernel<double><<<grid, block, 0, ctx->stream>>>(P);
+        select_kernel<double><<<grid, block, kKeySmem, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }
