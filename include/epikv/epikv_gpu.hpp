@@ -1,0 +1,396 @@
+// epikv_gpu.hpp -- the drop-in C++ boundary: the reference epikv hot-path API
+// (/root/reference/proj/include/epikv) with the same signatures, argument
+// meaning, results and exceptions, computed by the sm_100a kernels behind the
+// C ABI (include/epk/epk.h, libepk.so).
+//
+// The reference is a header-only library of inline functions in namespace
+// epikv, so the GPU versions live in namespace epikv::gpu over the reference's
+// OWN types (LayerCache, LayerScores, ForwardTrace, TokenScoreMap, Model,
+// BlockPrefillConfig, PrefillReport, KMeansResult, SensitivityProfile).  A call
+// site switches by qualification:
+//
+//   epikv::evict_to_budget(c, s, pins)      ->  epikv::gpu::evict_to_budget(c, s, pins)
+//   epikv::score_with_prompt(trace, agg)    ->  epikv::gpu::score_with_prompt(trace, agg)
+//   epikv::kmeans(points, k, seed, iters)   ->  epikv::gpu::kmeans(points, k, seed, iters)
+//   epikv::measure_sensitivity(m, t, b, s)  ->  epikv::gpu::measure_sensitivity(m, t, b, s)
+//   epikv::block_prefill(m, ctx, cfg, e, p) ->  epikv::gpu::block_prefill(m, ctx, cfg, e, p)
+//
+// Replaced reference interfaces (file:line under proj/include/epikv):
+//   evict_to_budget      kvcache.hpp:142      (K2 pooled select on fp64 keys; the kept
+//                                              KVEntry objects keep their stable order)
+//   score_with_prompt    scoring.hpp:80       (grid reduction kernel, fp64, bit-exact)
+//   kmeans               clustering.hpp:148   (K4, fp64, bit-exact)
+//   measure_sensitivity  allocation.hpp:55    (K5 reduction; the two model forwards
+//                                              stay the reference's, on the host)
+//   block_prefill        blockprefill.hpp:92  (the block loop: the toy-model
+//                                              forward stays on the host, scoring
+//                                              and eviction run on the GPU)
+// allocate (allocation.hpp:120) is L host scalars and stays the reference's.
+//
+// Link: -L<repo>/paper_2509_17396_b200 -lepk -lcudart.  Needs the reference
+// headers (and nlohmann/json) on the include path, as epikv itself does.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "epikv/allocation.hpp"
+#include "epikv/blockprefill.hpp"
+#include "epikv/clustering.hpp"
+#include "epikv/kvcache.hpp"
+#include "epikv/scoring.hpp"
+#include "epikv/toymodel.hpp"
+#include "epk/epk.h"
+
+namespace epikv {
+namespace gpu {
+
+namespace detail {
+
+// Maps a C-ABI status to the reference's exception types.
+inline void check(int rc) {
+    if (rc == EPK_OK) return;
+    const std::string msg = epk_last_error();
+    switch (rc) {
+        case EPK_ERR_DIM: throw DimensionError(msg);
+        case EPK_ERR_ZERO_NORM: throw ZeroNormError(msg);
+        default: throw Error(msg);
+    }
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+// One context per thread (the C ABI is reentrant; contexts are not shared).
+inline epk_ctx* ctx() {
+    thread_local struct Holder {
+        epk_ctx* c = nullptr;
+        ~Holder() {
+            if (c) epk_ctx_destroy(c);
+        }
+    } h;
+    if (!h.c) {
+        int dev = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        check(epk_ctx_create(dev, nullptr, &h.c));
+    }
+    return h.c;
+}
+
+// Device buffer (RAII).
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    explicit DBuf(size_t count) : n(count) {
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void upload(const T* h, size_t count) {
+        cuda_check(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    }
+    void download(T* h, size_t count) const {
+        cuda_check(cudaMemcpy(h, p, count * sizeof(T), cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    }
+};
+
+}  // namespace detail
+
+/// evict_to_budget (kvcache.hpp:142) on the GPU: pooled selection over the
+/// layer's heads by (score desc, position asc, head asc) with pins; the kept
+/// entries keep their per-head order.  Same result and exceptions as the
+/// reference.  (The host KVEntry payload never moves to the device; the
+/// device-resident cache path is epk_evict_step / epk_compact.)
+inline LayerCache evict_to_budget(const LayerCache& cache, const LayerScores& scores,
+                                  const std::unordered_set<std::size_t>& pinned = {}) {
+    const std::size_t H = cache.heads.size();
+    if (scores.size() != H) throw DimensionError("evict_to_budget: score head count mismatch");
+    const std::size_t limit = H * cache.budget;
+    if (cache.entry_count() <= limit) return cache;
+    // marshal: CSR rows, fp64 scores (pinned rows carry a dummy score)
+    std::vector<int32_t> pos, off(H + 1, 0), len(H, 0);
+    std::vector<double> sc;
+    std::size_t dim = 0;
+    for (std::size_t h = 0; h < H; ++h) {
+        for (const KVEntry& e : cache.heads[h]) {
+            if (e.position > 0x7fffffffu) throw Error("evict_to_budget: position exceeds the device int32 range");
+            pos.push_back(int32_t(e.position));
+            if (pinned.count(e.position)) {
+                sc.push_back(0.0);
+            } else {
+                auto it = scores[h].find(e.position);
+                if (it == scores[h].end())
+                    throw DimensionError("evict_to_budget: missing score for head " + std::to_string(h) +
+                                         " position " + std::to_string(e.position));
+                sc.push_back(it->second);
+            }
+            dim = std::max(dim, e.key.size());
+        }
+        len[h] = int32_t(cache.heads[h].size());
+        off[h + 1] = off[h] + len[h];
+    }
+    const std::size_t n = pos.size();
+    // the selection only needs positions and scores; the compaction order is
+    // the stable per-head order, so the kept entries are copied on the host
+    // from the device's keep mask (the K/V payload never has to move).
+    epk_ctx* c = detail::ctx();
+    detail::DBuf<int32_t> d_pos(n), d_off(H + 1), d_len(H);
+    detail::DBuf<double> d_sc(n), d_kv(2 * std::max<std::size_t>(n, 1));
+    detail::DBuf<uint8_t> d_keep(n);
+    d_pos.upload(pos.data(), n);
+    d_off.upload(off.data(), H + 1);
+    d_len.upload(len.data(), H);
+    d_sc.upload(sc.data(), n);
+    std::vector<int32_t> pins_sorted;
+    for (std::size_t p : pinned)
+        if (p <= 0x7fffffffu) pins_sorted.push_back(int32_t(p));
+    std::sort(pins_sorted.begin(), pins_sorted.end());
+    detail::DBuf<int32_t> d_pins(pins_sorted.size());
+    if (!pins_sorted.empty()) d_pins.upload(pins_sorted.data(), pins_sorted.size());
+    const int64_t base[2] = {0, int64_t(n)};
+    epk_cache_desc desc{1, int32_t(H), 2, EPK_F64, d_kv.p, d_kv.p, d_pos.p, d_off.p, d_len.p, base};
+    const int64_t budget = int64_t(cache.budget);
+    detail::check(epk_select_pooled(c, &desc, d_sc.p, EPK_F64, &budget, pins_sorted.empty() ? nullptr : d_pins.p,
+                                    int32_t(pins_sorted.size()), d_keep.p, nullptr, 1));
+    std::vector<uint8_t> keep(n);
+    d_keep.download(keep.data(), n);
+    LayerCache out(H, cache.budget);
+    std::size_t r = 0;
+    for (std::size_t h = 0; h < H; ++h)
+        for (const KVEntry& e : cache.heads[h])
+            if (keep[r++]) out.heads[h].push_back(e);
+    return out;
+}
+
+/// score_with_prompt (scoring.hpp:80) on the GPU: window Max/Avg over the
+/// prompt rows, max over a kv-head's query heads, cache columns only.
+inline TokenScoreMap score_with_prompt(const ForwardTrace& prompt_trace, Aggregation agg) {
+    const std::size_t p = prompt_trace.positions.size();
+    if (p == 0) throw Error("score_with_prompt: empty prompt");
+    TokenScoreMap map;
+    map.layers.resize(prompt_trace.layers.size());
+    epk_ctx* c = detail::ctx();
+    for (std::size_t l = 0; l < prompt_trace.layers.size(); ++l) {
+        const LayerTrace& lt = prompt_trace.layers[l];
+        const std::size_t H = lt.context_positions.size();
+        if (H == 0 || lt.attention.empty() || lt.attention.size() % H != 0)
+            throw DimensionError("score_with_prompt: attention grid shape mismatch");
+        const std::size_t group = lt.attention.size() / H;
+        std::vector<int64_t> off(H + 1, 0);
+        for (std::size_t h = 0; h < H; ++h) {
+            if (lt.context_positions[h].size() < p) throw DimensionError("score_with_prompt: attention grid shape mismatch");
+            off[h + 1] = off[h] + int64_t(lt.context_positions[h].size() - p);
+        }
+        std::vector<double> grids;
+        for (std::size_t qh = 0; qh < lt.attention.size(); ++qh) {
+            const Matrix& g = lt.attention[qh];
+            const std::size_t h = qh / group;
+            if (g.rows != p || g.cols != lt.context_positions[h].size())
+                throw DimensionError("score_with_prompt: attention grid shape mismatch");
+            grids.insert(grids.end(), g.values.begin(), g.values.end());
+        }
+        const std::size_t nout = static_cast<std::size_t>(off[H]);
+        detail::DBuf<double> d_grids(grids.size()), d_out(nout);
+        d_grids.upload(grids.data(), grids.size());
+        detail::check(epk_score_grids(c, int32_t(lt.attention.size()), int32_t(H), int32_t(p), off.data(), d_grids.p,
+                                      agg == Aggregation::Max ? EPK_AGG_MAX : EPK_AGG_AVG, d_out.p));
+        std::vector<double> out(nout);
+        d_out.download(out.data(), out.size());
+        map.layers[l].resize(H);
+        for (std::size_t h = 0; h < H; ++h)
+            for (int64_t j = 0; j < off[h + 1] - off[h]; ++j)
+                map.layers[l][h].emplace(lt.context_positions[h][std::size_t(j)], out[std::size_t(off[h] + j)]);
+    }
+    return map;
+}
+
+/// kmeans (clustering.hpp:148) on the GPU, bit-exact (fp64, same RNG stream).
+inline KMeansResult kmeans(const std::vector<Vec>& points, std::size_t k, std::uint64_t seed,
+                           std::size_t max_iters = 64) {
+    if (k < 1) throw Error("kmeans: cluster count must be >= 1");
+    if (points.size() < k)
+        throw Error("kmeans: fewer points (" + std::to_string(points.size()) + ") than clusters (" +
+                    std::to_string(k) + ")");
+    const std::size_t n = points.size(), dim = points[0].size();
+    std::vector<double> flat;
+    flat.reserve(n * dim);
+    for (const Vec& p : points) {
+        if (p.size() != dim) throw DimensionError("kmeans: points differ in dimension");
+        flat.insert(flat.end(), p.begin(), p.end());
+    }
+    detail::DBuf<double> d_pts(flat.size());
+    d_pts.upload(flat.data(), flat.size());
+    std::vector<int64_t> assign(n);
+    std::vector<double> cent(k * dim), sse(std::max<std::size_t>(max_iters, 1));
+    int64_t iters = 0;
+    detail::check(epk_kmeans(detail::ctx(), d_pts.p, int64_t(n), int64_t(dim), int64_t(k), seed, int64_t(max_iters),
+                             assign.data(), cent.data(), &iters, sse.data()));
+    KMeansResult r;
+    r.assignments.assign(assign.begin(), assign.end());
+    r.centroids.resize(k);
+    for (std::size_t c = 0; c < k; ++c) r.centroids[c].assign(cent.begin() + c * dim, cent.begin() + (c + 1) * dim);
+    r.iterations = std::size_t(iters);
+    r.sse_per_iteration.assign(sse.begin(), sse.begin() + iters);
+    return r;
+}
+
+/// measure_sensitivity (allocation.hpp:55): the two forwards (causal and
+/// sink+recent) are the reference's model substrate on the host; the key
+/// cosine reduction sigma_l runs on the GPU (fp64, deterministic order).
+inline SensitivityProfile measure_sensitivity(const Model& model, std::span<const TokenId> calibration_tokens,
+                                              std::size_t calibration_budget, std::size_t sink,
+                                              std::string input_id = "") {
+    const std::size_t n = calibration_tokens.size();
+    if (n < 2) throw Error("measure_sensitivity: need at least 2 calibration tokens");
+    if (calibration_budget < sink + 1) throw Error("measure_sensitivity: budget must be >= sink + 1");
+    TraceOptions opts;
+    opts.store_attention = false;
+    const ForwardTrace full = forward(model, calibration_tokens, MaskSpec::causal(), nullptr, opts);
+    const ForwardTrace block =
+        forward(model, calibration_tokens, MaskSpec::sink_recent(sink, calibration_budget - sink), nullptr, opts);
+    const std::size_t L = model.config.layers, H = model.config.kv_heads, d = model.config.head_dim;
+    std::vector<double> kf(L * H * n * d), kb(L * H * n * d);
+    for (std::size_t l = 0; l < L; ++l)
+        for (std::size_t h = 0; h < H; ++h) {
+            std::memcpy(kf.data() + (l * H + h) * n * d, full.layers[l].keys[h].values.data(), n * d * sizeof(double));
+            std::memcpy(kb.data() + (l * H + h) * n * d, block.layers[l].keys[h].values.data(), n * d * sizeof(double));
+        }
+    detail::DBuf<double> d_kf(kf.size()), d_kb(kb.size()), d_sigma(L);
+    detail::DBuf<int64_t> d_skip(1);
+    d_kf.upload(kf.data(), kf.size());
+    d_kb.upload(kb.data(), kb.size());
+    detail::check(epk_key_cosine_sigma(detail::ctx(), d_kf.p, d_kb.p, EPK_F64, int32_t(L), int32_t(H), int64_t(n),
+                                       int32_t(d), d_sigma.p, d_skip.p));
+    SensitivityProfile profile;
+    profile.sigma.resize(L);
+    d_sigma.download(profile.sigma.data(), L);
+    int64_t skipped = 0;
+    d_skip.download(&skipped, 1);
+    for (double s : profile.sigma) profile.sensitivity.push_back(1.0 - s);
+    profile.mask_sink = sink;
+    profile.mask_recent = calibration_budget - sink;
+    profile.input_id = std::move(input_id);
+    profile.model_seed = model.config.seed;
+    profile.skipped_zero_norm = std::size_t(skipped);
+    return profile;
+}
+
+/// block_prefill (blockprefill.hpp:92) with scoring and eviction on the GPU.
+/// The toy-model forwards (block and prompt) are the reference's own, on the
+/// host; every block's prompt grids are scored by the GPU reduction and every
+/// layer is evicted by the GPU selection, so the result is bit-identical to
+/// the reference.  Supports the patched, snapkv, kvzip, infinipot and
+/// streaming scorers (KeyDiff stays on the reference path).
+inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> context,
+                                   const BlockPrefillConfig& config, std::size_t episode_id = 0,
+                                   std::span<const std::size_t> positions = {}) {
+    const ModelConfig& cfg = model.config;
+    if (context.empty()) throw Error("block_prefill: empty context");
+    if (config.budget_per_head < 1 || config.block_size < 1)
+        throw Error("block_prefill: budget and block size must be >= 1");
+    if (config.scorer == ScorerKind::patched && !config.prompt_provider)
+        throw Error("block_prefill: patched scorer needs a prompt provider");
+    if (config.scorer == ScorerKind::keydiff) return epikv::block_prefill(model, context, config, episode_id, positions);
+    std::vector<std::size_t> default_positions;
+    if (positions.empty()) {
+        default_positions.resize(context.size());
+        for (std::size_t i = 0; i < context.size(); ++i) default_positions[i] = i;
+        positions = default_positions;
+    } else if (positions.size() != context.size()) {
+        throw DimensionError("block_prefill: positions size mismatch");
+    }
+    std::vector<std::size_t> layer_budgets(cfg.layers, config.budget_per_head);
+    if (config.allocation) {
+        if (config.allocation->layer_count() != cfg.layers)
+            throw Error("block_prefill: allocation layer count != model layers");
+        if (config.allocation->total() != cfg.layers * config.budget_per_head)
+            throw Error("block_prefill: allocation does not target layers * budget");
+        layer_budgets = config.allocation->layer_budgets;
+    }
+    PrefillReport report;
+    report.layer_budgets = layer_budgets;
+    report.cache.episode_id = episode_id;
+    report.cache.provenance.scorer = std::string(scorer_name(config.scorer));
+    report.cache.provenance.budget_per_head = config.budget_per_head;
+    report.cache.provenance.layer_budgets = layer_budgets;
+    for (std::size_t l = 0; l < cfg.layers; ++l) report.cache.layers.emplace_back(cfg.kv_heads, layer_budgets[l]);
+    const std::size_t prompt_base = positions.back() + 1;
+    const std::vector<std::size_t> zeros(cfg.layers, 0);
+    std::unordered_set<std::size_t> pins;
+    if (config.scorer == ScorerKind::streaming) {
+        if (config.streaming_sink > config.budget_per_head) throw Error("block_prefill: streaming sink exceeds budget");
+        if (config.allocation)
+            for (std::size_t b : layer_budgets)
+                if (config.streaming_sink > b) throw Error("block_prefill: streaming sink exceeds an allocated layer budget");
+    }
+    auto entries = [&](const EpisodicCache& c) {
+        std::vector<std::size_t> out;
+        for (const auto& layer : c.layers) out.push_back(layer.entry_count());
+        return out;
+    };
+    TraceOptions block_opts;
+    block_opts.store_attention = false;
+    const std::size_t n = context.size();
+    for (std::size_t start = 0; start < n; start += config.block_size) {
+        const std::size_t len = std::min(config.block_size, n - start);
+        const std::span<const TokenId> block = context.subspan(start, len);
+        const std::span<const std::size_t> block_positions = positions.subspan(start, len);
+        const std::size_t block_index = report.blocks_processed;
+        ForwardTrace trace = forward(model, block, block_positions, MaskSpec::causal(), &report.cache, block_opts);
+        append_to_cache(report.cache, trace);
+        report.occupancy.record(OccupancyKind::Append, entries(report.cache), zeros);
+        TokenScoreMap scores;
+        if (scorer_uses_prompt(config.scorer)) {
+            PatchedPrompt prompt;
+            switch (config.scorer) {
+                case ScorerKind::patched: prompt = config.prompt_provider(episode_id, block_index); break;
+                case ScorerKind::snapkv: prompt = snapkv_prompt(block); break;
+                case ScorerKind::kvzip: prompt = kvzip_prompt(block, cfg.vocab); break;
+                case ScorerKind::infinipot: prompt = infinipot_prompt(cfg.vocab); break;
+                default: break;
+            }
+            if (prompt.tokens.empty()) throw Error("block_prefill: empty patched prompt");
+            std::vector<std::size_t> prompt_positions(prompt.tokens.size());
+            for (std::size_t i = 0; i < prompt.tokens.size(); ++i) prompt_positions[i] = prompt_base + i;
+            report.prompt_ranges.push_back({prompt_base, prompt.tokens.size()});
+            const ForwardTrace prompt_trace =
+                forward(model, prompt.tokens, prompt_positions, MaskSpec::causal(), &report.cache);
+            report.occupancy.record(OccupancyKind::PromptResident, entries(report.cache),
+                                    std::vector<std::size_t>(cfg.layers, cfg.kv_heads * prompt.tokens.size()));
+            scores = gpu::score_with_prompt(prompt_trace, config.aggregation);
+        } else {
+            scores.layers.resize(report.cache.layers.size());
+            for (std::size_t l = 0; l < report.cache.layers.size(); ++l) {
+                scores.layers[l].resize(report.cache.layers[l].heads.size());
+                for (std::size_t h = 0; h < report.cache.layers[l].heads.size(); ++h)
+                    for (const KVEntry& e : report.cache.layers[l].heads[h])
+                        scores.layers[l][h].emplace(e.position, double(e.position));
+            }
+            pins.clear();
+            for (std::size_t p = 0; p < config.streaming_sink; ++p) pins.insert(p);
+        }
+        std::size_t evicted = 0;
+        for (std::size_t l = 0; l < cfg.layers; ++l) {
+            const std::size_t before = report.cache.layers[l].entry_count();
+            report.cache.layers[l] = gpu::evict_to_budget(report.cache.layers[l], scores.layers[l], pins);
+            evicted += before - report.cache.layers[l].entry_count();
+        }
+        report.evictions_per_block.push_back(evicted);
+        report.occupancy.record(OccupancyKind::Evict, entries(report.cache), zeros);
+        ++report.blocks_processed;
+    }
+    return report;
+}
+
+}  // namespace gpu
+}  // namespace epikv

@@ -33,3 +33,16 @@ def test_no_cpu_fallback_without_gpu():
     import paper_2509_17396_b200 as epk
     with pytest.raises(RuntimeError):
         epk.Context(0)
+
+
+def test_cpp_dropin_header_compiles(tmp_path):
+    """include/epikv/epikv_gpu.hpp compiles against the reference headers."""
+    ref = "/root/reference/proj/include"
+    if not os.path.isdir(ref):
+        pytest.skip("reference headers absent")
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "epikv/epikv_gpu.hpp"\nint main() { return 0; }\n')
+    json_inc = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty"
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", f"-I{ROOT}/include", f"-I{ref}", f"-I{json_inc}",
+                        "-I/usr/local/cuda/include", str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]

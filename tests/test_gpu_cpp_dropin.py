@@ -1,0 +1,20 @@
+"""The C++ drop-in (include/epikv/epikv_gpu.hpp) against the reference
+library call for call: tests/cpp/test_dropin.cpp, built against the
+reference headers in place by tests/cpp/Makefile (travels to the GPU box)."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_build", "test_dropin")
+
+
+def test_cpp_dropin_matches_reference(gpu):
+    if not os.path.exists(BIN):
+        pytest.skip("C++ drop-in driver not built (needs /root/reference at build time)")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "0 failed" in r.stdout

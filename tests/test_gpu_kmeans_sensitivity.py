@@ -74,3 +74,27 @@ def test_allocate_golden(gpu):
         assert a.layer_budgets == g[f"al{i}_b"].tolist()
         assert a.weights == g[f"al{i}_w"].tolist()
         assert a.total() == len(a.layer_budgets) * int(g[f"al{i}_M"])
+
+
+def test_kmeans_sharded_device_ops_nccl_world1(gpu, orc):
+    """kmeans_sharded through the K4 device ops under a 1-rank NCCL group
+    equals the single-GPU kmeans (the N>1 chain is covered with gloo)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(4)
+        pts = rng.standard_normal((500, 64))
+        r = gpu.kmeans_sharded(torch.as_tensor(pts, device="cuda"), 0, 500, 6, 9)
+        a, c, it, sse = orc.kmeans(pts, 6, 9)
+        assert r.assignments == a.tolist() and np.array_equal(r.centroids, c) and r.iterations == it
+        assert np.array_equal(np.array(r.sse_per_iteration), sse)
+    finally:
+        dist.destroy_process_group()
