@@ -457,7 +457,9 @@ def main():
     roof = None
     if dom is not None:
         bound, amount, unit, peak = work[dom]
-        kms = kernels[dom]["ms_per_step"] / kernels[dom]["launches_per_step"]
+        nl = kernels[dom]["launches_per_step"]
+        kms = kernels[dom]["ms_per_step"] / nl
+        amount = amount / nl  # the work of ONE launch (a layer group)
         ach = amount / (kms / 1000.0)
         roof = {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
                 "traffic": traffic_from_profiles(dom), "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"

@@ -23,7 +23,7 @@
  *   epk_select_per_head  top_k_indices (numerics.hpp:111-125) per kv-head
  *   epk_compact          evict_to_budget output loop (kvcache.hpp:192-199)
  *   epk_append           append_to_cache (toymodel.hpp:428-443)
- *   epk_evict_step       one block step of block_prefill (blockprefill.hpp:420-444):
+ *   epk_evict_step       one block step of block_prefill (blockprefill.hpp:157-226):
  *                        score -> per-layer evict, all layers
  *   epk_kmeans*          kmeans (clustering.hpp:148-260)
  *   epk_key_cosine_sigma measure_sensitivity reduction (allocation.hpp:80-100)
@@ -102,10 +102,10 @@ const char* epk_status_string(int status);
 int epk_version(void);
 /* Options for epk_evict_step:
  *   EPK_OPT_LAYER_GROUP  layers scored/selected/compacted per group (0 = auto:
- *                        the largest group whose K fits in ~40 MB of L2, so
- *                        the second scoring pass re-reads K from L2)
- *   EPK_OPT_OVERLAP      1 (default): each group's compaction runs on a second
- *                        stream, overlapping the next group's scoring */
+ *                        all layers in one group)
+ *   EPK_OPT_OVERLAP      1 (default): with more than one group, each group's
+ *                        select + compaction runs on a second stream,
+ *                        overlapping the next group's scoring */
 #define EPK_OPT_LAYER_GROUP 1
 #define EPK_OPT_OVERLAP 2
 int epk_ctx_set_option(epk_ctx* ctx, int32_t option, int64_t value);

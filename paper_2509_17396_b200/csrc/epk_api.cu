@@ -400,15 +400,12 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     float* scores = scores_ws ? scores_ws : static_cast<float*>(ctx->step_buf);
     uint8_t* keep = static_cast<uint8_t*>(ctx->step_buf) + align_up(rows * 4, 256);
 
-    // Layer groups: small enough that a group's K (read by both scoring
-    // passes) stays in L2 between them.
+    // Layer groups (EPK_OPT_LAYER_GROUP): 0 = auto = all layers in one group.
+    // Smaller groups let a group's select+compact (side stream) overlap the
+    // next group's scoring, at the cost of more, smaller launches.
     const int L = in->layers;
     int G = ctx->layer_group;
-    if (G <= 0) {
-        const int64_t k_bytes_per_layer =
-            (rows / std::max(1, L)) * int64_t(in->head_dim) * dtype_size(in->dtype);
-        G = int(std::max<int64_t>(1, (40ll << 20) / std::max<int64_t>(1, k_bytes_per_layer)));
-    }
+    if (G <= 0) G = L;
     G = std::min(G, L);
     const bool overlap = ctx->overlap && G < L;
     if (overlap && !ctx->side) {
@@ -427,19 +424,18 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
         rc = epk_score(ctx, &vin, static_cast<const char*>(q) + l0 * qlayer, static_cast<const char*>(kp) + l0 * klayer,
                        q_heads, prompt_len, aggregation, mode, n_max, scores);
         if (rc) return rc;
-        rc = launch_select(ctx, &vin, scores, EPK_F32, budgets + l0, pins, n_pins, keep, kept ? kept + l0 : nullptr, 0);
-        if (rc) return rc;
+        // select + compact of this group run on the side stream (when
+        // overlapping) so the main stream goes straight on to the next
+        // group's scoring; scores/keep are row-indexed, groups never alias.
         if (overlap) {
             EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_fork, main));
             EPK_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
             ctx->stream = ctx->side;
-            rc = launch_compact(ctx, &vin, &vout, keep, out_slack);
-            ctx->stream = main;
-            if (rc) return rc;
-        } else {
-            rc = launch_compact(ctx, &vin, &vout, keep, out_slack);
-            if (rc) return rc;
         }
+        rc = launch_select(ctx, &vin, scores, EPK_F32, budgets + l0, pins, n_pins, keep, kept ? kept + l0 : nullptr, 0);
+        if (rc == EPK_OK) rc = launch_compact(ctx, &vin, &vout, keep, out_slack);
+        ctx->stream = main;
+        if (rc) return rc;
     }
     if (overlap) {
         EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->side));

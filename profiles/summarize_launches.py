@@ -13,7 +13,8 @@ def main(path, out):
     i_name, i_val = h.index("Kernel Name"), h.index("Metric Value")
     agg = collections.OrderedDict()
     for r in rows[1:]:
-        n = r[i_name].split("(")[0].replace("void ", "").replace("epk::", "").split("<")[0]
+        n = r[i_name].split("(")[0].replace("void ", "").replace("epk::", "")
+        n = n.replace("tc_score_kernel<0>", "tc_score_kernel<P1>").replace("tc_score_kernel<1>", "tc_score_kernel<P2>")
         agg.setdefault(n, []).append(float(r[i_val].replace(",", "")))
     ours = {n: v for n, v in agg.items() if n.startswith(("tc_", "select", "compact", "f32_", "append"))}
     tot = sum(sum(v) / len(v) for v in ours.values())
