@@ -212,6 +212,16 @@ def run_ours(args, c, rank, world, device, torch, dist):
     for k in kernels:
         kernels[k]["share"] = kernels[k]["ms_per_step"] / prof_total if prof_total else None
 
+    if args.timeline:  # one profiled step's launch timeline (start, duration, stream)
+        ctx.profile(True)
+        for i in range(3):
+            step(i)
+        tl = ctx.profile_timeline()
+        ctx.profile(False)
+        with open(args.timeline, "w") as f:
+            f.write("# kernel  start_ms  dur_ms  stream(0 main, 1 side)\n")
+            for name, t0, d, side in tl:
+                f.write(f"{name:16s} {t0:9.4f} {d:8.4f} {side}\n")
     e2e = run_e2e(args, c, epk, torch, device, ctx, dist) if not args.no_e2e else None
     return dict(ms=ms_max, launches=launches, clocks=clk, kernels=kernels, e2e=e2e, live=live, keep=keep)
 
@@ -415,6 +425,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layer-group", type=int, default=0, help="layers per step group (0 = auto, L2-sized)")
     ap.add_argument("--no-overlap", action="store_true", help="compaction on the main stream")
+    ap.add_argument("--timeline", default=None, help="write one profiled step's kernel timeline to this file")
     args = ap.parse_args()
     c = CONFIGS[args.config]
 

@@ -117,6 +117,11 @@ int64_t epk_ctx_launch_count(epk_ctx* ctx);
  * count; index >= 0 returns the kernel name (<= 31 chars) and milliseconds. */
 int epk_ctx_profile(epk_ctx* ctx, int32_t enable);
 int64_t epk_ctx_profile_read(epk_ctx* ctx, int64_t index, char* name_out, float* ms_out);
+/* Timeline of record `index` (after epk_ctx_profile_read(ctx, -1, ...)):
+ * start relative to record 0's start, duration, and whether it was launched
+ * on the context's side stream (overlapped select/compaction). */
+int epk_ctx_profile_timeline(epk_ctx* ctx, int64_t index, char* name_out, float* start_ms, float* dur_ms,
+                             int32_t* side);
 
 /* ---- K1 / K1': fused patched-prompt scoring --------------------------------- *
  * scores[layer_base[l] + r] = score of live row r of layer l (fp32 [dev]).

@@ -54,6 +54,8 @@ _SIGS = {
     "epk_ctx_profile": (C.c_int, [vp, i32]),
     "epk_ctx_set_option": (C.c_int, [vp, i32, i64]),
     "epk_ctx_profile_read": (i64, [vp, i64, C.c_char_p, C.POINTER(C.c_float)]),
+    "epk_ctx_profile_timeline": (C.c_int, [vp, i64, C.c_char_p, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                           C.POINTER(C.c_int32)]),
     "epk_score": (C.c_int, [vp, C.POINTER(CacheDesc), vp, vp, i32, i32, i32, i32, i64, vp]),
     "epk_score_grids": (C.c_int, [vp, i32, i32, i32, vp, vp, i32, vp]),
     "epk_select_pooled": (C.c_int, [vp, C.POINTER(CacheDesc), vp, i32, vp, vp, i32, vp, vp, i32]),

@@ -64,6 +64,18 @@ class Context:
             out.append((name.value.decode(), float(ms.value)))
         return out
 
+    def profile_timeline(self) -> list[tuple[str, float, float, int]]:
+        """[(kernel, start ms from the first record, duration ms, side stream)]."""
+        lib = _lib.load()
+        n = int(lib.epk_ctx_profile_read(self.handle, -1, None, None))
+        out = []
+        name = C.create_string_buffer(32)
+        t0, d, side = C.c_float(), C.c_float(), C.c_int32()
+        for i in range(max(n, 0)):
+            lib.epk_ctx_profile_timeline(self.handle, i, name, C.byref(t0), C.byref(d), C.byref(side))
+            out.append((name.value.decode(), float(t0.value), float(d.value), int(side.value)))
+        return out
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             _lib.load().epk_ctx_destroy(self.handle)

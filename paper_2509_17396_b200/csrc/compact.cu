@@ -47,6 +47,11 @@ struct CompactParams {
     int32_t* chunk_cnt;     // [layers][max_chunks]
     int32_t* chunk_prefix;  // [layers][max_chunks]
     int* err_flag;
+    // threshold mode (the tensor-core step): keep[] is derived here from the
+    // scorer's keys and the per-layer threshold (select_threshold_kernel)
+    const uint32_t* keys;  // [rows] global, or null (keep[] given)
+    const uint64_t* thr;   // [layers][2]
+    uint8_t* keep_out;
 };
 
 __device__ __forceinline__ int head_of_row(const int32_t* off, int H, int64_t r) {
@@ -66,7 +71,30 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_count_kernel(const 
     const int64_t rows = P.in_off[layer * (P.H + 1) + P.H];
     const int64_t r0 = int64_t(chunk) * kChunkRows;
     int c = 0;
-    if (r0 < rows) {
+    if (r0 < rows && P.keys) {
+        // keep = live && (key < T || (key == T && (position << 8 | head) <= U))
+        const int64_t base = P.in_lt.base[layer];
+        const int32_t* off = P.in_off + layer * (P.H + 1);
+        const uint64_t t0 = P.thr[2 * layer], U = P.thr[2 * layer + 1];
+        const bool all = (t0 >> 32) != 0;
+        const uint32_t T = uint32_t(t0);
+        uint8_t* kp = P.keep_out + base;
+#pragma unroll
+        for (int i = 0; i < kChunkRows / 32; ++i) {
+            const int64_t r = r0 + i * 32 + lane;
+            uint8_t k = 0;
+            if (r < rows) {
+                const int h = head_of_row(off, P.H, r);
+                if (r - off[h] < P.in_len[layer * P.H + h]) {
+                    const uint32_t key = __ldcg(P.keys + base + r);
+                    k = (all || key < T ||
+                         (key == T && ((uint64_t(uint32_t(P.in_pos[base + r])) << 8) | uint64_t(h)) <= U)) ? 1 : 0;
+                }
+                kp[r] = k;
+            }
+            c += k;
+        }
+    } else if (r0 < rows) {
         const uint8_t* kp = P.keep + P.in_lt.base[layer];
 #pragma unroll
         for (int i = 0; i < kChunkRows / 32; ++i) {
@@ -199,7 +227,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_gather_kernel(const
 }
 
 int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const uint8_t* keep,
-                   int slack) {
+                   int slack, const uint32_t* keys, const uint64_t* thr) {
     if (in->layers != out->layers || in->kv_heads != out->kv_heads || in->head_dim != out->head_dim ||
         in->dtype != out->dtype)
         return fail(EPK_ERR_DIM, "compact: in/out cache shapes differ");
@@ -230,6 +258,9 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     P.out_off = out->head_off;
     P.out_len = out->head_len;
     P.err_flag = ctx->err_flag;
+    P.keys = keys;
+    P.thr = thr;
+    P.keep_out = const_cast<uint8_t*>(keep);
     const int64_t ws = 2 * int64_t(in->layers) * P.max_chunks * 4 + 1024;
     rc = ws2_require(ctx, ws);
     if (rc) return rc;

@@ -54,7 +54,7 @@ void prof_begin(epk_ctx* ctx, const char* name) {
     cudaEventCreate(&r.start);
     cudaEventCreate(&r.stop);
     cudaEventRecord(r.start, ctx->stream);
-    r.stop = r.stop;
+    r.side = (ctx->side && ctx->stream == ctx->side) ? 1 : 0;
     ctx->prof.push_back(r);
 }
 
@@ -104,10 +104,13 @@ int make_layer_table(const epk_cache_desc* c, LayerTable* t) {
 
 int launch_select(epk_ctx*, const epk_cache_desc*, const void*, int, const int64_t*, const int32_t*, int, uint8_t*,
                   int32_t*, int);
-int launch_compact(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*, int);
+int launch_compact(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*, int, const uint32_t*,
+                   const uint64_t*);
+int launch_select_threshold(epk_ctx*, const epk_cache_desc*, const FusedSelect*, const int64_t*, uint64_t*, int32_t*);
 int launch_append(epk_ctx*, const epk_cache_desc*, const void*, const void*, const int32_t*, int);
 int launch_score_f32(epk_ctx*, const epk_cache_desc*, const float*, const float*, int, int, int, int64_t, float*);
-int launch_score_tc(epk_ctx*, const epk_cache_desc*, const void*, const void*, int, int, int, int64_t, float*);
+int launch_score_tc(epk_ctx*, const epk_cache_desc*, const void*, const void*, int, int, int, int64_t, float*,
+                    const FusedSelect*);
 int launch_score_grids(epk_ctx*, int, int, int, const int64_t*, const double*, int, double*);
 int launch_expf_probe(epk_ctx*, const float*, float*, int64_t);
 int launch_km_dist(epk_ctx*, const double*, int64_t, int64_t, const double*, int64_t, double*);
@@ -276,6 +279,20 @@ int64_t epk_ctx_profile_read(epk_ctx* ctx, int64_t index, char* name_out, float*
     return int64_t(ctx->prof.size());
 }
 
+int epk_ctx_profile_timeline(epk_ctx* ctx, int64_t index, char* name_out, float* start_ms, float* dur_ms,
+                             int32_t* side) {
+    if (!ctx || index < 0 || index >= int64_t(ctx->prof.size())) return EPK_ERR_ARG;
+    const epk_prof_rec& r = ctx->prof[size_t(index)];
+    std::snprintf(name_out, 32, "%s", r.name);
+    float t0 = 0.f, d = 0.f;
+    cudaEventElapsedTime(&t0, ctx->prof[0].start, r.start);
+    cudaEventElapsedTime(&d, r.start, r.stop);
+    *start_ms = t0;
+    *dur_ms = d;
+    *side = r.side;
+    return EPK_OK;
+}
+
 int epk_score(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const void* kp, int32_t q_heads,
               int32_t prompt_len, int32_t aggregation, int32_t mode, int64_t n_max, float* scores) {
     int rc = check_ctx(ctx);
@@ -290,7 +307,7 @@ int epk_score(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const void* 
         return launch_score_f32(ctx, c, static_cast<const float*>(q), static_cast<const float*>(kp), q_heads,
                                 prompt_len, aggregation == EPK_AGG_MAX, n_max, scores);
     if (mode == EPK_SCORE_TC_BF16)
-        return launch_score_tc(ctx, c, q, kp, q_heads, prompt_len, aggregation == EPK_AGG_MAX, n_max, scores);
+        return launch_score_tc(ctx, c, q, kp, q_heads, prompt_len, aggregation == EPK_AGG_MAX, n_max, scores, nullptr);
     return fail(EPK_ERR_ARG, "bad score mode");
 }
 
@@ -332,7 +349,7 @@ int epk_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* ou
     if (rc) return rc;
     if ((rc = check_cache(in)) || (rc = check_cache(out))) return rc;
     if (!keep) return fail(EPK_ERR_ARG, "compact: null keep");
-    return launch_compact(ctx, in, out, keep, slack);
+    return launch_compact(ctx, in, out, keep, slack, nullptr, nullptr);
 }
 
 int epk_append(epk_ctx* ctx, const epk_cache_desc* c, const void* k_new, const void* v_new, const int32_t* positions,
@@ -378,9 +395,21 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     if ((rc = check_cache(in)) || (rc = check_cache(out))) return rc;
     if (in->layers != out->layers) return fail(EPK_ERR_DIM, "evict_step: in/out layer counts differ");
     const int64_t rows = in->layer_base[in->layers];
-    // Step buffers (scores, keep mask) live in their own allocation so the
-    // kernels' workspace growth never aliases them.
-    const int64_t need = align_up(rows * 4, 256) + align_up(rows, 256);
+    const int L = in->layers;
+    // Tensor-core steps without pins take the fused selection: the scorer
+    // writes keys + score histograms, select_threshold_kernel finds each
+    // layer's threshold from them, the compaction derives keep[] itself.
+    const bool fused = mode == EPK_SCORE_TC_BF16 && n_pins == 0 && in->kv_heads <= 64;
+    // Step buffers live in their own allocation so the kernels' workspace
+    // growth never aliases them.  Layout: histograms at fixed offsets for
+    // kMaxLayers layers (zeroed once here, re-zeroed by every threshold
+    // select), thresholds, then the row-indexed scores / keep mask / keys.
+    const int64_t o_hc = int64_t(kMaxLayers) * 65536 * 4;
+    const int64_t o_thr = o_hc + int64_t(kMaxLayers) * 256 * 4;
+    const int64_t o_scores = o_thr + int64_t(kMaxLayers) * 16;
+    const int64_t o_keep = o_scores + align_up(rows * 4, 256);
+    const int64_t o_keys = o_keep + align_up(rows, 256);
+    const int64_t need = o_keys + align_up(rows * 4, 256);
     const bool capturing = [&] {
         cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(ctx->stream, &st);
@@ -389,21 +418,26 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     if (need > ctx->step_bytes) {
         if (capturing) return fail(EPK_ERR_ARG, "run one step before capturing a graph");
         if (ctx->step_buf) {
-            EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            EPK_CUDA_CHECK(cudaDeviceSynchronize());
             EPK_CUDA_CHECK(cudaFree(ctx->step_buf));
             ctx->step_buf = nullptr;
             ctx->step_bytes = 0;
         }
         EPK_CUDA_CHECK(cudaMalloc(&ctx->step_buf, size_t(need)));
+        EPK_CUDA_CHECK(cudaMemsetAsync(ctx->step_buf, 0, size_t(need), ctx->stream));
         ctx->step_bytes = need;
     }
-    float* scores = scores_ws ? scores_ws : static_cast<float*>(ctx->step_buf);
-    uint8_t* keep = static_cast<uint8_t*>(ctx->step_buf) + align_up(rows * 4, 256);
+    char* sb = static_cast<char*>(ctx->step_buf);
+    float* scores = scores_ws ? scores_ws : reinterpret_cast<float*>(sb + o_scores);
+    uint8_t* keep = reinterpret_cast<uint8_t*>(sb + o_keep);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(sb + o_keys);
+    uint32_t* hist_f = reinterpret_cast<uint32_t*>(sb);
+    uint32_t* hist_c = reinterpret_cast<uint32_t*>(sb + o_hc);
+    uint64_t* thr = reinterpret_cast<uint64_t*>(sb + o_thr);
 
     // Layer groups (EPK_OPT_LAYER_GROUP): 0 = auto = all layers in one group.
     // Smaller groups let a group's select+compact (side stream) overlap the
     // next group's scoring, at the cost of more, smaller launches.
-    const int L = in->layers;
     int G = ctx->layer_group;
     if (G <= 0) G = L;
     G = std::min(G, L);
@@ -421,19 +455,36 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
         const int l1 = std::min(L, l0 + G);
         const epk_cache_desc vin = layer_view(in, l0, l1);
         const epk_cache_desc vout = layer_view(out, l0, l1);
-        rc = epk_score(ctx, &vin, static_cast<const char*>(q) + l0 * qlayer, static_cast<const char*>(kp) + l0 * klayer,
-                       q_heads, prompt_len, aggregation, mode, n_max, scores);
+        const void* qg = static_cast<const char*>(q) + l0 * qlayer;
+        const void* kpg = static_cast<const char*>(kp) + l0 * klayer;
+        const FusedSelect fs{keys, hist_f + int64_t(l0) * 65536, hist_c + int64_t(l0) * 256};
+        if (fused) {
+            if (prompt_len <= 0) return fail(EPK_ERR_EMPTY_PROMPT, "score_with_prompt: empty prompt");
+            if (q_heads < in->kv_heads || q_heads % in->kv_heads != 0)
+                return fail(EPK_ERR_DIM, "score_with_prompt: attention grid shape mismatch");
+            if (aggregation != EPK_AGG_MAX && aggregation != EPK_AGG_AVG) return fail(EPK_ERR_ARG, "bad aggregation");
+            rc = launch_score_tc(ctx, &vin, qg, kpg, q_heads, prompt_len, aggregation == EPK_AGG_MAX, n_max, scores,
+                                 &fs);
+        } else {
+            rc = epk_score(ctx, &vin, qg, kpg, q_heads, prompt_len, aggregation, mode, n_max, scores);
+        }
         if (rc) return rc;
         // select + compact of this group run on the side stream (when
         // overlapping) so the main stream goes straight on to the next
-        // group's scoring; scores/keep are row-indexed, groups never alias.
+        // group's scoring; scores/keys/keep are row-indexed and the
+        // histograms/thresholds layer-indexed, so groups never alias.
         if (overlap) {
             EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_fork, main));
             EPK_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
             ctx->stream = ctx->side;
         }
-        rc = launch_select(ctx, &vin, scores, EPK_F32, budgets + l0, pins, n_pins, keep, kept ? kept + l0 : nullptr, 0);
-        if (rc == EPK_OK) rc = launch_compact(ctx, &vin, &vout, keep, out_slack);
+        if (fused) {
+            rc = launch_select_threshold(ctx, &vin, &fs, budgets + l0, thr + 2 * l0, kept ? kept + l0 : nullptr);
+            if (rc == EPK_OK) rc = launch_compact(ctx, &vin, &vout, keep, out_slack, keys, thr + 2 * l0);
+        } else {
+            rc = launch_select(ctx, &vin, scores, EPK_F32, budgets + l0, pins, n_pins, keep, kept ? kept + l0 : nullptr, 0);
+            if (rc == EPK_OK) rc = launch_compact(ctx, &vin, &vout, keep, out_slack, nullptr, nullptr);
+        }
         ctx->stream = main;
         if (rc) return rc;
     }

@@ -15,6 +15,7 @@
 struct epk_prof_rec {
     char name[32];
     cudaEvent_t start, stop;
+    int side;  // 1: launched on the context's side stream
 };
 
 struct epk_ctx {
@@ -91,6 +92,15 @@ struct LayerTable {
 };
 
 int make_layer_table(const epk_cache_desc* c, LayerTable* t);
+
+// Threshold-select buffers the tensor-core scorer fills in its SCORE pass
+// (select.cu select_threshold_kernel consumes them).  Pointers are for the
+// launch's first layer.
+struct FusedSelect {
+    uint32_t* keys;         // [rows] per global cache row
+    uint32_t* hist_fine;    // [layers][65536] counts of float_bits(score) >> 14
+    uint32_t* hist_coarse;  // [layers][256] counts of that bin >> 8
+};
 
 // ---------------------------------------------------------------------------
 // Order-preserving score keys.  Selection sorts ascending on

@@ -11,25 +11,37 @@
 // shared memory.
 //
 // One persistent kernel template, two modes; every MMA is 128 x 256 x 128
-// (the shape that keeps tcgen05 at ~94% of issue peak -- 128 x 128 tiles
-// saturate shared-memory operand bandwidth at ~69%, see
-// profiles/mma_rate_r01.txt):
-//   STATS (P1): A = 128-row query chunk (resident), B = 256-row K stage,
+// (the shape that keeps tcgen05 near its issue peak -- 128 x 128 tiles
+// saturate shared-memory operand bandwidth):
+//   STATS (P1): A = 128-row query chunk (resident), B = 256-row K tile,
 //               D[query row][cache col] -> epilogue lanes own a query row and
-//               keep an online (max, sum exp2) per chunk -> partial (m, Z) per
-//               (row, split, column half); tc_merge_kernel folds them into
-//               lse2 = log2 sum 2^(x - m) + m.
-//   SCORE (P2): A = 128-row K stage, B = two query chunks (256 query rows),
+//               keep an online (max, sum exp2) per chunk -> one partial (m, Z)
+//               per (row, CTA segment, column half).
+//   SCORE (P2): A = 128-row K tile, B = two query chunks (256 query rows),
 //               D[cache row][query row] -> epilogue lanes own a cache row and
-//               reduce max_r (x c2 - lse2[r]) -> one exp2 per cache row.
+//               reduce max_r (x c2 - lse2[r]) -> one exp2 per cache row.  The
+//               P1 partials of a head are folded into lse2 = log2 sum 2^(x-m)+m
+//               by the epilogue warps when a CTA reaches the head (no separate
+//               merge launch).
+//
+// Work partition (tile-balanced): a mode's work is the sequence of RUNS
+// (STATS: (layer, kv-head, query-chunk group); SCORE: (layer, kv-head)), each
+// a run of K tiles (STATS: ceil(n_h/256) cache tiles + the causal prompt
+// tiles; SCORE: ceil(n_h/128)).  Every CTA computes the run prefix from the
+// device-resident head lengths (ragged after pooled eviction) and takes the
+// contiguous global tile range [T b/grid, T (b+1)/grid); a run cut by a CTA
+// boundary becomes two segments whose softmax partials P2 combines.  So the
+// makespan is within one tile of the mean for any layer group and any
+// per-head raggedness.
+//
 // Shared memory keeps Q as [d-half][all query rows] (128-byte swizzled rows,
 // 8-row groups 1024 B apart) so any two consecutive 128-row chunks form one
-// 256-row B operand.  TMEM: two 256-column accumulator slots.
-// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer, warps 2-9 epilogue (warp e: TMEM lane quarter e & 3, column half
-// e >> 2 of every job).  Items = (layer, kv-head, 1024-column split [,
-// query-chunk group]) dealt to CTAs in contiguous ranges, so a CTA loads a
-// head's Q once.
+// 256-row B operand.  TMEM (512 columns): STATS four 128-column accumulator
+// slots (each epilogue warp group double-buffers), SCORE two 256-column slots.
+// Warp roles (352 threads): warp 0 TMA producer, warps 1-2 MMA issuers (one
+// elected lane each; they alternate jobs, warp 1 also owns the TMEM
+// allocation), warps 3-10 epilogue (warp e: TMEM lane quarter warp & 3,
+// column half of every job).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -46,45 +58,134 @@ namespace epk {
 using namespace sm100;
 
 constexpr int kD = 128;
-constexpr int kRowB = 128;        // bytes of one d-half row (64 bf16)
-constexpr int kChunk = 128;       // query rows per chunk (MMA M in P1)
-constexpr int kSplitCols = 1024;  // cache columns per item
+constexpr int kRowB = 128;   // bytes of one d-half row (64 bf16)
+constexpr int kChunk = 128;  // query rows per chunk (MMA M in P1)
 constexpr int kEpiWarps = 8;
 constexpr int kMmaWarps = 2;  // MMA issuers alternate jobs: one issues while the other synchronises
 constexpr int kThreads = 32 * (1 + kMmaWarps + kEpiWarps);
-constexpr int kMaxQRes = 4;       // resident query chunks (P1: per chunk group)
+constexpr int kMaxQRes = 4;  // resident query chunks (P1: per chunk group)
 
 enum { MODE_STATS = 0, MODE_SCORE = 1 };
 
 struct TcParams {
     LayerTable lt;
     int L, H, Hq, G, p, Gp, NQ;
-    int splits;        // ceil(n_max / 1024)
-    int cgroups;       // STATS: query-chunk groups
-    int cg_chunks;     // STATS: chunks per group
-    int krows;         // K stage rows: 256 (STATS) / 128 (SCORE)
-    int kstages;       // K ring depth
-    int qcap;          // rows per d-half in the Q region
-    int resident;      // SCORE: all query chunks resident (else streamed pairs)
+    int cgroups;    // STATS query-chunk groups (SCORE: P1's, for the merge)
+    int cg_chunks;  // chunks per group
+    int krows;      // K tile rows: 256 (STATS) / 128 (SCORE)
+    int kstages;    // K ring depth
+    int qcap;       // rows per d-half in the Q region
+    int resident;   // SCORE: all query chunks resident (else streamed pairs)
+    int runs;       // runs of this launch
+    int ptiles;     // STATS: causal prompt tiles per run
+    int p1_grid;    // STATS grid (SCORE reads it to locate the partials)
+    int p1_runs;    // STATS runs
+    int slots;      // partial slots per query row (2 per STATS CTA)
     const int32_t* head_off;
     const int32_t* head_len;
-    float c2;       // d^-1/2 * log2(e)
-    float* part_m;  // [L*H*NQ*128][2*splits]
+    int32_t* p1_pre;  // [p1_runs + 1] STATS run prefix (written by STATS CTA 0)
+    float c2;         // d^-1/2 * log2(e)
+    float* part_m;    // [L*H*NQ*128][slots]
     float* part_z;
-    float* lse2;  // [L*H*NQ*128]
     float* scores;
     int agg_max;
-    int64_t items;
-    unsigned long long* trace;  // diagnostics (EPK_TC_TRACE): CTA 0 timeline records
+    // SCORE, fused selection histogram (threshold select, select.cu): per
+    // live row its order-preserving key, and per layer a 65536-bin histogram
+    // of float_bits(score) >> 14 plus a 256-bin coarse one (bin >> 8).
+    uint32_t* keys;         // [rows] or null
+    uint32_t* hist_fine;    // [L][65536]
+    uint32_t* hist_coarse;  // [L][256]
 };
 
-// Timeline record for CTA 0: per-role private regions of 60000 records,
-// plain stores (no atomics): (event << 56) | clock low 56 bits.
-#define EPK_TRACE(P, role, ev)                                                                          \
-    do {                                                                                                \
-        if ((P).trace && blockIdx.x == 0 && tr_n < 60000)                                               \
-            (P).trace[1 + (role) * 60000 + tr_n++] = (uint64_t(ev) << 56) | (uint64_t(clock64()) & 0xFFFFFFFFFFFFFFull); \
-    } while (0)
+// ---- tile-balanced partition ------------------------------------------------
+// CTA b owns global tiles [B(b), B(b+1)), B(b) = floor(T b / grid).
+__device__ __forceinline__ int part_bound(int64_t T, int grid, int b) { return int(T * b / grid); }
+// number of CTAs b in [0, grid) with B(b) <= x  (the CTA holding tile x is cnt(x) - 1)
+__device__ __forceinline__ int part_cnt(int64_t T, int grid, int64_t x) {
+    return int(min(int64_t(grid), ((x + 1) * grid + T - 1) / T));
+}
+
+template <int MODE>
+__device__ __forceinline__ int run_tiles(const TcParams& P, int r) {
+    if (MODE == MODE_STATS) {
+        const int n = P.head_len[r / P.cgroups];
+        return n > 0 ? (n + 127) / 128 + P.ptiles : 0;
+    }
+    return (P.head_len[r] + 127) / 128;
+}
+
+// Exclusive prefix of run tiles into s_pre[0..runs] (warp 0).
+template <int MODE>
+__device__ void run_prefix(const TcParams& P, int32_t* s_pre) {
+    const int lane = threadIdx.x & 31;
+    const int per = (P.runs + 31) / 32;
+    const int a = min(P.runs, lane * per), b = min(P.runs, a + per);
+    int sum = 0;
+    for (int i = a; i < b; ++i) sum += run_tiles<MODE>(P, i);
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    int run = incl - sum;
+    for (int i = a; i < b; ++i) {
+        s_pre[i] = run;
+        run += run_tiles<MODE>(P, i);
+    }
+    if (lane == 31) s_pre[P.runs] = incl;
+}
+
+struct Seg {
+    int r, hk, l, h, cg;
+    int n_h;
+    int64_t krow0;       // first K row of the head (global)
+    int t0, nc, np, p0;  // first cache tile, cache tiles, prompt tiles, first prompt tile
+    int c0, nq;          // first query chunk, chunks
+    int slot;            // STATS: 2 * (this CTA - first CTA of the run)
+    __device__ int ntiles() const { return nc + np; }
+};
+
+// The segment of this CTA's range that starts at global tile g.
+template <int MODE>
+__device__ __forceinline__ Seg seg_at(const TcParams& P, const int32_t* s_pre, int g, int g_end, int64_t T) {
+    int lo = 0, hi = P.runs - 1;
+    while (lo < hi) {  // last run with s_pre[r] <= g (skips empty runs)
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_pre[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    Seg x;
+    x.r = lo;
+    const int R0 = s_pre[lo], R1 = s_pre[lo + 1];
+    const int ta = g - R0, tb = min(R1, g_end) - R0;
+    if (MODE == MODE_STATS) {
+        x.hk = lo / P.cgroups;
+        x.cg = lo % P.cgroups;
+    } else {
+        x.hk = lo;
+        x.cg = 0;
+    }
+    x.l = x.hk / P.H;
+    x.h = x.hk % P.H;
+    x.n_h = P.head_len[x.hk];
+    x.krow0 = P.lt.base[x.l] + P.head_off[x.l * (P.H + 1) + x.h];
+    const int ntc = (x.n_h + P.krows - 1) / P.krows;
+    x.t0 = ta;
+    x.nc = max(0, min(tb, ntc) - ta);
+    const int pa = max(ta, ntc);
+    x.np = max(0, tb - pa);
+    x.p0 = pa - ntc;
+    if (MODE == MODE_STATS) {
+        x.c0 = x.cg * P.cg_chunks;
+        x.nq = min(P.cg_chunks, P.NQ - x.c0);
+        x.slot = 2 * (int(blockIdx.x) - (part_cnt(T, gridDim.x, R0) - 1));
+    } else {
+        x.c0 = 0;
+        x.nq = P.NQ;
+        x.slot = 0;
+    }
+    return x;
+}
 
 // D (+)= A * B^T over K = 128: 8 K-steps of 16 across the two 64-wide
 // d-halves.  a_half / b_half: byte distance between the operands' d-halves.
@@ -107,46 +208,6 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, uint32_t half_bytes, con
                                           int row) {
     tma_load_2d(dst, map, bar, 0, row);
     tma_load_2d(dst + half_bytes, map, bar, 64, row);
-}
-
-struct Item {
-    int l, h, s, cg;
-    int n_h;
-    int64_t krow0;   // first K row of the head (global)
-    int t0, nc, np;  // first cache tile, cache tiles, prompt tiles (tiles of krows)
-    int c0, nq;      // first query chunk, chunks
-    __device__ int ntiles() const { return nc + np; }
-    __device__ int64_t qkey() const { return (int64_t(l) * 4096 + h) * 64 + cg; }
-};
-
-template <int MODE>
-__device__ __forceinline__ Item decode(const TcParams& P, int64_t it) {
-    Item x;
-    if (MODE == MODE_STATS) {
-        x.cg = int(it % P.cgroups);
-        it /= P.cgroups;
-    } else {
-        x.cg = 0;
-    }
-    x.s = int(it % P.splits);
-    const int64_t r = it / P.splits;
-    x.h = int(r % P.H);
-    x.l = int(r / P.H);
-    x.n_h = P.head_len[x.l * P.H + x.h];
-    x.krow0 = P.lt.base[x.l] + P.head_off[x.l * (P.H + 1) + x.h];
-    const int per = kSplitCols / P.krows;
-    const int tiles = (x.n_h + P.krows - 1) / P.krows;
-    x.t0 = x.s * per;
-    x.nc = max(0, min(tiles, x.t0 + per) - x.t0);
-    x.np = (MODE == MODE_STATS && x.s == P.splits - 1) ? (P.p + P.krows - 1) / P.krows : 0;
-    if (MODE == MODE_STATS) {
-        x.c0 = x.cg * P.cg_chunks;
-        x.nq = min(P.cg_chunks, P.NQ - x.c0);
-    } else {
-        x.c0 = 0;
-        x.nq = P.NQ;
-    }
-    return x;
 }
 
 // SCORE epilogue on W columns of one cache row (query rows r0 .. r0+W):
@@ -187,8 +248,10 @@ __device__ __forceinline__ void score_cols(const float (&v)[W], const float* lse
 }
 
 // STATS epilogue on W columns of one query row, `lim` of them valid:
-// online (max, sum 2^(x c2 - max)) update of (m, z).
-template <int W>
+// online (max, sum 2^(x c2 - max)) update of (m, z).  Pairs of columns go
+// through FFMA2/FADD2; POLY of every 4 pairs take their exp2 on the FMA pipe
+// (exp2_poly2) so the SFU -- the bound of this pass -- carries only the rest.
+template <int W, int POLY>
 __device__ __forceinline__ void stats_cols(float (&v)[W], int lim, float c2, float& m, float& z) {
     float mx = -INFINITY;
     if (lim >= W) {
@@ -207,20 +270,107 @@ __device__ __forceinline__ void stats_cols(float (&v)[W], int lim, float c2, flo
         m = mx;
     }
     if (m != -INFINITY) {
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        const uint64_t c2x2 = f2_pack(c2, c2), nm2 = f2_pack(-m, -m);
+        uint64_t acc0 = f2_pack(0.f, 0.f), acc1 = acc0;
 #pragma unroll
         for (int i = 0; i < W; i += 4) {
-            s0 += ex2(fmaf(v[i], c2, -m));
-            s1 += ex2(fmaf(v[i + 1], c2, -m));
-            s2 += ex2(fmaf(v[i + 2], c2, -m));
-            s3 += ex2(fmaf(v[i + 3], c2, -m));
+            const uint64_t t0 = ffma2(f2_pack(v[i], v[i + 1]), c2x2, nm2);
+            const uint64_t t1 = ffma2(f2_pack(v[i + 2], v[i + 3]), c2x2, nm2);
+            uint64_t e[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint64_t t = q ? t1 : t0;
+                if (((i / 2 + q) & 3) >= 4 - POLY) {
+                    e[q] = exp2_poly2(t);
+                } else {
+                    float a, b;
+                    f2_unpack(t, a, b);
+                    e[q] = f2_pack(ex2(a), ex2(b));
+                }
+            }
+            acc0 = fadd2(acc0, e[0]);
+            acc1 = fadd2(acc1, e[1]);
         }
-        z += (s0 + s1) + (s2 + s3);
+        float a0, a1, b0, b1;
+        f2_unpack(acc0, a0, a1);
+        f2_unpack(acc1, b0, b1);
+        z += (a0 + a1) + (b0 + b1);
     }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr int kMaxSlots = 16;  // P1 CTAs per run held in the P2 slot list
+
+// SCORE output of one live row: the score, and (fused selection) its key and
+// histogram counts.
+__device__ __forceinline__ void emit_score(const TcParams& P, int layer, int64_t row, float sc, uint32_t* s_coarse) {
+    P.scores[row] = sc;
+    if (P.keys) {
+        P.keys[row] = desc_key(sc);
+        const uint32_t b = min(__float_as_uint(sc) >> 14, 65535u);
+        atomicAdd(&P.hist_fine[int64_t(layer) * 65536 + b], 1u);
+        atomicAdd(&s_coarse[b >> 8], 1u);
+    }
+}
+
+// Adds the CTA's coarse histogram of `layer` to the global one and clears it
+// (the 256 epilogue threads, after a barrier).
+__device__ __forceinline__ void flush_coarse(const TcParams& P, int layer, uint32_t* s_coarse, int etid) {
+    const uint32_t v = s_coarse[etid];
+    if (v) {
+        atomicAdd(&P.hist_coarse[layer * 256 + etid], v);
+        s_coarse[etid] = 0;
+    }
+}
+
+// lse2 from a row's partials at the listed slots.
+__device__ __forceinline__ float merge_slots(const float* pm, const float* pz, const int* slot, int n) {
+    float M = -INFINITY;
+    for (int i = 0; i < n; ++i) M = fmaxf(M, fmaxf(pm[slot[i]], pm[slot[i] + 1]));
+    if (M == -INFINITY) return INFINITY;
+    float Z = 0.f;
+    for (int i = 0; i < n; ++i) {
+        const float m0 = pm[slot[i]], m1 = pm[slot[i] + 1];
+        if (m0 != -INFINITY) Z += pz[slot[i]] * ex2(m0 - M);
+        if (m1 != -INFINITY) Z += pz[slot[i] + 1] * ex2(m1 - M);
+    }
+    return M + log2f(Z);
+}
+
+// lse2 of STATS query row rq of head hk from the partials of every P1 CTA
+// that covered the row's run (general path: any number of P1 CTAs).
+__device__ float merge_lse2(const TcParams& P, int hk, int rq, int64_t T1) {
+    const int cg = (rq / kChunk) / P.cg_chunks;
+    const int run = hk * P.cgroups + cg;
+    const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
+    if (R1 <= R0) return INFINITY;
+    const int b0 = part_cnt(T1, P.p1_grid, R0) - 1, b1 = part_cnt(T1, P.p1_grid, R1 - 1) - 1;
+    const int64_t row = int64_t(hk) * (P.NQ * kChunk) + rq;
+    const float* pm = P.part_m + row * P.slots;
+    const float* pz = P.part_z + row * P.slots;
+    float M = -INFINITY;
+    for (int b = b0; b <= b1; ++b) {
+        const int lo = max(R0, part_bound(T1, P.p1_grid, b)), hi = min(R1, part_bound(T1, P.p1_grid, b + 1));
+        if (lo >= hi) continue;
+        const int s = 2 * (b - b0);
+        M = fmaxf(M, fmaxf(pm[s], pm[s + 1]));
+    }
+    if (M == -INFINITY) return INFINITY;
+    float Z = 0.f;
+    for (int b = b0; b <= b1; ++b) {
+        const int lo = max(R0, part_bound(T1, P.p1_grid, b)), hi = min(R1, part_bound(T1, P.p1_grid, b + 1));
+        if (lo >= hi) continue;
+        const int s = 2 * (b - b0);
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            if (pm[s + u] != -INFINITY) Z += pz[s + u] * ex2(pm[s + u] - M);
+    }
+    return M + log2f(Z);
+}
+
+// <= 128 registers (45K of the SM's 64K) and <= kSmemBudget of shared memory,
+// so the side stream's select/compaction CTAs can co-reside with a scorer CTA.
+template <int MODE, int POLY>
+__global__ void __maxnreg__(128)
     tc_score_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kp) {
     extern __shared__ uint8_t smem_raw[];
@@ -232,50 +382,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t k_stage = 2 * k_half;
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + 2 * q_half;
-    float* s_lse = reinterpret_cast<float*>(sK + P.kstages * k_stage);     // SCORE: NQ*128 lse2
-    float* s_pair = s_lse + (MODE == MODE_SCORE ? P.NQ * kChunk : 0);     // SCORE: 128 half maxima
-    float* s_avg = s_pair + (MODE == MODE_SCORE ? kChunk : 0);            // SCORE avg: G*128 sums
+    float* s_lse = reinterpret_cast<float*>(sK + P.kstages * k_stage);  // SCORE: NQ*128 lse2
+    float* s_pair = s_lse + (MODE == MODE_SCORE ? P.NQ * kChunk : 0);  // SCORE: 128 half maxima
+    float* s_avg = s_pair + (MODE == MODE_SCORE ? kChunk : 0);         // SCORE avg: G*128 sums
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_avg + (MODE == MODE_SCORE && !P.agg_max ? P.G * kChunk : 0));
     uint64_t* k_full = bars;
     uint64_t* k_empty = k_full + P.kstages;
     uint64_t* q_full = k_empty + P.kstages;  // per resident chunk, or per streamed pair slot
     uint64_t* q_empty = q_full + kMaxQRes;
     uint64_t* t_full = q_empty + kMaxQRes;
-    uint64_t* t_empty = t_full + 2;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 2);
+    uint64_t* t_empty = t_full + 4;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 4);
+    int32_t* s_pre = reinterpret_cast<int32_t*>(tmem_holder + 4);  // [runs + 1]
 
+    __shared__ int s_slot[16 * kMaxSlots];  // SCORE: P1 slot lists per chunk group
+    __shared__ int s_nslot[16];
+    __shared__ uint32_t s_coarse[256];      // SCORE: coarse histogram of the current layer
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t per = (P.items + gridDim.x - 1) / gridDim.x;
-    const int64_t it_beg = int64_t(blockIdx.x) * per;
-    const int64_t it_end = min(P.items, it_beg + per);
     const bool resident = MODE == MODE_STATS || P.resident;
-    int tr_n = 0;  // EPK_TRACE record count of this thread
 
-    if (warp == 0 && lane == 0) {
-        tma_prefetch(&tm_k);
-        tma_prefetch(&tm_q);
-        if (MODE == MODE_STATS) tma_prefetch(&tm_kp);
-        for (int s = 0; s < P.kstages; ++s) {
-            mbar_init(&k_full[s], 1);
-            mbar_init(&k_empty[s], kMmaWarps);  // every MMA warp releases every stage
+    if (warp == 0) {
+        run_prefix<MODE>(P, s_pre);
+        if (lane == 0) {
+            tma_prefetch(&tm_k);
+            tma_prefetch(&tm_q);
+            if (MODE == MODE_STATS) tma_prefetch(&tm_kp);
+            for (int s = 0; s < P.kstages; ++s) {
+                mbar_init(&k_full[s], 1);
+                mbar_init(&k_empty[s], kMmaWarps);  // every MMA warp releases every stage
+            }
+            for (int s = 0; s < kMaxQRes; ++s) {
+                mbar_init(&q_full[s], 1);
+                mbar_init(&q_empty[s], resident ? kMmaWarps : 1);  // streamed slots belong to one MMA warp
+            }
+            for (int s = 0; s < 4; ++s) {
+                mbar_init(&t_full[s], 1);
+                // STATS: a slot is drained by the 4 warps of its job parity;
+                // SCORE: by all 8 (two column halves)
+                mbar_init(&t_empty[s], MODE == MODE_STATS ? kEpiWarps / 2 : kEpiWarps);
+            }
+            fence_barrier_init();
         }
-        for (int s = 0; s < kMaxQRes; ++s) {
-            mbar_init(&q_full[s], 1);
-            mbar_init(&q_empty[s], resident ? kMmaWarps : 1);  // streamed slots belong to one MMA warp
-        }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&t_full[s], 1);
-            mbar_init(&t_empty[s], kEpiWarps);
-        }
-        fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_holder, 512);
     if (MODE == MODE_SCORE && !P.agg_max)
         for (int i = threadIdx.x; i < P.G * kChunk; i += blockDim.x) s_avg[i] = 0.f;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_coarse[i] = 0;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
+    const int64_t T = s_pre[P.runs];
+    if (MODE == MODE_STATS && blockIdx.x == 0)
+        for (int i = threadIdx.x; i <= P.runs; i += blockDim.x) P.p1_pre[i] = s_pre[i];
+    const int it_beg = part_bound(T, gridDim.x, blockIdx.x);
+    const int it_end = part_bound(T, gridDim.x, blockIdx.x + 1);
 
     if (warp == 0) {
         const bool leader = elect_one_sync();
@@ -283,14 +444,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             int ks = 0;
             uint32_t kph = 0;
             uint32_t qload[kMaxQRes] = {0, 0, 0, 0};
-            int64_t key = -1, pj = 0;
+            int key = -1;
+            int64_t pj = 0;
             const int npairs = (P.NQ + 1) / 2;
-            for (int64_t it = it_beg; it < it_end; ++it) {
-                const Item x = decode<MODE>(P, it);
-                if (x.ntiles() == 0) continue;
+            for (int g = it_beg; g < it_end;) {
+                const Seg x = seg_at<MODE>(P, s_pre, g, it_end, T);
+                g += x.ntiles();
                 const int qrow0 = (x.l * P.Hq + x.h * P.G) * P.p;
-                if (resident && x.qkey() != key) {
-                    key = x.qkey();
+                if (resident && x.r != key) {
+                    key = x.r;
                     for (int c = 0; c < x.nq; ++c) {
                         mbar_wait(&q_empty[c], (qload[c] & 1) ^ 1);
                         if (leader) {
@@ -302,9 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
-                    if (leader) EPK_TRACE(P, 0, 1);
                     mbar_wait(&k_empty[ks], kph ^ 1);
-                    if (leader) EPK_TRACE(P, 0, 2);
                     if (leader) {
                         mbar_expect_tx(&k_full[ks], k_stage);
                         if (t < x.nc)
@@ -312,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       int(x.krow0 + int64_t(x.t0 + t) * P.krows));
                         else
                             load_rows(sK + ks * k_stage, k_half, &tm_kp, &k_full[ks],
-                                      (x.l * P.H + x.h) * P.p + (t - x.nc) * P.krows);
+                                      (x.l * P.H + x.h) * P.p + (x.p0 + t - x.nc) * P.krows);
                     }
                     __syncwarp();
                     if (++ks == P.kstages) {
@@ -339,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp <= kMmaWarps) {
         // MMA warp mw issues the jobs with (job & 1) == mw into TMEM slot mw;
-        // both walk the same item/tile sequence and both release every K stage.
+        // both walk the same segment/tile sequence and both release every K stage.
         const uint32_t mw = uint32_t(warp - 1);
         const bool leader = elect_one_sync();
         {  // ------------------------- MMA issuers (warp-wide, one lane issues) ------------
@@ -347,26 +507,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t kph = 0;
             uint32_t qload[kMaxQRes] = {0, 0, 0, 0};
             uint32_t job = 0;
-            int64_t key = -1;
+            int key = -1;
             int held = 0;
             const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK);
-            const bool tr = leader && mw == 0;
-            for (int64_t it = it_beg; it < it_end; ++it) {
-                const Item x = decode<MODE>(P, it);
-                if (x.ntiles() == 0) continue;
+            for (int g = it_beg; g < it_end;) {
+                const Seg x = seg_at<MODE>(P, s_pre, g, it_end, T);
+                g += x.ntiles();
                 bool fresh = false;
-                if (resident && x.qkey() != key) {
+                if (resident && x.r != key) {
                     if (leader)
                         for (int c = 0; c < held; ++c) mma_commit(&q_empty[c]);  // old Q retires with its MMAs
                     __syncwarp();
-                    key = x.qkey();
+                    key = x.r;
                     held = x.nq;
                     fresh = true;
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
-                    if (tr) EPK_TRACE(P, 1, 3);
                     mbar_wait(&k_full[ks], kph);
-                    if (tr) EPK_TRACE(P, 1, 4);
                     const uint32_t kst = k0 + uint32_t(ks) * k_stage;
                     if (MODE == MODE_STATS) {
                         for (int c = 0; c < x.nq; ++c, ++job) {
@@ -375,12 +532,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ++qload[c];
                             }
                             if ((job & 1) != mw) continue;
-                            const int ts = int(mw);
-                            mbar_wait(&t_empty[ts], ((job >> 1) & 1) ^ 1);
+                            const int ts = int(job & 3);  // four 128-column slots
+                            mbar_wait(&t_empty[ts], ((job >> 2) & 1) ^ 1);
                             tc_fence_after();
                             if (leader) {
-                                mma_128xN(tmem + uint32_t(ts * 256), q0 + uint32_t(c * kChunk * kRowB), q_half, kst,
-                                          k_half, idesc_bf16_f32(128, 256));
+                                mma_128xN(tmem + uint32_t(ts * 128), q0 + uint32_t(c * kChunk * kRowB), q_half, kst,
+                                          k_half, idesc_bf16_f32(128, 128));
                                 mma_commit(&t_full[ts]);
                             }
                             __syncwarp();
@@ -404,9 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 qb = q0 + uint32_t(slot * 2 * kChunk * kRowB);
                             }
                             const int ts = int(mw);
-                            if (tr) EPK_TRACE(P, 1, 5);
                             mbar_wait(&t_empty[ts], ((job >> 1) & 1) ^ 1);
-                            if (tr) EPK_TRACE(P, 1, 6);
                             tc_fence_after();
                             if (leader) {
                                 mma_128xN(tmem + uint32_t(ts * 256), kst, k_half, qb, q_half,
@@ -415,7 +570,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 if (!resident) mma_commit(&q_empty[slot]);
                             }
                             __syncwarp();
-                            if (tr) EPK_TRACE(P, 1, 7);
                         }
                     }
                     if (leader) mma_commit(&k_empty[ks]);
@@ -435,10 +589,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
         const int etid = e * 32 + lane;
         uint32_t job = 0;
-        int64_t lkey = -1;
+        int lkey = -1;
         const float inv_p = 1.0f / float(P.p);
-        for (int64_t it = it_beg; it < it_end; ++it) {
-            const Item x = decode<MODE>(P, it);
+        const int64_t T1 = MODE == MODE_SCORE ? int64_t(P.p1_pre[P.p1_runs]) : 0;
+        for (int g = it_beg; g < it_end;) {
+            const Seg x = seg_at<MODE>(P, s_pre, g, it_end, T);
+            g += x.ntiles();
             if (MODE == MODE_STATS) {
                 float m[kMaxQRes], z[kMaxQRes];
 #pragma unroll
@@ -446,50 +602,86 @@ __global__ void __launch_bounds__(kThreads, 1)
                     m[c] = -INFINITY;
                     z[c] = 0.f;
                 }
+                // Warps of parity `half` take the jobs (tile, chunk) with
+                // (job & 1) == half -- i.e. TMEM slot `half` -- whole (128
+                // columns), so the two epilogue warps sharing an SM
+                // sub-partition work on different jobs and their max / exp2
+                // phases interleave on the SFU.
                 for (int t = 0; t < x.ntiles(); ++t) {
 #pragma unroll
                     for (int c = 0; c < kMaxQRes; ++c) {
                         if (c >= x.nq) break;
+                        if (int(job & 1) != half) {
+                            ++job;
+                            continue;
+                        }
                         const int rq = (x.c0 + c) * kChunk + r_local;  // query row of the head (g*p + t)
                         int lim;  // valid columns of this job from its first column
                         if (t < x.nc)
                             lim = x.n_h - (x.t0 + t) * P.krows;
                         else
-                            lim = min(P.p, rq % P.p + 1) - (t - x.nc) * P.krows;
-                        const int ts = int(job & 1);
-                        mbar_wait(&t_full[ts], (job >> 1) & 1);
+                            lim = min(P.p, rq % P.p + 1) - (x.p0 + t - x.nc) * P.krows;
+                        const int ts = int(job & 3);
+                        mbar_wait(&t_full[ts], (job >> 2) & 1);
                         tc_fence_after();
                         {
-                            float v[128];
-                            tmem_ld128(tmem + lane_addr + uint32_t(ts * 256 + half * 128), v);
+                            float v[64];
+                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 128), v);
+                            stats_cols<64, POLY>(v, lim, P.c2, m[c], z[c]);
+                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 128 + 64), v);
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&t_empty[ts]);  // slot free: values are in registers
-                            stats_cols<128>(v, lim - half * 128, P.c2, m[c], z[c]);
+                            stats_cols<64, POLY>(v, lim - 64, P.c2, m[c], z[c]);
                         }
                         ++job;
                     }
                 }
-                // partial (m, Z) of this column half for each query row of the item
+                // partial (m, Z) of this column half for each query row of the segment
 #pragma unroll
                 for (int cc = 0; cc < kMaxQRes; ++cc) {
                     if (cc < x.nq) {
                         const int rq = (x.c0 + cc) * kChunk + r_local;
-                        const int64_t o = ((int64_t(x.l) * P.H + x.h) * (P.NQ * kChunk) + rq) * (2 * P.splits) +
-                                          2 * x.s + half;
+                        const int64_t o = (int64_t(x.hk) * (P.NQ * kChunk) + rq) * P.slots + x.slot + half;
                         P.part_m[o] = m[cc];
                         P.part_z[o] = z[cc];
                     }
                 }
             } else {
-                if (x.ntiles() == 0) continue;
-                const int64_t hk = int64_t(x.l) * P.H + x.h;
-                if (hk != lkey) {  // the head's lse2 (all 8 warps)
+                if (x.hk != lkey) {  // the head's lse2 from the P1 partials (all 8 warps)
                     named_bar_sync(1, 32 * kEpiWarps);
-                    for (int r = etid; r < P.NQ * kChunk; r += 32 * kEpiWarps)
-                        s_lse[r] = P.lse2[hk * (P.NQ * kChunk) + r];
+                    if (P.keys && lkey >= 0 && lkey / P.H != x.l) flush_coarse(P, lkey / P.H, s_coarse, etid);
+                    if (etid < P.cgroups) {  // slot list of each P1 run (head, chunk group)
+                        const int run = x.hk * P.cgroups + etid;
+                        const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
+                        int n = 0;
+                        if (R1 > R0) {
+                            const int b0 = part_cnt(T1, P.p1_grid, R0) - 1, b1 = part_cnt(T1, P.p1_grid, R1 - 1) - 1;
+                            for (int b = b0; b <= b1 && n >= 0; ++b) {
+                                const int lo = max(R0, part_bound(T1, P.p1_grid, b));
+                                const int hi = min(R1, part_bound(T1, P.p1_grid, b + 1));
+                                if (lo >= hi) continue;
+                                if (n == kMaxSlots) n = -1;  // too many: rows take the general path
+                                else s_slot[etid * kMaxSlots + n++] = 2 * (b - b0);
+                            }
+                        }
+                        s_nslot[etid] = n;
+                    }
                     named_bar_sync(1, 32 * kEpiWarps);
-                    lkey = hk;
+                    for (int r = etid; r < P.NQ * kChunk; r += 32 * kEpiWarps) {
+                        float v = INFINITY;
+                        if (r < P.Gp) {
+                            const int cg = (r / kChunk) / P.cg_chunks;
+                            const int n = s_nslot[cg];
+                            const int64_t row = int64_t(x.hk) * (P.NQ * kChunk) + r;
+                            v = n >= 0 ? merge_slots(P.part_m + row * P.slots, P.part_z + row * P.slots,
+                                                     s_slot + cg * kMaxSlots, n)
+                                       : merge_lse2(P, x.hk, r, T1);
+                        }
+                        s_lse[r] = v;
+                    }
+                    named_bar_sync(1, 32 * kEpiWarps);
+                    lkey = x.hk;
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
                     float best = -INFINITY;
@@ -497,37 +689,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int ncols = min(2, x.nq - 2 * j) * kChunk;  // query rows of the job
                         const int hw = ncols / 2;                         // columns per warp half
                         const int ts = int(job & 1);
-                        if (lane == 0 && e == 0) EPK_TRACE(P, 2, 8);
                         mbar_wait(&t_full[ts], (job >> 1) & 1);
-                        if (lane == 0 && e == 0) EPK_TRACE(P, 2, 9);
                         tc_fence_after();
                         const int r0 = 2 * j * kChunk + half * hw;  // first query row of this warp's columns
                         if (hw == 128) {
-                            float v[128];
-                            tmem_ld128(tmem + lane_addr + uint32_t(ts * 256 + half * hw), v);
+                            float v[64];
+                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + half * hw), v);
+                            score_cols<64>(v, s_lse + r0, r0, P, best, s_avg, r_local);
+                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + half * hw + 64), v);
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&t_empty[ts]);  // slot free: values are in registers
-                            if (lane == 0 && e == 0) EPK_TRACE(P, 2, 10);
-                            score_cols<128>(v, s_lse + r0, r0, P, best, s_avg, r_local);
+                            score_cols<64>(v, s_lse + r0 + 64, r0 + 64, P, best, s_avg, r_local);
                         } else {
                             float v[64];
                             tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + half * hw), v);
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&t_empty[ts]);
-                            if (lane == 0 && e == 0) EPK_TRACE(P, 2, 10);
                             score_cols<64>(v, s_lse + r0, r0, P, best, s_avg, r_local);
                         }
                         ++job;
                     }
-                    if (lane == 0 && e == 0) EPK_TRACE(P, 2, 11);
                     // combine the two column halves of each cache row
                     const int jrow = (x.t0 + t) * P.krows + r_local;
                     if (P.agg_max) {
                         if (half == 1) s_pair[r_local] = best;
                         named_bar_sync(2 + quarter, 64);
-                        if (half == 0 && jrow < x.n_h) P.scores[x.krow0 + jrow] = ex2(fmaxf(best, s_pair[r_local]));
+                        if (half == 0 && jrow < x.n_h)
+                            emit_score(P, x.l, x.krow0 + jrow, ex2(fmaxf(best, s_pair[r_local])), s_coarse);
                         named_bar_sync(2 + quarter, 64);
                     } else {
                         named_bar_sync(2 + quarter, 64);
@@ -537,40 +727,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 b = fmaxf(b, s_avg[gg * kChunk + r_local] * inv_p);
                                 s_avg[gg * kChunk + r_local] = 0.f;
                             }
-                            if (jrow < x.n_h) P.scores[x.krow0 + jrow] = b;
+                            if (jrow < x.n_h) emit_score(P, x.l, x.krow0 + jrow, b, s_coarse);
                         }
                         named_bar_sync(2 + quarter, 64);
                     }
                 }
             }
         }
+        if (MODE == MODE_SCORE && P.keys && lkey >= 0) {  // last layer's coarse histogram
+            named_bar_sync(1, 32 * kEpiWarps);
+            flush_coarse(P, lkey / P.H, s_coarse, etid);
+        }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == 1) tmem_dealloc(tmem, 512);
-}
-
-// lse2 per query row = log2 sum_s Z_s 2^(m_s - M) + M over the partials.
-__global__ void tc_merge_kernel(const __grid_constant__ TcParams P) {
-    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t rows = int64_t(P.L) * P.H * P.NQ * kChunk;
-    if (idx >= rows) return;
-    const int rq = int(idx % (P.NQ * kChunk));
-    if (rq >= P.Gp) {
-        P.lse2[idx] = INFINITY;
-        return;
-    }
-    const int np = 2 * P.splits;
-    float M = -INFINITY;
-    for (int s = 0; s < np; ++s) M = fmaxf(M, P.part_m[idx * np + s]);
-    float Z = 0.f;
-    if (M != -INFINITY)
-        for (int s = 0; s < np; ++s) {
-            const float ms = P.part_m[idx * np + s];
-            if (ms != -INFINITY) Z += P.part_z[idx * np + s] * ex2(ms - M);
-        }
-    P.lse2[idx] = M + log2f(Z);
 }
 
 // ---------------------------------------------------------------------------
@@ -605,11 +777,12 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int box_rows
 static int smem_bytes(const TcParams& P, int mode) {
     return 1024 + 2 * P.qcap * kRowB + P.kstages * 2 * P.krows * kRowB +
            (mode == MODE_SCORE ? (P.NQ + 1 + (P.agg_max ? 0 : P.G)) * kChunk * 4 : 0) +
-           (2 * P.kstages + 2 * kMaxQRes + 4) * 8 + 16;
+           (2 * P.kstages + 2 * kMaxQRes + 8) * 8 + 16 + (P.runs + 1) * 4;
 }
 
 int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const void* kp, int hq, int p, int agg_max,
-                    int64_t n_max, float* scores) {
+                    int64_t n_max, float* scores, const FusedSelect* fs) {
+    (void)n_max;  // the tile partition reads the live head lengths on the device
     if (c->dtype != EPK_BF16) return fail(EPK_ERR_ARG, "score(tensor core): cache dtype must be BF16");
     if (c->head_dim != kD) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): head_dim must be 128");
     const int H = c->kv_heads;
@@ -626,116 +799,123 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     P.Gp = P.G * p;
     P.NQ = (P.Gp + kChunk - 1) / kChunk;
     if (P.NQ > 16) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): group*prompt_len must be <= 2048");
-    P.splits = int(std::max<int64_t>(1, (n_max + kSplitCols - 1) / kSplitCols));
+    if (int64_t(P.L) * H * 16 > (1 << 20)) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): too many heads");
     P.head_off = c->head_off;
     P.head_len = c->head_len;
     P.c2 = float((1.0 / std::sqrt(double(kD))) * 1.4426950408889634);
     P.scores = scores;
     P.agg_max = agg_max;
-    P.trace = nullptr;
-    static unsigned long long* trace_buf = nullptr;
-    if (std::getenv("EPK_TC_TRACE")) {
-        if (!trace_buf) EPK_CUDA_CHECK(cudaMalloc(&trace_buf, 8 * 180001));
-        EPK_CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, 8 * 180001, ctx->stream));
-        P.trace = trace_buf;
-    }
-    const int64_t rows = int64_t(P.L) * H * P.NQ * kChunk;
-    rc = ws_require(ctx, rows * 2 * P.splits * 8 + rows * 4 + 4096);
-    if (rc) return rc;
-    WsCarver carve(ctx->ws);
-    P.part_m = carve.take<float>(rows * 2 * P.splits);
-    P.part_z = carve.take<float>(rows * 2 * P.splits);
-    P.lse2 = carve.take<float>(rows);
+    P.keys = fs ? fs->keys : nullptr;
+    P.hist_fine = fs ? fs->hist_fine : nullptr;
+    P.hist_coarse = fs ? fs->hist_coarse : nullptr;
+    P.ptiles = (p + 127) / 128;
+    const int grid = ctx->num_sms;  // persistent: one CTA per SM, tile-balanced ranges
 
     // Dynamic shared memory limit: the per-block opt-in maximum minus the
     // kernel's static/reserved shared memory.
+    // STATS kernels by exp2 split (POLY of every 4 column pairs on the FMA
+    // pipe); EPK_TC_POLY picks one (default 0: measured on B200 the FFMA2
+    // polynomial costs more issue than the SFU time it saves).
+    using KernelFn = void (*)(TcParams, CUtensorMap, CUtensorMap, CUtensorMap);
+    static const KernelFn stats_fns[4] = {tc_score_kernel<MODE_STATS, 0>, tc_score_kernel<MODE_STATS, 1>,
+                                          tc_score_kernel<MODE_STATS, 2>, tc_score_kernel<MODE_STATS, 3>};
+    const KernelFn score_fn = tc_score_kernel<MODE_SCORE, 0>;
+    int poly = 0;
+    if (const char* e = std::getenv("EPK_TC_POLY")) poly = std::max(0, std::min(3, std::atoi(e)));
+    const KernelFn stats_fn = stats_fns[poly];
     static int limit = 0;
     if (!limit) {
         int optin = 0;
         EPK_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-        cudaFuncAttributes fa0, fa1;
-        EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa0, tc_score_kernel<MODE_STATS>));
-        EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa1, tc_score_kernel<MODE_SCORE>));
-        limit = optin - int(std::max(fa0.sharedSizeBytes, fa1.sharedSizeBytes));
-        EPK_CUDA_CHECK(cudaFuncSetAttribute(tc_score_kernel<MODE_STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            limit));
-        EPK_CUDA_CHECK(cudaFuncSetAttribute(tc_score_kernel<MODE_SCORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            limit));
+        size_t stat = 0;
+        for (KernelFn f : stats_fns) {
+            cudaFuncAttributes fa;
+            EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f)));
+            stat = std::max(stat, fa.sharedSizeBytes);
+        }
+        cudaFuncAttributes fa1;
+        EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa1, reinterpret_cast<const void*>(score_fn)));
+        limit = optin - int(std::max(stat, fa1.sharedSizeBytes));
+        for (KernelFn f : stats_fns)
+            EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+        EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(score_fn),
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
     }
 
+    // Shared-memory budget: leave ~30 KB of the SM for co-resident side-stream
+    // kernels (EPK_TC_SMEM_KB overrides, for experiments).
+    int budget = std::min(limit, 200 * 1024);
+    if (const char* e = std::getenv("EPK_TC_SMEM_KB")) budget = std::min(limit, std::atoi(e) * 1024);
     CUtensorMap tm_k1, tm_k2, tm_q, tm_kp;
-    if ((rc = make_map(&tm_k1, c->k, c->layer_base[c->layers], 256))) return rc;
-    if ((rc = make_map(&tm_k2, c->k, c->layer_base[c->layers], 128))) return rc;
+    CUtensorMap& tm_k = tm_k1;
+    (void)tm_k2;
+    if ((rc = make_map(&tm_k, c->k, c->layer_base[c->layers], 128))) return rc;
     if ((rc = make_map(&tm_q, q, int64_t(P.L) * hq * p, kChunk))) return rc;
-    if ((rc = make_map(&tm_kp, kp, int64_t(P.L) * H * p, 256))) return rc;
+    if ((rc = make_map(&tm_kp, kp, int64_t(P.L) * H * p, 128))) return rc;
 
-    // P1: 256-row K stages; query chunks in groups sized so two stages fit.
-    P.krows = 256;
+    // P1: 128-row K tiles (the MMA N = 128 is enough: P1 is bound by the
+    // SFU exp2 rate, not the tensor pipe); query chunks in groups sized so
+    // >= 2 K stages fit the budget.
+    P.krows = 128;
     P.resident = 1;
     P.cg_chunks = std::min(P.NQ, kMaxQRes);
     for (;;) {
+        P.cgroups = (P.NQ + P.cg_chunks - 1) / P.cg_chunks;
+        P.runs = P.L * H * P.cgroups;
         P.qcap = P.cg_chunks * kChunk;
         P.kstages = 2;
-        if (smem_bytes(P, MODE_STATS) <= limit || P.cg_chunks == 1) break;
+        if (smem_bytes(P, MODE_STATS) <= budget || P.cg_chunks == 1) break;
         --P.cg_chunks;
     }
     while (P.kstages < 4) {
         ++P.kstages;
-        if (smem_bytes(P, MODE_STATS) > limit) {
+        if (smem_bytes(P, MODE_STATS) > budget) {
             --P.kstages;
             break;
         }
     }
-    if (const char* ks = std::getenv("EPK_P1_KSTAGES")) P.kstages = std::max(1, std::min(P.kstages, std::atoi(ks)));
     if (smem_bytes(P, MODE_STATS) > limit) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
-    P.cgroups = (P.NQ + P.cg_chunks - 1) / P.cg_chunks;
-    P.items = int64_t(P.L) * H * P.splits * P.cgroups;
+    P.p1_grid = grid;
+    P.p1_runs = P.runs;
+    P.slots = 2 * grid;
+    const int64_t rows = int64_t(P.L) * H * P.NQ * kChunk;
+    rc = ws_require(ctx, 2 * rows * P.slots * 4 + int64_t(P.runs + 1) * 4 + 4096);
+    if (rc) return rc;
+    WsCarver carve(ctx->ws);
+    P.part_m = carve.take<float>(rows * P.slots);
+    P.part_z = carve.take<float>(rows * P.slots);
+    P.p1_pre = carve.take<int32_t>(P.runs + 1);
     if (std::getenv("EPK_TC_VERBOSE"))
-        fprintf(stderr, "P1: NQ=%d cg_chunks=%d kstages=%d smem=%d limit=%d items=%lld\n", P.NQ, P.cg_chunks,
-                P.kstages, smem_bytes(P, MODE_STATS), limit, (long long)P.items);
-    const int grid1 = int(std::min<int64_t>(P.items, ctx->num_sms));
+        fprintf(stderr, "P1: NQ=%d cg_chunks=%d cgroups=%d kstages=%d smem=%d limit=%d runs=%d\n", P.NQ, P.cg_chunks,
+                P.cgroups, P.kstages, smem_bytes(P, MODE_STATS), limit, P.runs);
     EPK_PROF(ctx, "p1_rowstats");
-    tc_score_kernel<MODE_STATS><<<grid1, kThreads, smem_bytes(P, MODE_STATS), ctx->stream>>>(P, tm_k1, tm_q, tm_kp);
-    EPK_LAUNCH_CHECK(ctx);
-    EPK_PROF(ctx, "p1_merge");
-    tc_merge_kernel<<<unsigned((rows + 255) / 256), 256, 0, ctx->stream>>>(P);
+    stats_fn<<<grid, kThreads, smem_bytes(P, MODE_STATS), ctx->stream>>>(P, tm_k, tm_q, tm_kp);
     EPK_LAUNCH_CHECK(ctx);
 
-    // P2: 128-row K stages; all query chunks resident when they fit, else
-    // streamed as chunk pairs through two 256-row slots.
+    // P2: 128-row K tiles; all query chunks resident when they fit, else
+    // streamed as chunk pairs through two 256-row slots.  cgroups/cg_chunks
+    // stay P1's (the merge maps query rows to P1 runs).
     P.krows = 128;
+    P.runs = P.L * H;
     P.resident = P.NQ <= kMaxQRes;
     P.qcap = P.resident ? P.NQ * kChunk : 4 * kChunk;
     P.kstages = 1;
     while (P.kstages < 4) {
         ++P.kstages;
-        if (smem_bytes(P, MODE_SCORE) > limit) {
+        if (smem_bytes(P, MODE_SCORE) > budget) {
             --P.kstages;
             break;
         }
     }
-    if (const char* ks = std::getenv("EPK_P2_KSTAGES")) P.kstages = std::max(2, std::min(P.kstages, std::atoi(ks)));
-    if (P.kstages < 2 || smem_bytes(P, MODE_SCORE) > limit)
-        return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
-    P.cgroups = 1;
-    P.cg_chunks = P.NQ;
-    P.items = int64_t(P.L) * H * P.splits;
+    if (P.kstages < 2) P.kstages = 2;  // over the co-residency budget: use the whole opt-in limit
+    if (smem_bytes(P, MODE_SCORE) > limit) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
     if (std::getenv("EPK_TC_VERBOSE"))
-        fprintf(stderr, "P2: NQ=%d resident=%d kstages=%d smem=%d items=%lld\n", P.NQ, P.resident, P.kstages,
-                smem_bytes(P, MODE_SCORE), (long long)P.items);
-    const int grid2 = int(std::min<int64_t>(P.items, ctx->num_sms));
+        fprintf(stderr, "P2: NQ=%d resident=%d kstages=%d smem=%d runs=%d\n", P.NQ, P.resident, P.kstages,
+                smem_bytes(P, MODE_SCORE), P.runs);
     EPK_PROF(ctx, "p2_colscore");
-    tc_score_kernel<MODE_SCORE><<<grid2, kThreads, smem_bytes(P, MODE_SCORE), ctx->stream>>>(P, tm_k2, tm_q, tm_kp);
+    score_fn<<<grid, kThreads, smem_bytes(P, MODE_SCORE), ctx->stream>>>(P, tm_k, tm_q, tm_kp);
     EPK_LAUNCH_CHECK(ctx);
-    if (P.trace) {  // dump CTA 0's P2 timeline
-        static std::vector<unsigned long long> h(180001);
-        EPK_CUDA_CHECK(cudaMemcpyAsync(h.data(), trace_buf, 8 * 180001, cudaMemcpyDeviceToHost, ctx->stream));
-        EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-        if (FILE* f = std::fopen(std::getenv("EPK_TC_TRACE"), "wb")) {
-            std::fwrite(h.data(), 8, h.size(), f);
-            std::fclose(f);
-        }
-    }
     return EPK_OK;
 }
 

@@ -7,26 +7,34 @@
 // per-head mode restates top_k_indices (numerics.hpp:111-125): ties to the
 // lower index.
 //
-// Algorithm: MSB-first radix select.  One 8-CTA thread-block cluster per
-// segment (layer, or (layer, head) in per-head mode); each CTA histograms the
-// 8-bit digit of its slice of the segment into shared memory with
-// warp-aggregated atomics (__match_any_sync), the cluster sums the 8
-// histograms through distributed shared memory, and every CTA derives the
-// same bucket.  After the score digits the exact threshold score key T is
-// known; if T is shared by more rows than slots remain, a second radix select
-// over the unique tiebreak (position << 8 | head) picks exactly the lowest
-// ones.  Result: the same set std::sort would give, with no sort.
-#include <cooperative_groups.h>
-
+// One lean CTA per segment (layer, or (layer, head) in per-head mode): 512
+// threads, <= 32 registers, ~20 KB of shared memory, so a select CTA can
+// co-reside with a scorer CTA and the side stream's selection overlaps the
+// next layer group's scoring.  Passes over the segment (global memory, L2
+// resident after the first):
+//   keys     every row -> its order-preserving score key (desc_key; ~0 for
+//            gap rows and pinned rows) in a key buffer; min/max of the
+//            candidate keys (their common leading bits are skipped); pinned
+//            count;
+//   radix    11-bit digit histograms of the candidates below the known
+//            prefix, until the bucket holding the k-th smallest key has at
+//            most kCap candidates (one pass for softmax scores);
+//   collect  that bucket's candidates (key, tiebreak = position << 8 | head)
+//            -> shared memory; the rest of the key bits and the tiebreak are
+//            resolved by 8-bit radix passes over the shared list;
+//   final    keep[r] = key < T || (key == T && tiebreak <= U) || pinned.
+// If the bucket never gets small (massive exact ties), the tiebreak radix runs
+// over global memory instead.  Result: the set std::sort would give.
 #include "epk_internal.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace epk {
 
-constexpr int kSelCluster = 8;
-constexpr int kSelThreads = 1024;
+constexpr int kSelThreads = 512;
+constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kMaxHeads = 64;
+constexpr int kDigit = 11;  // global radix digit (2048 bins)
+constexpr int kBins = 1 << kDigit;
+constexpr int kCap = 1024;  // candidates resolved in shared memory
 
 struct SelectParams {
     LayerTable lt;
@@ -35,6 +43,7 @@ struct SelectParams {
     const int32_t* head_len;
     const int32_t* pos;
     const void* scores;
+    void* keys;  // [rows] key buffer (u32 for fp32 scores, u64 for fp64)
     const int32_t* pins;
     int n_pins;
     int H;
@@ -42,7 +51,6 @@ struct SelectParams {
     uint8_t* keep;
     int32_t* kept_per_layer;
     int* err_flag;
-    int key_cap;  // keys of this CTA's slice cached in dynamic shared memory
 };
 
 template <typename ScoreT>
@@ -67,271 +75,417 @@ __device__ __forceinline__ bool is_pinned(const int32_t* pins, int n, int32_t p)
     return false;
 }
 
-// Finds the bucket holding the k-th smallest element (1-based) from 256
-// totals; writes (bucket, count strictly before it, count in it).
-__device__ void find_bucket(const uint32_t* tot, int64_t k, int* out_bucket, int64_t* out_before,
-                            int64_t* out_eq) {
-    const int lane = threadIdx.x & 31;
-    int64_t local[8];
-    int64_t lsum = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        local[i] = tot[lane * 8 + i];
-        lsum += local[i];
-    }
-    int64_t incl = lsum;
+template <typename KeyT>
+struct SelShared {
+    int32_t off[kMaxHeads + 1];
+    int32_t len[kMaxHeads];
+    int64_t red[kSelWarps];
+    KeyT mm[2 * kSelWarps];
+    int bucket;
+    int ncand;
+    int64_t before, eq;
+    union {
+        uint32_t hist[2][kBins];  // global radix passes (two copies: odd/even warps)
+        struct {
+            KeyT key[kCap];
+            uint64_t tb[kCap];
+            uint32_t hist[256];
+        } c;  // shared-list radix
+    } u;
+};
+
+// Block-wide: the bucket of `tot[0..nbins)` holding the k-th smallest element
+// (1-based) -> S.bucket, S.before (count strictly before), S.eq (in it).
+template <typename KeyT>
+__device__ void find_bucket(SelShared<KeyT>& S, const uint32_t* tot, int nbins, int64_t k) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (nbins + kSelThreads - 1) / kSelThreads;
+    const int b0 = tid * per;
+    int64_t mine = 0;
+    for (int i = 0; i < per; ++i)
+        if (b0 + i < nbins) mine += tot[b0 + i];
+    int64_t incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
     }
-    const int64_t excl = incl - lsum;
-    const bool mine = excl < k && k <= incl;
-    const unsigned owner = __ballot_sync(0xffffffffu, mine);
-    if (owner == 0) {  // cannot happen for a valid k; be defensive
-        if (lane == 0) {
-            *out_bucket = 255;
-            *out_before = 0;
-            *out_eq = 0;
-        }
-        return;
-    }
-    if (lane == __ffs(owner) - 1) {
+    __syncthreads();
+    if (lane == 31) S.red[warp] = incl;
+    __syncthreads();
+    int64_t excl = incl - mine;
+    for (int w = 0; w < warp; ++w) excl += S.red[w];
+    if (mine > 0 && excl < k && k <= excl + mine) {  // exactly one thread
         int64_t c = excl;
-        for (int i = 0; i < 8; ++i) {
-            if (c + local[i] >= k) {
-                *out_bucket = lane * 8 + i;
-                *out_before = c;
-                *out_eq = local[i];
+        for (int i = 0; i < per; ++i) {
+            const int64_t t = b0 + i < nbins ? tot[b0 + i] : 0;
+            if (c + t >= k) {
+                S.bucket = b0 + i;
+                S.before = c;
+                S.eq = t;
                 break;
             }
-            c += local[i];
+            c += t;
         }
     }
+    __syncthreads();
+}
+
+// The exact selection below a known key prefix: `eq` candidates match
+// (prefix, mask) with `lo` key bits still open and `k_rem` slots left among
+// them.  Global 11-bit radix passes narrow the bucket until it fits the
+// shared list (kCap), the list is resolved by 8-bit passes, and ties on the
+// threshold key T are cut by the tiebreak (position << 8 | head), giving U.
+// load4(i, k) reads group i's keys (~0 for non-candidates); tiebreak(r) of a
+// layer row; rows of group i are g0 + 4 i + u.
+template <typename KeyT, typename Load4, typename TieOf>
+__device__ __forceinline__ void radix_core(SelShared<KeyT>& S, int ngroups, Load4& load4, TieOf& tiebreak, int g0,
+                                           KeyT& prefix, KeyT& mask, int& lo, int64_t& eq, int64_t& k_rem, KeyT& T,
+                                           uint64_t& U) {
+    constexpr int kTieBits = 40;  // (position < 2^31) << 8 | head (< 256)
+    const KeyT kNone = ~KeyT(0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // ---- global radix passes until the bucket fits the shared list ----------
+    uint32_t* hist = S.u.hist[warp & 1];
+    while (lo > 0 && eq > kCap) {
+        const int hi = lo;
+        lo = hi > kDigit ? hi - kDigit : 0;
+        const KeyT dmask = (KeyT(1) << (hi - lo)) - 1;
+        for (int i = tid; i < 2 * kBins; i += blockDim.x) (&S.u.hist[0][0])[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < ngroups; i += 2 * blockDim.x) {
+            KeyT k[2][4];
+            load4(i, k[0]);
+            const bool two = i + int(blockDim.x) < ngroups;
+            if (two) load4(i + blockDim.x, k[1]);
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if ((v == 0 || two) && k[v][u] != kNone && ((k[v][u] ^ prefix) & mask) == 0)
+                        atomicAdd(&hist[int((k[v][u] >> lo) & dmask)], 1u);
+        }
+        __syncthreads();
+        for (int i = tid; i < kBins; i += blockDim.x) S.u.hist[0][i] += S.u.hist[1][i];
+        __syncthreads();
+        find_bucket(S, S.u.hist[0], int(dmask) + 1, k_rem);
+        k_rem -= S.before;
+        eq = S.eq;
+        prefix |= KeyT(S.bucket) << lo;
+        mask |= dmask << lo;
+    }
+
+    U = ~uint64_t(0);
+    if (eq <= kCap) {
+        // ---- collect the bucket's candidates into shared memory -------------
+        if (tid == 0) S.ncand = 0;
+        __syncthreads();
+        for (int ib = warp * 32; ib < ngroups; ib += blockDim.x) {  // warp-uniform
+            const int i = ib + lane;
+            KeyT k[4] = {kNone, kNone, kNone, kNone};
+            if (i < ngroups) load4(i, k);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool c = k[u] != kNone && ((k[u] ^ prefix) & mask) == 0;
+                const unsigned bal = __ballot_sync(0xffffffffu, c);
+                if (bal == 0) continue;
+                const int leader = __ffs(bal) - 1;
+                int at = 0;
+                if (lane == leader) at = atomicAdd(&S.ncand, __popc(bal));
+                at = __shfl_sync(0xffffffffu, at, leader) + __popc(bal & ((1u << lane) - 1u));
+                if (c) {
+                    S.u.c.key[at] = k[u];
+                    S.u.c.tb[at] = tiebreak(g0 + 4 * i + u);
+                }
+            }
+        }
+        __syncthreads();
+        const int n = S.ncand;  // == eq
+        // ---- remaining key bits: 8-bit radix over the shared list -----------
+        uint32_t* h2 = S.u.c.hist;
+        while (lo > 0) {
+            const int hi = lo;
+            lo = hi > 8 ? hi - 8 : 0;
+            const KeyT dmask = (KeyT(1) << (hi - lo)) - 1;
+            for (int i = tid; i < 256; i += blockDim.x) h2[i] = 0;
+            __syncthreads();
+            for (int i = tid; i < n; i += blockDim.x) {
+                const KeyT k = S.u.c.key[i];
+                if (((k ^ prefix) & mask) == 0) atomicAdd(&h2[int((k >> lo) & dmask)], 1u);
+            }
+            __syncthreads();
+            find_bucket(S, h2, int(dmask) + 1, k_rem);
+            k_rem -= S.before;
+            eq = S.eq;
+            prefix |= KeyT(S.bucket) << lo;
+            mask |= dmask << lo;
+        }
+        T = prefix;
+        // ---- tiebreak among the list's rows with key T -----------------------
+        if (eq > k_rem) {
+            uint64_t tprefix = 0, tmask = 0;
+            for (int shift = kTieBits - 8; shift >= 0; shift -= 8) {
+                for (int i = tid; i < 256; i += blockDim.x) h2[i] = 0;
+                __syncthreads();
+                for (int i = tid; i < n; i += blockDim.x) {
+                    const uint64_t tb = S.u.c.tb[i];
+                    if (S.u.c.key[i] == T && ((tb ^ tprefix) & tmask) == 0)
+                        atomicAdd(&h2[int((tb >> shift) & 0xFF)], 1u);
+                }
+                __syncthreads();
+                find_bucket(S, h2, 256, k_rem);
+                k_rem -= S.before;
+                tprefix |= uint64_t(S.bucket) << shift;
+                tmask |= uint64_t(0xFF) << shift;
+            }
+            U = tprefix;
+        }
+    } else {
+        // every key bit resolved and still more than kCap rows share key T:
+        // tiebreak radix over global memory
+        T = prefix;
+        if (eq > k_rem) {
+            uint64_t tprefix = 0, tmask = 0;
+            for (int shift = kTieBits - 8; shift >= 0; shift -= 8) {
+                for (int i = tid; i < 2 * kBins; i += blockDim.x) (&S.u.hist[0][0])[i] = 0;
+                __syncthreads();
+                for (int i = tid; i < ngroups; i += blockDim.x) {
+                    KeyT k[4];
+                    load4(i, k);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (k[u] != T) continue;
+                        const uint64_t tb = tiebreak(g0 + 4 * i + u);
+                        if (((tb ^ tprefix) & tmask) == 0) atomicAdd(&hist[int((tb >> shift) & 0xFF)], 1u);
+                    }
+                }
+                __syncthreads();
+                for (int i = tid; i < 256; i += blockDim.x) S.u.hist[0][i] += S.u.hist[1][i];
+                __syncthreads();
+                find_bucket(S, S.u.hist[0], 256, k_rem);
+                k_rem -= S.before;
+                tprefix |= uint64_t(S.bucket) << shift;
+                tmask |= uint64_t(0xFF) << shift;
+            }
+            U = tprefix;
+        }
+    }
+
 }
 
 template <typename ScoreT>
-__global__ void __cluster_dims__(kSelCluster, 1, 1) __launch_bounds__(kSelThreads, 1)
-    select_kernel(const __grid_constant__ SelectParams P) {
+__global__ void __launch_bounds__(kSelThreads, 4) select_kernel(const __grid_constant__ SelectParams P) {
     using KeyT = typename KeyOf<ScoreT>::T;
     constexpr int kKeyBits = int(sizeof(KeyT) * 8);
     constexpr int kTieBits = 40;  // (position < 2^31) << 8 | head (< 256)
+    const KeyT kNone = ~KeyT(0);  // no finite or infinite score maps to it
+    __shared__ SelShared<KeyT> S;
 
-    cg::cluster_group cluster = cg::this_cluster();
-    const int rank = int(cluster.block_rank());
-    const int seg = blockIdx.x / kSelCluster;
+    const int seg = blockIdx.x;
     const int H = P.H;
     const int layer = P.per_head ? seg / H : seg;
     const int seg_head = P.per_head ? seg % H : -1;
-
-    __shared__ int32_t s_off[kMaxHeads + 1];
-    __shared__ int32_t s_len[kMaxHeads];
-    __shared__ uint32_t s_hist[2][256];
-    __shared__ uint32_t s_tot[256];
-    __shared__ int64_t s_red[kSelThreads / 32];
-    __shared__ int s_bucket;
-    __shared__ int64_t s_before, s_eq;
-
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    constexpr int nwarps = kSelThreads / 32;
 
-    for (int i = tid; i <= H; i += blockDim.x) s_off[i] = P.head_off[layer * (H + 1) + i];
-    for (int i = tid; i < H; i += blockDim.x) s_len[i] = P.head_len[layer * H + i];
+    for (int i = tid; i <= H; i += blockDim.x) S.off[i] = P.head_off[layer * (H + 1) + i];
+    for (int i = tid; i < H; i += blockDim.x) S.len[i] = P.head_len[layer * H + i];
     __syncthreads();
 
-    // Segment row space (layer-relative rows, gaps included).
-    int64_t seg_begin, seg_end, n_live = 0;
+    // Segment row space (layer-relative rows [sb, se), gaps included).
+    int sb, se;
+    int64_t n_live = 0;
     if (P.per_head) {
-        seg_begin = s_off[seg_head];
-        seg_end = seg_begin + s_len[seg_head];
-        n_live = s_len[seg_head];
+        sb = S.off[seg_head];
+        se = sb + S.len[seg_head];
+        n_live = S.len[seg_head];
     } else {
-        seg_begin = 0;
-        seg_end = s_off[H];
-        for (int h = 0; h < H; ++h) n_live += s_len[h];
+        sb = 0;
+        se = S.off[H];
+        for (int h = 0; h < H; ++h) n_live += S.len[h];
     }
-    const int64_t span = seg_end - seg_begin;
-    const int64_t my_begin = seg_begin + span * rank / kSelCluster;
-    const int64_t my_end = seg_begin + span * (rank + 1) / kSelCluster;
     const int64_t base = P.lt.base[layer];
+    // 4-row groups aligned in global row space: group i covers layer rows
+    // [g0 + 4i, g0 + 4i + 4), g0 = (base + sb rounded down to 4) - base.
+    const int g0 = int(((base + sb) & ~int64_t(3)) - base);
+    const int ngroups = se > sb ? (se - g0 + 3) / 4 : 0;
     const ScoreT* scores = static_cast<const ScoreT*>(P.scores) + base;
+    KeyT* keys = static_cast<KeyT*>(P.keys) + base;
     const int32_t* pos = P.pos + base;
     uint8_t* keep = P.keep + base;
     const bool use_pins = !P.per_head && P.n_pins > 0;
 
-    auto head_of = [&](int64_t r) -> int {
+    auto head_of = [&](int r) -> int {
         if (P.per_head) return seg_head;
         int lo = 0, hi = H - 1;
-        while (lo < hi) {  // last h with s_off[h] <= r
+        while (lo < hi) {  // last h with off[h] <= r
             const int mid = (lo + hi + 1) >> 1;
-            if (s_off[mid] <= r) lo = mid; else hi = mid - 1;
+            if (S.off[mid] <= r) lo = mid; else hi = mid - 1;
         }
         return lo;
     };
-    auto is_live = [&](int64_t r, int h) -> bool { return r - s_off[h] < s_len[h]; };
+    auto is_live = [&](int r, int h) -> bool { return r - S.off[h] < S.len[h]; };
+    auto block_sum = [&](int64_t v) -> int64_t {
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        __syncthreads();
+        if (lane == 0) S.red[warp] = v;
+        __syncthreads();
+        int64_t t = 0;
+        for (int w = 0; w < kSelWarps; ++w) t += S.red[w];
+        __syncthreads();
+        return t;
+    };
+    auto tiebreak = [&](int r) -> uint64_t {
+        return P.per_head ? uint64_t(r) : ((uint64_t(uint32_t(pos[r])) << 8) | uint64_t(head_of(r)));
+    };
+    // Keys of group i (rows outside [sb, se) -> kNone).
+    auto load4 = [&](int i, KeyT (&k)[4]) {
+        const int r0 = g0 + 4 * i;
+        if (r0 >= sb && r0 + 4 <= se) {
+            if constexpr (sizeof(KeyT) == 4) {
+                const uint4 v = __ldcg(reinterpret_cast<const uint4*>(keys + r0));
+                k[0] = v.x;
+                k[1] = v.y;
+                k[2] = v.z;
+                k[3] = v.w;
+            } else {
+                const ulonglong2 v0 = __ldcg(reinterpret_cast<const ulonglong2*>(keys + r0));
+                const ulonglong2 v1 = __ldcg(reinterpret_cast<const ulonglong2*>(keys + r0 + 2));
+                k[0] = v0.x;
+                k[1] = v0.y;
+                k[2] = v1.x;
+                k[3] = v1.y;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) k[u] = (r0 + u >= sb && r0 + u < se) ? keys[r0 + u] : kNone;
+        }
+    };
 
-    // ---- pinned count (pooled mode with pins) -------------------------------
-    int64_t pinned_live = 0;
-    if (use_pins) {
-        int64_t c = 0;
-        for (int64_t r = my_begin + tid; r < my_end; r += blockDim.x) {
-            const int h = head_of(r);
-            if (is_live(r, h) && is_pinned(P.pins, P.n_pins, pos[r])) ++c;
+    if (P.per_head)  // gap rows after the head's live rows: never kept
+        for (int r = se + tid; r < S.off[seg_head + 1]; r += blockDim.x) keep[r] = 0;
+
+    // ---- keys (gap and pinned rows -> kNone), min/max, pinned count ---------
+    int64_t pinned_mine = 0;
+    KeyT kmin = kNone, kmax = 0;
+    for (int i = tid; i < ngroups; i += blockDim.x) {
+        const int r0 = g0 + 4 * i;
+        KeyT k[4];
+        int h = head_of(max(r0, sb));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = r0 + u;
+            k[u] = kNone;
+            if (r < sb || r >= se) continue;
+            while (!P.per_head && h + 1 < H && S.off[h + 1] <= r) ++h;
+            if (!is_live(r, h)) continue;
+            if (use_pins && is_pinned(P.pins, P.n_pins, pos[r])) {
+                ++pinned_mine;
+                continue;
+            }
+            k[u] = desc_key(__ldcg(scores + r));
+            kmin = k[u] < kmin ? k[u] : kmin;
+            kmax = k[u] > kmax ? k[u] : kmax;
         }
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) s_red[warp] = c;
-        __syncthreads();
-        if (tid == 0) {
-            int64_t t = 0;
-            for (int w = 0; w < nwarps; ++w) t += s_red[w];
-            s_hist[0][0] = uint32_t(t);
+        if (r0 >= sb && r0 + 4 <= se) {
+            if constexpr (sizeof(KeyT) == 4) {
+                *reinterpret_cast<uint4*>(keys + r0) = make_uint4(k[0], k[1], k[2], k[3]);
+            } else {
+                *reinterpret_cast<ulonglong2*>(keys + r0) = make_ulonglong2(k[0], k[1]);
+                *reinterpret_cast<ulonglong2*>(keys + r0 + 2) = make_ulonglong2(k[2], k[3]);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (r0 + u >= sb && r0 + u < se) keys[r0 + u] = k[u];
         }
-        cluster.sync();
-        if (tid == 0) {
-            int64_t t = 0;
-            for (int q = 0; q < kSelCluster; ++q) t += *cluster.map_shared_rank(&s_hist[0][0], q);
-            s_before = t;
-        }
-        cluster.sync();  // everyone has read s_hist[0][0] before it is reused
-        __syncthreads();
-        pinned_live = s_before;
     }
+    const int64_t pinned_live = use_pins ? block_sum(pinned_mine) : 0;
 
-    if (P.per_head && rank == 0)  // gap rows after the head's live rows: never kept
-        for (int64_t r = seg_end + tid; r < s_off[seg_head + 1]; r += blockDim.x) keep[r] = 0;
     const int64_t limit = P.per_head ? P.budget[layer] : int64_t(H) * P.budget[layer];
+    auto write_keep_all = [&](int mode) {  // 0: live rows, 1: nothing, 2: pinned live rows
+        for (int r = sb + tid; r < se; r += blockDim.x) {
+            uint8_t kf = 0;
+            if (mode == 0) {
+                kf = is_live(r, head_of(r)) ? 1 : 0;
+            } else if (mode == 2) {
+                kf = (is_live(r, head_of(r)) && use_pins && is_pinned(P.pins, P.n_pins, pos[r])) ? 1 : 0;
+            }
+            keep[r] = kf;
+        }
+    };
     if (n_live <= limit) {
-        for (int64_t r = my_begin + tid; r < my_end; r += blockDim.x) keep[r] = is_live(r, head_of(r)) ? 1 : 0;
-        if (rank == 0 && tid == 0 && P.kept_per_layer && !P.per_head) P.kept_per_layer[layer] = int32_t(n_live);
+        write_keep_all(0);
+        if (tid == 0 && P.kept_per_layer && !P.per_head) P.kept_per_layer[layer] = int32_t(n_live);
         return;
     }
     if (pinned_live > limit) {
-        if (tid == 0 && rank == 0) atomicCAS(P.err_flag, 0, EPK_ERR_PIN_OVERFLOW);
-        for (int64_t r = my_begin + tid; r < my_end; r += blockDim.x) keep[r] = 0;
+        if (tid == 0) atomicCAS(P.err_flag, 0, EPK_ERR_PIN_OVERFLOW);
+        write_keep_all(1);
         return;
     }
     int64_t k_rem = limit - pinned_live;
     if (k_rem == 0) {  // only the pins survive
-        for (int64_t r = my_begin + tid; r < my_end; r += blockDim.x) {
-            const int h = head_of(r);
-            keep[r] = (is_live(r, h) && use_pins && is_pinned(P.pins, P.n_pins, pos[r])) ? 1 : 0;
-        }
-        if (rank == 0 && tid == 0 && P.kept_per_layer && !P.per_head) P.kept_per_layer[layer] = int32_t(limit);
+        write_keep_all(2);
+        if (tid == 0 && P.kept_per_layer && !P.per_head) P.kept_per_layer[layer] = int32_t(limit);
         return;
     }
+    const int64_t n_cand = n_live - pinned_live;  // > k_rem > 0
 
-    // ---- this CTA's candidate keys -> shared memory (one global pass) ---------
-    // Non-candidates (gap rows, pinned rows) hold the sentinel ~0, which no
-    // finite or infinite score maps to.
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    KeyT* s_keys = reinterpret_cast<KeyT*>(s_dyn);
-    const KeyT kNone = ~KeyT(0);
-    const int64_t nmine = my_end - my_begin;
-    const bool cached = nmine <= P.key_cap;
-    auto fetch_key = [&](int64_t r) -> KeyT {
-        const int h = head_of(r);
-        if (!is_live(r, h) || (use_pins && is_pinned(P.pins, P.n_pins, pos[r]))) return kNone;
-        return desc_key(scores[r]);
-    };
-    if (cached) {
-#pragma unroll 4
-        for (int64_t i = tid; i < nmine; i += blockDim.x) s_keys[i] = fetch_key(my_begin + i);
-        __syncthreads();
+    // ---- common leading bits of the candidates ------------------------------
+    for (int o = 16; o > 0; o >>= 1) {
+        const KeyT a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
     }
-    auto key_of = [&](int64_t r) -> KeyT { return cached ? s_keys[r - my_begin] : fetch_key(r); };
+    if (lane == 0) {
+        S.mm[2 * warp] = kmin;
+        S.mm[2 * warp + 1] = kmax;
+    }
+    __syncthreads();
+    for (int w = 0; w < kSelWarps; ++w) {
+        kmin = S.mm[2 * w] < kmin ? S.mm[2 * w] : kmin;
+        kmax = S.mm[2 * w + 1] > kmax ? S.mm[2 * w + 1] : kmax;
+    }
+    const KeyT diff = kmin ^ kmax;
+    int lo = diff == 0 ? 0 : kKeyBits - (sizeof(KeyT) == 4 ? __clz(uint32_t(diff)) : __clzll(uint64_t(diff)));
+    KeyT mask = lo >= kKeyBits ? KeyT(0) : ~((KeyT(1) << lo) - 1);
+    KeyT prefix = kmin & mask;
+    int64_t eq = n_cand;  // candidates matching (prefix, mask)
 
-    // ---- radix select on the score key --------------------------------------
-    KeyT prefix = 0, mask = 0;
-    int pass = 0;
-    for (int shift = kKeyBits - 8; shift >= 0; shift -= 8, ++pass) {
-        uint32_t* hist = s_hist[pass & 1];
-        for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
-        for (int64_t b0 = my_begin + int64_t(warp) * 32; b0 < my_end; b0 += int64_t(nwarps) * 32) {
-            const int64_t r = b0 + lane;
-            int digit = 256;
-            if (r < my_end) {
-                const KeyT key = key_of(r);
-                if (key != kNone && ((key ^ prefix) & mask) == 0) digit = int((key >> shift) & 0xFF);
-            }
-            const unsigned grp = __match_any_sync(0xffffffffu, digit);
-            if (digit != 256 && lane == __ffs(grp) - 1) atomicAdd(&hist[digit], uint32_t(__popc(grp)));
-        }
-        cluster.sync();
-        if (tid < 256) {
-            uint32_t t = 0;
-            for (int q = 0; q < kSelCluster; ++q) t += cluster.map_shared_rank(hist, q)[tid];
-            s_tot[tid] = t;
-        }
-        __syncthreads();
-        if (warp == 0) find_bucket(s_tot, k_rem, &s_bucket, &s_before, &s_eq);
-        __syncthreads();
-        k_rem -= s_before;
-        prefix |= KeyT(s_bucket) << shift;
-        mask |= KeyT(0xFF) << shift;
-    }
-    const KeyT T = prefix;
-    const int64_t eq_count = s_eq;
-
-    // ---- tiebreak among rows whose score key equals T ----------------------
-    uint64_t U = ~uint64_t(0);
-    if (eq_count > k_rem) {
-        uint64_t tprefix = 0, tmask = 0;
-        for (int shift = kTieBits - 8; shift >= 0; shift -= 8, ++pass) {
-            uint32_t* hist = s_hist[pass & 1];
-            for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
-            __syncthreads();
-            for (int64_t b0 = my_begin + int64_t(warp) * 32; b0 < my_end; b0 += int64_t(nwarps) * 32) {
-                const int64_t r = b0 + lane;
-                int digit = 256;
-                if (r < my_end && key_of(r) == T) {
-                    const int h = head_of(r);
-                    {
-                        const uint64_t tb = P.per_head ? uint64_t(r) : ((uint64_t(uint32_t(pos[r])) << 8) | uint64_t(h));
-                        if (((tb ^ tprefix) & tmask) == 0) digit = int((tb >> shift) & 0xFF);
-                    }
-                }
-                const unsigned grp = __match_any_sync(0xffffffffu, digit);
-                if (digit != 256 && lane == __ffs(grp) - 1) atomicAdd(&hist[digit], uint32_t(__popc(grp)));
-            }
-            cluster.sync();
-            if (tid < 256) {
-                uint32_t t = 0;
-                for (int q = 0; q < kSelCluster; ++q) t += cluster.map_shared_rank(hist, q)[tid];
-                s_tot[tid] = t;
-            }
-            __syncthreads();
-            if (warp == 0) find_bucket(s_tot, k_rem, &s_bucket, &s_before, &s_eq);
-            __syncthreads();
-            k_rem -= s_before;
-            tprefix |= uint64_t(s_bucket) << shift;
-            tmask |= uint64_t(0xFF) << shift;
-        }
-        U = tprefix;
-    }
+    KeyT T;
+    uint64_t U;
+    radix_core<KeyT>(S, ngroups, load4, tiebreak, g0, prefix, mask, lo, eq, k_rem, T, U);
 
     // ---- write the keep mask -------------------------------------------------
-    for (int64_t r = my_begin + tid; r < my_end; r += blockDim.x) {
-        const KeyT key = key_of(r);
-        uint8_t kf = 0;
-        if (key != kNone) {
-            if (key < T) {
-                kf = 1;
-            } else if (key == T) {
-                const int h = head_of(r);
-                const uint64_t tb = P.per_head ? uint64_t(r) : ((uint64_t(uint32_t(pos[r])) << 8) | uint64_t(h));
-                kf = tb <= U ? 1 : 0;
+    for (int i = tid; i < ngroups; i += blockDim.x) {
+        const int r0 = g0 + 4 * i;
+        KeyT k[4];
+        load4(i, k);
+        uint8_t kf[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = r0 + u;
+            kf[u] = 0;
+            if (r < sb || r >= se) continue;
+            if (k[u] != kNone) {
+                if (k[u] < T) kf[u] = 1;
+                else if (k[u] == T) kf[u] = tiebreak(r) <= U ? 1 : 0;
+            } else if (use_pins) {
+                kf[u] = (is_live(r, head_of(r)) && is_pinned(P.pins, P.n_pins, pos[r])) ? 1 : 0;
             }
-        } else if (use_pins) {
-            const int h = head_of(r);
-            kf = (is_live(r, h) && is_pinned(P.pins, P.n_pins, pos[r])) ? 1 : 0;
         }
-        keep[r] = kf;
+        if (r0 >= sb && r0 + 4 <= se && (reinterpret_cast<uintptr_t>(keep + r0) & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(keep + r0) =
+                uint32_t(kf[0]) | (uint32_t(kf[1]) << 8) | (uint32_t(kf[2]) << 16) | (uint32_t(kf[3]) << 24);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (r0 + u >= sb && r0 + u < se) keep[r0 + u] = kf[u];
+        }
     }
-    if (rank == 0 && tid == 0 && P.kept_per_layer && !P.per_head) P.kept_per_layer[layer] = int32_t(limit);
-    cluster.sync();  // no CTA exits while others may still read its histograms
+    if (tid == 0 && P.kept_per_layer && !P.per_head) P.kept_per_layer[layer] = int32_t(limit);
 }
 
 int launch_select(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int score_dtype,
@@ -347,6 +501,12 @@ int launch_select(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int
         if (budgets[l] < 0) return fail(EPK_ERR_ARG, "select: negative budget");
         P.budget[l] = budgets[l];
     }
+    // key buffer: the side-stream workspace (compaction reuses it afterwards,
+    // in stream order)
+    const int64_t rows = c->layer_base[c->layers];
+    rc = ws2_require(ctx, rows * (score_dtype == EPK_F32 ? 4 : 8) + 4096);
+    if (rc) return rc;
+    P.keys = ctx->ws2;
     P.head_off = c->head_off;
     P.head_len = c->head_len;
     P.pos = c->pos;
@@ -359,20 +519,150 @@ int launch_select(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int
     P.kept_per_layer = kept;
     P.err_flag = ctx->err_flag;
     const int segs = per_head ? c->layers * c->kv_heads : c->layers;
-    dim3 grid(segs * kSelCluster), block(kSelThreads);
-    constexpr int kKeySmem = 96 * 1024;
-    static bool attr = false;
-    if (!attr) {
-        EPK_CUDA_CHECK(cudaFuncSetAttribute(select_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kKeySmem));
-        EPK_CUDA_CHECK(cudaFuncSetAttribute(select_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kKeySmem));
-        attr = true;
-    }
-    P.key_cap = kKeySmem / (score_dtype == EPK_F32 ? 4 : 8);
     EPK_PROF(ctx, per_head ? "select_per_head" : "select");
     if (score_dtype == EPK_F32)
-        select_kernel<float><<<grid, block, kKeySmem, ctx->stream>>>(P);
+        select_kernel<float><<<segs, kSelThreads, 0, ctx->stream>>>(P);
     else
-        select_kernel<double><<<grid, block, kKeySmem, ctx->stream>>>(P);
+        select_kernel<double><<<segs, kSelThreads, 0, ctx->stream>>>(P);
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Threshold select (the tensor-core step's fused path, no pins).  The scorer
+// (score_tc.cu, SCORE pass) already wrote each live row's key and counted
+// float_bits(score) >> 14 into a 65536-bin per-layer histogram (+ a 256-bin
+// coarse one).  Scores are softmax weights in [0, 1], so bin b holds exactly
+// the keys with key >> 14 == 0x1FFFF - b: the coarse and fine histograms give
+// the threshold bin and its rank in two 1 KB reads, then radix_core resolves
+// the bin's candidates.  Output per layer: thr[2l] = T | keep_all << 32,
+// thr[2l+1] = U; the compaction applies keep = key < T || (key == T &&
+// tiebreak <= U) to the live rows.  The histograms are zeroed for the next
+// step.  Bin and key prefix agree for every score in [0, 2) (bits >> 14 <
+// 65536); the scorer's softmax weights are in [0, 1] up to rounding.
+// ---------------------------------------------------------------------------
+struct ThreshParams {
+    LayerTable lt;
+    int64_t budget[kMaxLayers];
+    const int32_t* head_off;
+    const int32_t* head_len;
+    const int32_t* pos;
+    const uint32_t* keys;  // [rows] global cache rows
+    uint32_t* hist_fine;   // [layers][65536]
+    uint32_t* hist_coarse;  // [layers][256]
+    uint64_t* thr;          // [layers][2]
+    int32_t* kept_per_layer;
+    int H;
+    int* err_flag;
+};
+
+__global__ void __launch_bounds__(kSelThreads, 4) select_threshold_kernel(const __grid_constant__ ThreshParams P) {
+    using KeyT = uint32_t;
+    const KeyT kNone = ~KeyT(0);
+    __shared__ SelShared<KeyT> S;
+    __shared__ uint32_t s_tot[256];
+    const int layer = blockIdx.x;
+    const int H = P.H;
+    const int tid = threadIdx.x;
+
+    for (int i = tid; i <= H; i += blockDim.x) S.off[i] = P.head_off[layer * (H + 1) + i];
+    for (int i = tid; i < H; i += blockDim.x) S.len[i] = P.head_len[layer * H + i];
+    __syncthreads();
+    int64_t n_live = 0;
+    for (int h = 0; h < H; ++h) n_live += S.len[h];
+    const int sb = 0, se = S.off[H];
+    const int64_t base = P.lt.base[layer];
+    const int g0 = int((base & ~int64_t(3)) - base);
+    const int ngroups = se > sb ? (se - g0 + 3) / 4 : 0;
+    const KeyT* keys = P.keys + base;
+    const int32_t* pos = P.pos + base;
+    uint32_t* hf = P.hist_fine + int64_t(layer) * 65536;
+    uint32_t* hc = P.hist_coarse + layer * 256;
+    const int64_t limit = int64_t(H) * P.budget[layer];
+
+    auto head_of = [&](int r) -> int {
+        int lo = 0, hi = H - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (S.off[mid] <= r) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    };
+    auto tiebreak = [&](int r) -> uint64_t { return (uint64_t(uint32_t(pos[r])) << 8) | uint64_t(head_of(r)); };
+    // live rows only (gap rows hold stale keys)
+    auto load4 = [&](int i, KeyT (&k)[4]) {
+        const int r0 = g0 + 4 * i;
+        int h = head_of(max(r0, 0));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = r0 + u;
+            k[u] = kNone;
+            if (r < sb || r >= se) continue;
+            while (h + 1 < H && S.off[h + 1] <= r) ++h;
+            if (r - S.off[h] < S.len[h]) k[u] = __ldcg(keys + r);
+        }
+    };
+
+    uint64_t thr0, thr1 = ~uint64_t(0);
+    if (n_live <= limit) {
+        thr0 = uint64_t(1) << 32;  // keep every live row
+    } else {
+        int64_t k_rem = limit;
+        // coarse bins in key order (descending score): i -> coarse bin 255 - i
+        if (tid < 256) s_tot[tid] = __ldcg(hc + 255 - tid);
+        __syncthreads();
+        find_bucket(S, s_tot, 256, k_rem);
+        k_rem -= S.before;
+        const int cb = 255 - S.bucket;
+        __syncthreads();
+        if (tid < 256) s_tot[tid] = __ldcg(hf + cb * 256 + 255 - tid);
+        __syncthreads();
+        find_bucket(S, s_tot, 256, k_rem);
+        k_rem -= S.before;
+        const int b = cb * 256 + 255 - S.bucket;
+        int64_t eq = S.eq;
+        KeyT prefix = KeyT(0x1FFFF - b) << 14, mask = 0xFFFFC000u;
+        int lo = 14;
+        KeyT T;
+        uint64_t U;
+        radix_core<KeyT>(S, ngroups, load4, tiebreak, g0, prefix, mask, lo, eq, k_rem, T, U);
+        thr0 = T;
+        thr1 = U;
+    }
+    if (tid == 0) {
+        P.thr[2 * layer] = thr0;
+        P.thr[2 * layer + 1] = thr1;
+        if (P.kept_per_layer) P.kept_per_layer[layer] = int32_t(min(n_live, limit));
+    }
+    __syncthreads();
+    // zero the histograms for the next step
+    uint4* hf4 = reinterpret_cast<uint4*>(hf);
+    for (int i = tid; i < 65536 / 4; i += blockDim.x) hf4[i] = make_uint4(0, 0, 0, 0);
+    if (tid < 256) hc[tid] = 0;
+}
+
+int launch_select_threshold(epk_ctx* ctx, const epk_cache_desc* c, const FusedSelect* fs, const int64_t* budgets,
+                            uint64_t* thr, int32_t* kept) {
+    if (c->kv_heads > kMaxHeads) return fail(EPK_ERR_UNSUPPORTED, "select: more than 64 kv heads");
+    ThreshParams P;
+    int rc = make_layer_table(c, &P.lt);
+    if (rc) return rc;
+    for (int l = 0; l < c->layers; ++l) {
+        if (budgets[l] < 0) return fail(EPK_ERR_ARG, "select: negative budget");
+        P.budget[l] = budgets[l];
+    }
+    P.head_off = c->head_off;
+    P.head_len = c->head_len;
+    P.pos = c->pos;
+    P.keys = fs->keys;
+    P.hist_fine = fs->hist_fine;
+    P.hist_coarse = fs->hist_coarse;
+    P.thr = thr;
+    P.kept_per_layer = kept;
+    P.H = c->kv_heads;
+    P.err_flag = ctx->err_flag;
+    EPK_PROF(ctx, "select");
+    select_threshold_kernel<<<c->layers, kSelThreads, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }
