@@ -105,9 +105,14 @@ int epk_version(void);
  *                        all layers in one group)
  *   EPK_OPT_OVERLAP      1 (default): with more than one group, each group's
  *                        select + compaction runs on a second stream,
- *                        overlapping the next group's scoring */
+ *                        overlapping the next group's scoring
+ *   EPK_OPT_FUSED        0 (default) / 1: tensor-core steps without pins run as
+ *                        ONE persistent cooperative kernel (score, threshold
+ *                        select and compaction of every layer, compaction
+ *                        overlapping later layers' scoring); experimental */
 #define EPK_OPT_LAYER_GROUP 1
 #define EPK_OPT_OVERLAP 2
+#define EPK_OPT_FUSED 3
 int epk_ctx_set_option(epk_ctx* ctx, int32_t option, int64_t value);
 /* Number of kernels this library launched on the context since creation. */
 int64_t epk_ctx_launch_count(epk_ctx* ctx);

@@ -29,6 +29,7 @@ struct epk_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int layer_group = 0;  // layers per group in epk_evict_step (0 = auto: group K fits in L2)
     int overlap = 1;      // run each group's compaction on `side`
+    int fused = 0;        // EPK_OPT_FUSED: single-kernel step (step.cu) where supported
     void* step_buf = nullptr;  // epk_evict_step scores + keep mask
     int64_t step_bytes = 0;
     int* err_flag = nullptr;  // deferred device-side error code (device int)

@@ -1,0 +1,165 @@
+// tc_common.cuh -- device and host helpers shared by the tensor-core scorer
+// (score_tc.cu) and the fused step kernel (step.cu): the 128 x N x 128 bf16
+// tcgen05 MMA over SWIZZLE_128B operands, the TMA row loads, the two
+// epilogues (STATS: online max / sum exp2 per query row; SCORE: max over query
+// rows of x c2 - lse2), and the K-major bf16 tensor-map encoder.
+#pragma once
+
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <string>
+
+#include "epk_internal.cuh"
+#include "sm100.cuh"
+
+namespace epk {
+
+using namespace sm100;
+
+constexpr int kD = 128;
+constexpr int kRowB = 128;   // bytes of one d-half row (64 bf16)
+constexpr int kChunk = 128;  // query rows per chunk (MMA M in P1)
+
+// D (+)= A * B^T over K = 128: 8 K-steps of 16 across the two 64-wide
+// d-halves.  a_half / b_half: byte distance between the operands' d-halves.
+__device__ __forceinline__ void mma_128xN(uint32_t d_tmem, uint32_t a, uint32_t a_half, uint32_t b, uint32_t b_half,
+                                          uint32_t idesc) {
+    // desc(addr + off) == desc(addr) + (off >> 4): shared addresses < 256 KB
+    // never carry out of the 14-bit start-address field.
+    const uint64_t da = sdesc_k_sw128(a), db = sdesc_k_sw128(b);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t k = uint32_t((kk & 3) * 32);
+        const uint32_t h = uint32_t(kk >> 2);
+        mma_bf16_ss(d_tmem, da + ((h * a_half + k) >> 4), db + ((h * b_half + k) >> 4), idesc, kk > 0 ? 1u : 0u);
+    }
+}
+
+// Loads `rows` rows (both d-halves) of a [*, 128] bf16 tensor into a
+// [d-half][rows] region whose halves are `half_bytes` apart.
+__device__ __forceinline__ void load_rows(uint8_t* dst, uint32_t half_bytes, const CUtensorMap* map, uint64_t* bar,
+                                          int row) {
+    tma_load_2d(dst, map, bar, 0, row);
+    tma_load_2d(dst + half_bytes, map, bar, 64, row);
+}
+
+// SCORE epilogue on W columns of one cache row (query rows r0 .. r0+W),
+// nlse = -lse2 of those rows: Max: best = max(best, x c2 - lse2) as FFMA2 +
+// three-input max (1.25 issue slots per column); Avg: per-window sums of
+// 2^(x c2 - lse2) accumulated per query head in shared memory.
+template <int W, typename PT>
+__device__ __forceinline__ void score_cols(const float (&v)[W], const float* nlse, int r0, const PT& P,
+                                           float& best, float* s_avg, int r_local) {
+    if (P.agg_max) {
+        const uint64_t c2x2 = f2_pack(P.c2, P.c2);
+        float b0 = best, b1 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < W; i += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(nlse + i);
+            float a0, a1, a2, a3;
+            f2_unpack(ffma2(f2_pack(v[i], v[i + 1]), c2x2, f2_pack(l4.x, l4.y)), a0, a1);
+            f2_unpack(ffma2(f2_pack(v[i + 2], v[i + 3]), c2x2, f2_pack(l4.z, l4.w)), a2, a3);
+            b0 = fmaxf(fmaxf(b0, a0), a1);
+            b1 = fmaxf(fmaxf(b1, a2), a3);
+        }
+        best = fmaxf(b0, b1);
+    } else {
+        float acc = 0.f;
+        int gcur = r0 / P.p;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const int rq = r0 + i;
+            if (rq < P.Gp) {
+                const int gg = rq / P.p;
+                if (gg != gcur) {
+                    atomicAdd(&s_avg[gcur * kChunk + r_local], acc);
+                    acc = 0.f;
+                    gcur = gg;
+                }
+                acc += ex2(fmaf(v[i], P.c2, nlse[i]));
+            }
+        }
+        if (gcur < P.G) atomicAdd(&s_avg[gcur * kChunk + r_local], acc);
+    }
+}
+
+// STATS epilogue on W columns of one query row, `lim` of them valid:
+// online (max, sum 2^(x c2 - max)) update of (m, z).  Pairs of columns go
+// through FFMA2/FADD2; POLY of every 4 pairs take their exp2 on the FMA pipe
+// (exp2_poly2) so the SFU -- the bound of this pass -- carries only the rest.
+template <int W, int POLY>
+__device__ __forceinline__ void stats_cols(float (&v)[W], int lim, float c2, float& m, float& z) {
+    float mx = -INFINITY;
+    if (lim >= W) {
+#pragma unroll
+        for (int i = 0; i < W; ++i) mx = fmaxf(mx, v[i]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            v[i] = (i < lim) ? v[i] : -INFINITY;
+            mx = fmaxf(mx, v[i]);
+        }
+    }
+    mx *= c2;
+    if (mx > m) {
+        z *= ex2(m - mx);
+        m = mx;
+    }
+    if (m != -INFINITY) {
+        const uint64_t c2x2 = f2_pack(c2, c2), nm2 = f2_pack(-m, -m);
+        uint64_t acc0 = f2_pack(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+        for (int i = 0; i < W; i += 4) {
+            const uint64_t t0 = ffma2(f2_pack(v[i], v[i + 1]), c2x2, nm2);
+            const uint64_t t1 = ffma2(f2_pack(v[i + 2], v[i + 3]), c2x2, nm2);
+            uint64_t e[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint64_t t = q ? t1 : t0;
+                if (((i / 2 + q) & 3) >= 4 - POLY) {
+                    e[q] = exp2_poly2(t);
+                } else {
+                    float a, b;
+                    f2_unpack(t, a, b);
+                    e[q] = f2_pack(ex2(a), ex2(b));
+                }
+            }
+            acc0 = fadd2(acc0, e[0]);
+            acc1 = fadd2(acc1, e[1]);
+        }
+        float a0, a1, b0, b1;
+        f2_unpack(acc0, a0, a1);
+        f2_unpack(acc1, b0, b1);
+        z += (a0 + a1) + (b0 + b1);
+    }
+}
+
+// ---- host: K-major bf16 [rows, 128] tensor maps with SWIZZLE_128B boxes -----
+inline PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+inline int make_map(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return fail(EPK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {cuuint64_t(kD), cuuint64_t(std::max<int64_t>(rows, 1))};
+    cuuint64_t strides[1] = {cuuint64_t(kD * 2)};
+    cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(EPK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return EPK_OK;
+}
+
+}  // namespace epk
