@@ -52,6 +52,8 @@ struct CompactParams {
     const uint32_t* keys;  // [rows] global, or null (keep[] given)
     const uint64_t* thr;   // [layers][2]
     uint8_t* keep_out;
+    uint32_t* hist_fine;    // threshold mode: [layers][65536], zeroed here for the next step
+    uint32_t* hist_coarse;  // [layers][256]
 };
 
 __device__ __forceinline__ int head_of_row(const int32_t* off, int H, int64_t r) {
@@ -65,6 +67,14 @@ __device__ __forceinline__ int head_of_row(const int32_t* off, int H, int64_t r)
 
 __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_count_kernel(const __grid_constant__ CompactParams P) {
     const int layer = blockIdx.y;
+    if (P.hist_fine) {  // threshold mode: this CTA's share of the layer's histogram reset
+        const int per = (65536 / 4 + gridDim.x - 1) / gridDim.x;
+        uint4* hf4 = reinterpret_cast<uint4*>(P.hist_fine + int64_t(layer) * 65536);
+        for (int i = blockIdx.x * per + threadIdx.x; i < min(65536 / 4, (blockIdx.x + 1) * per); i += blockDim.x)
+            hf4[i] = make_uint4(0, 0, 0, 0);
+        if (blockIdx.x == 0)
+            for (int i = threadIdx.x; i < 256; i += blockDim.x) P.hist_coarse[layer * 256 + i] = 0;
+    }
     const int chunk = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (chunk >= P.max_chunks) return;
@@ -227,7 +237,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_gather_kernel(const
 }
 
 int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const uint8_t* keep,
-                   int slack, const uint32_t* keys, const uint64_t* thr) {
+                   int slack, const uint32_t* keys, const uint64_t* thr, uint32_t* hist_fine, uint32_t* hist_coarse) {
     if (in->layers != out->layers || in->kv_heads != out->kv_heads || in->head_dim != out->head_dim ||
         in->dtype != out->dtype)
         return fail(EPK_ERR_DIM, "compact: in/out cache shapes differ");
@@ -261,6 +271,8 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     P.keys = keys;
     P.thr = thr;
     P.keep_out = const_cast<uint8_t*>(keep);
+    P.hist_fine = hist_fine;
+    P.hist_coarse = hist_coarse;
     const int64_t ws = 2 * int64_t(in->layers) * P.max_chunks * 4 + 1024;
     rc = ws2_require(ctx, ws);
     if (rc) return rc;

@@ -105,7 +105,7 @@ int make_layer_table(const epk_cache_desc* c, LayerTable* t) {
 int launch_select(epk_ctx*, const epk_cache_desc*, const void*, int, const int64_t*, const int32_t*, int, uint8_t*,
                   int32_t*, int);
 int launch_compact(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*, int, const uint32_t*,
-                   const uint64_t*);
+                   const uint64_t*, uint32_t*, uint32_t*);
 int launch_select_threshold(epk_ctx*, const epk_cache_desc*, const FusedSelect*, const int64_t*, uint64_t*, int32_t*);
 bool step_fused_supported(const epk_cache_desc*, int, int, int);
 int launch_step_fused(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const void*, const void*, int, int,
@@ -353,7 +353,7 @@ int epk_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* ou
     if (rc) return rc;
     if ((rc = check_cache(in)) || (rc = check_cache(out))) return rc;
     if (!keep) return fail(EPK_ERR_ARG, "compact: null keep");
-    return launch_compact(ctx, in, out, keep, slack, nullptr, nullptr);
+    return launch_compact(ctx, in, out, keep, slack, nullptr, nullptr, nullptr, nullptr);
 }
 
 int epk_append(epk_ctx* ctx, const epk_cache_desc* c, const void* k_new, const void* v_new, const int32_t* positions,
@@ -413,7 +413,9 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     // select), thresholds, then the row-indexed scores / keep mask / keys.
     const int64_t o_hc = int64_t(kMaxLayers) * 65536 * 4;
     const int64_t o_thr = o_hc + int64_t(kMaxLayers) * 256 * 4;
-    const int64_t o_scores = o_thr + int64_t(kMaxLayers) * 16;
+    const int64_t o_cand = o_thr + int64_t(kMaxLayers) * 16;             // [kMaxLayers][1024] uint4
+    const int64_t o_cnt = o_cand + int64_t(kMaxLayers) * 1024 * 16;     // cand_n, done: [kMaxLayers] each
+    const int64_t o_scores = o_cnt + int64_t(kMaxLayers) * 8;
     const int64_t o_keep = o_scores + align_up(rows * 4, 256);
     const int64_t o_keys = o_keep + align_up(rows, 256);
     const int64_t need = o_keys + align_up(rows * 4, 256);
@@ -475,7 +477,13 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
         const epk_cache_desc vout = layer_view(out, l0, l1);
         const void* qg = static_cast<const char*>(q) + l0 * qlayer;
         const void* kpg = static_cast<const char*>(kp) + l0 * klayer;
-        const FusedSelect fs{keys, hist_f + int64_t(l0) * 65536, hist_c + int64_t(l0) * 256};
+        unsigned* cnt = reinterpret_cast<unsigned*>(sb + o_cnt);
+        const FusedSelect fs{keys,
+                             hist_f + int64_t(l0) * 65536,
+                             hist_c + int64_t(l0) * 256,
+                             reinterpret_cast<uint4*>(sb + o_cand) + int64_t(l0) * 1024,
+                             cnt + l0,
+                             cnt + kMaxLayers + l0};
         if (fused) {
             if (prompt_len <= 0) return fail(EPK_ERR_EMPTY_PROMPT, "score_with_prompt: empty prompt");
             if (q_heads < in->kv_heads || q_heads % in->kv_heads != 0)
@@ -498,10 +506,11 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
         }
         if (fused) {
             rc = launch_select_threshold(ctx, &vin, &fs, budgets + l0, thr + 2 * l0, kept ? kept + l0 : nullptr);
-            if (rc == EPK_OK) rc = launch_compact(ctx, &vin, &vout, keep, out_slack, keys, thr + 2 * l0);
+            if (rc == EPK_OK)
+                rc = launch_compact(ctx, &vin, &vout, keep, out_slack, keys, thr + 2 * l0, fs.hist_fine, fs.hist_coarse);
         } else {
             rc = launch_select(ctx, &vin, scores, EPK_F32, budgets + l0, pins, n_pins, keep, kept ? kept + l0 : nullptr, 0);
-            if (rc == EPK_OK) rc = launch_compact(ctx, &vin, &vout, keep, out_slack, nullptr, nullptr);
+            if (rc == EPK_OK) rc = launch_compact(ctx, &vin, &vout, keep, out_slack, nullptr, nullptr, nullptr, nullptr);
         }
         ctx->stream = main;
         if (rc) return rc;

@@ -101,6 +101,9 @@ struct FusedSelect {
     uint32_t* keys;         // [rows] per global cache row
     uint32_t* hist_fine;    // [layers][65536] counts of float_bits(score) >> 14
     uint32_t* hist_coarse;  // [layers][256] counts of that bin >> 8
+    uint4* cand;            // [layers][1024] threshold-bin candidates (select)
+    unsigned* cand_n;       // [layers] candidate counts (zero between steps)
+    unsigned* done;         // [layers] select arrival counters (zero between steps)
 };
 
 // ---------------------------------------------------------------------------

@@ -25,6 +25,8 @@
 //   final    keep[r] = key < T || (key == T && tiebreak <= U) || pinned.
 // If the bucket never gets small (massive exact ties), the tiebreak radix runs
 // over global memory instead.  Result: the set std::sort would give.
+#include <algorithm>
+
 #include "epk_internal.cuh"
 
 namespace epk {
@@ -529,57 +531,105 @@ int launch_select(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int
 }
 
 // ---------------------------------------------------------------------------
-// Threshold select (the tensor-core step's fused path, no pins).  The scorer
-// (score_tc.cu, SCORE pass) already wrote each live row's key and counted
+// Threshold select (the tensor-core step, no pins).  The scorer (score_tc.cu,
+// SCORE pass) already wrote each live row's key and counted
 // float_bits(score) >> 14 into a 65536-bin per-layer histogram (+ a 256-bin
-// coarse one).  Scores are softmax weights in [0, 1], so bin b holds exactly
-// the keys with key >> 14 == 0x1FFFF - b: the coarse and fine histograms give
-// the threshold bin and its rank in two 1 KB reads, then radix_core resolves
-// the bin's candidates.  Output per layer: thr[2l] = T | keep_all << 32,
-// thr[2l+1] = U; the compaction applies keep = key < T || (key == T &&
-// tiebreak <= U) to the live rows.  The histograms are zeroed for the next
-// step.  Bin and key prefix agree for every score in [0, 2) (bits >> 14 <
-// 65536); the scorer's softmax weights are in [0, 1] up to rounding.
+// coarse one).  Scores are softmax weights in [0, 1] (bin and key prefix agree
+// for any score in [0, 2)), so bin b holds exactly the keys with
+// key >> 14 == 0x1FFFF - b.  Grid: kTSParts CTAs per layer (128 threads):
+//   every CTA   finds the threshold bin and its rank from the coarse and fine
+//               histograms (two 1 KB reads) and appends the candidates of
+//               its slice of the layer (live rows in that bin) to the layer's
+//               candidate list;
+//   last CTA    (per-layer arrival counter) resolves the exact threshold key T
+//               and tiebreak U among the candidates (8-bit radix on the
+//               remaining 14 key bits, then on position << 8 | head), writes
+//               thr[l] = {T | keep_all << 32, U} and resets the counters for
+//               the next step (compact_count_kernel zeroes the histograms).
+// The compaction then keeps live rows with key < T || (key == T && tiebreak
+// <= U).
 // ---------------------------------------------------------------------------
+constexpr int kTSThreads = 128;
+constexpr int kTSCand = 1024;  // candidates resolved in shared memory
+
 struct ThreshParams {
     LayerTable lt;
     int64_t budget[kMaxLayers];
     const int32_t* head_off;
     const int32_t* head_len;
     const int32_t* pos;
-    const uint32_t* keys;  // [rows] global cache rows
-    uint32_t* hist_fine;   // [layers][65536]
-    uint32_t* hist_coarse;  // [layers][256]
-    uint64_t* thr;          // [layers][2]
+    const uint32_t* keys;    // [rows] global cache rows
+    uint32_t* hist_fine;     // [layers][65536]
+    uint32_t* hist_coarse;   // [layers][256]
+    uint64_t* thr;           // [layers][2]
+    uint4* cand;             // [layers][kTSCand] {key, 0, tiebreak lo, tiebreak hi}
+    unsigned* cand_n;        // [layers]
+    unsigned* done;          // [layers]
     int32_t* kept_per_layer;
     int H;
+    int parts;
     int* err_flag;
 };
 
-__global__ void __launch_bounds__(kSelThreads, 4) select_threshold_kernel(const __grid_constant__ ThreshParams P) {
-    using KeyT = uint32_t;
-    const KeyT kNone = ~KeyT(0);
-    __shared__ SelShared<KeyT> S;
-    __shared__ uint32_t s_tot[256];
-    const int layer = blockIdx.x;
-    const int H = P.H;
-    const int tid = threadIdx.x;
+struct TSShared {
+    int32_t off[kMaxHeads + 1];
+    int32_t len[kMaxHeads];
+    uint32_t tot[256];
+    uint32_t hist[256];
+    uint32_t ck[kTSCand];
+    uint64_t ct[kTSCand];
+    int64_t red[kTSThreads / 32];
+    int bucket;
+    int64_t before, eq;
+    int last;
+};
 
-    for (int i = tid; i <= H; i += blockDim.x) S.off[i] = P.head_off[layer * (H + 1) + i];
-    for (int i = tid; i < H; i += blockDim.x) S.len[i] = P.head_len[layer * H + i];
+// Bucket of tot[0..nbins) (nbins <= 256) holding the k-th smallest (1-based).
+__device__ void ts_find_bucket(TSShared& S, const uint32_t* tot, int nbins, int64_t k) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int b0 = tid * 2;
+    const int64_t mine = (b0 < nbins ? tot[b0] : 0) + (b0 + 1 < nbins ? tot[b0 + 1] : 0);
+    int64_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    __syncthreads();
+    if (lane == 31) S.red[w] = incl;
+    __syncthreads();
+    int64_t excl = incl - mine;
+    for (int q = 0; q < w; ++q) excl += S.red[q];
+    if (mine > 0 && excl < k && k <= excl + mine) {
+        const int64_t t0 = b0 < nbins ? tot[b0] : 0;
+        if (excl + t0 >= k) {
+            S.bucket = b0;
+            S.before = excl;
+            S.eq = t0;
+        } else {
+            S.bucket = b0 + 1;
+            S.before = excl + t0;
+            S.eq = tot[b0 + 1];
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __grid_constant__ ThreshParams P) {
+    __shared__ TSShared S;
+    const int l = blockIdx.y, part = blockIdx.x;
+    const int H = P.H;
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i <= H; i += kTSThreads) S.off[i] = P.head_off[l * (H + 1) + i];
+    for (int i = tid; i < H; i += kTSThreads) S.len[i] = P.head_len[l * H + i];
     __syncthreads();
     int64_t n_live = 0;
     for (int h = 0; h < H; ++h) n_live += S.len[h];
-    const int sb = 0, se = S.off[H];
-    const int64_t base = P.lt.base[layer];
-    const int g0 = int((base & ~int64_t(3)) - base);
-    const int ngroups = se > sb ? (se - g0 + 3) / 4 : 0;
-    const KeyT* keys = P.keys + base;
+    const int region = S.off[H];
+    const int64_t base = P.lt.base[l];
+    const uint32_t* keys = P.keys + base;
     const int32_t* pos = P.pos + base;
-    uint32_t* hf = P.hist_fine + int64_t(layer) * 65536;
-    uint32_t* hc = P.hist_coarse + layer * 256;
-    const int64_t limit = int64_t(H) * P.budget[layer];
-
+    const int64_t limit = int64_t(H) * P.budget[l];
     auto head_of = [&](int r) -> int {
         int lo = 0, hi = H - 1;
         while (lo < hi) {
@@ -588,57 +638,135 @@ __global__ void __launch_bounds__(kSelThreads, 4) select_threshold_kernel(const 
         }
         return lo;
     };
-    auto tiebreak = [&](int r) -> uint64_t { return (uint64_t(uint32_t(pos[r])) << 8) | uint64_t(head_of(r)); };
-    // live rows only (gap rows hold stale keys)
-    auto load4 = [&](int i, KeyT (&k)[4]) {
-        const int r0 = g0 + 4 * i;
-        int h = head_of(max(r0, 0));
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int r = r0 + u;
-            k[u] = kNone;
-            if (r < sb || r >= se) continue;
-            while (h + 1 < H && S.off[h + 1] <= r) ++h;
-            if (r - S.off[h] < S.len[h]) k[u] = __ldcg(keys + r);
-        }
-    };
-
-    uint64_t thr0, thr1 = ~uint64_t(0);
-    if (n_live <= limit) {
-        thr0 = uint64_t(1) << 32;  // keep every live row
-    } else {
-        int64_t k_rem = limit;
-        // coarse bins in key order (descending score): i -> coarse bin 255 - i
-        if (tid < 256) s_tot[tid] = __ldcg(hc + 255 - tid);
+    uint32_t kb = 0;
+    int64_t k_rem = limit, eq = 0;
+    const bool select = n_live > limit;
+    if (select) {
+        // threshold bin: coarse then fine histogram, bins in key order
+        for (int i = tid; i < 256; i += kTSThreads) S.tot[i] = __ldcg(P.hist_coarse + l * 256 + 255 - i);
         __syncthreads();
-        find_bucket(S, s_tot, 256, k_rem);
+        ts_find_bucket(S, S.tot, 256, k_rem);
         k_rem -= S.before;
         const int cb = 255 - S.bucket;
+        for (int i = tid; i < 256; i += kTSThreads)
+            S.tot[i] = __ldcg(P.hist_fine + int64_t(l) * 65536 + cb * 256 + 255 - i);
         __syncthreads();
-        if (tid < 256) s_tot[tid] = __ldcg(hf + cb * 256 + 255 - tid);
-        __syncthreads();
-        find_bucket(S, s_tot, 256, k_rem);
+        ts_find_bucket(S, S.tot, 256, k_rem);
         k_rem -= S.before;
-        const int b = cb * 256 + 255 - S.bucket;
-        int64_t eq = S.eq;
-        KeyT prefix = KeyT(0x1FFFF - b) << 14, mask = 0xFFFFC000u;
+        eq = S.eq;
+        kb = uint32_t(0x1FFFF - (cb * 256 + 255 - S.bucket));
+        // this part's slice: candidates -> the layer's list (keys loaded 16 per
+        // thread up front, one memory round trip per 2048 rows)
+        const int r_beg = int(int64_t(region) * part / P.parts), r_end = int(int64_t(region) * (part + 1) / P.parts);
+        for (int b0 = r_beg; b0 < r_end; b0 += 16 * kTSThreads) {  // warp-uniform
+            uint32_t kv[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int rr = b0 + u * kTSThreads + tid;
+                kv[u] = rr < r_end ? __ldcg(keys + rr) : 0u;
+            }
+            int h = head_of(min(b0 + tid, max(r_end - 1, 0)));
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int rr = b0 + u * kTSThreads + tid;
+                bool c = false;
+                if (rr < r_end) {
+                    while (h + 1 < H && S.off[h + 1] <= rr) ++h;
+                    c = rr - S.off[h] < S.len[h] && (kv[u] >> 14) == kb;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, c);
+                if (bal == 0) continue;
+                const int leader = __ffs(bal) - 1;
+                unsigned at = 0;
+                if (lane == leader) at = atomicAdd(P.cand_n + l, unsigned(__popc(bal)));
+                at = __shfl_sync(0xffffffffu, at, leader) + __popc(bal & ((1u << lane) - 1u));
+                if (c && at < unsigned(kTSCand)) {
+                    const uint64_t tb = (uint64_t(uint32_t(pos[rr])) << 8) | uint64_t(h);
+                    P.cand[int64_t(l) * kTSCand + at] = make_uint4(kv[u], 0u, uint32_t(tb), uint32_t(tb >> 32));
+                }
+            }
+        }
+    }
+    // the last CTA of the layer resolves
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) S.last = atomicAdd(P.done + l, 1u) == unsigned(P.parts - 1);
+    __syncthreads();
+    if (!S.last) return;
+    __threadfence();
+    uint64_t t0 = uint64_t(1) << 32, t1 = ~uint64_t(0);  // keep every live row
+    if (select) {
+        const unsigned n = __ldcg(P.cand_n + l);
+        const bool listed = int64_t(n) == eq && n <= unsigned(kTSCand);
+        if (listed) {
+            for (int i = tid; i < int(n); i += kTSThreads) {
+                const uint4 cv = __ldcg(P.cand + int64_t(l) * kTSCand + i);
+                S.ck[i] = cv.x;
+                S.ct[i] = (uint64_t(cv.w) << 32) | cv.z;
+            }
+            __syncthreads();
+        }
+        // for_each(f): f(key, tiebreak) over the bin's candidates
+        auto each = [&](auto&& f) {
+            if (listed) {
+                for (int i = tid; i < int(n); i += kTSThreads) f(S.ck[i], S.ct[i]);
+            } else {  // list overflow: the layer's rows in global memory
+                for (int rr = tid; rr < region; rr += kTSThreads) {
+                    const int h = head_of(rr);
+                    if (rr - S.off[h] >= S.len[h]) continue;
+                    const uint32_t key = __ldcg(keys + rr);
+                    if ((key >> 14) == kb) f(key, (uint64_t(uint32_t(pos[rr])) << 8) | uint64_t(h));
+                }
+            }
+        };
+        uint32_t prefix = kb << 14, mask = 0xFFFFC000u;
         int lo = 14;
-        KeyT T;
-        uint64_t U;
-        radix_core<KeyT>(S, ngroups, load4, tiebreak, g0, prefix, mask, lo, eq, k_rem, T, U);
-        thr0 = T;
-        thr1 = U;
+        while (lo > 0) {
+            const int hi = lo;
+            lo = hi > 8 ? hi - 8 : 0;
+            const uint32_t dmask = (1u << (hi - lo)) - 1;
+            for (int i = tid; i < 256; i += kTSThreads) S.hist[i] = 0;
+            __syncthreads();
+            each([&](uint32_t k, uint64_t) {
+                if (((k ^ prefix) & mask) == 0) atomicAdd(&S.hist[(k >> lo) & dmask], 1u);
+            });
+            __syncthreads();
+            ts_find_bucket(S, S.hist, int(dmask) + 1, k_rem);
+            k_rem -= S.before;
+            eq = S.eq;
+            prefix |= uint32_t(S.bucket) << lo;
+            mask |= dmask << lo;
+        }
+        const uint32_t T = prefix;
+        uint64_t U = ~uint64_t(0);
+        if (eq > k_rem) {
+            uint64_t tp = 0, tm = 0;
+            for (int shift = 32; shift >= 0; shift -= 8) {
+                for (int i = tid; i < 256; i += kTSThreads) S.hist[i] = 0;
+                __syncthreads();
+                each([&](uint32_t k, uint64_t tb) {
+                    if (k == T && ((tb ^ tp) & tm) == 0) atomicAdd(&S.hist[(tb >> shift) & 0xFF], 1u);
+                });
+                __syncthreads();
+                ts_find_bucket(S, S.hist, 256, k_rem);
+                k_rem -= S.before;
+                tp |= uint64_t(S.bucket) << shift;
+                tm |= uint64_t(0xFF) << shift;
+            }
+            U = tp;
+        }
+        t0 = T;
+        t1 = U;
     }
     if (tid == 0) {
-        P.thr[2 * layer] = thr0;
-        P.thr[2 * layer + 1] = thr1;
-        if (P.kept_per_layer) P.kept_per_layer[layer] = int32_t(min(n_live, limit));
+        P.thr[2 * l] = t0;
+        P.thr[2 * l + 1] = t1;
+        if (P.kept_per_layer) P.kept_per_layer[l] = int32_t(min(n_live, limit));
+        P.cand_n[l] = 0;
+        P.done[l] = 0;
     }
-    __syncthreads();
-    // zero the histograms for the next step
-    uint4* hf4 = reinterpret_cast<uint4*>(hf);
-    for (int i = tid; i < 65536 / 4; i += blockDim.x) hf4[i] = make_uint4(0, 0, 0, 0);
-    if (tid < 256) hc[tid] = 0;
+    // (the histograms are zeroed for the next step by compact_count_kernel,
+    // spread over its CTAs)
 }
 
 int launch_select_threshold(epk_ctx* ctx, const epk_cache_desc* c, const FusedSelect* fs, const int64_t* budgets,
@@ -647,9 +775,11 @@ int launch_select_threshold(epk_ctx* ctx, const epk_cache_desc* c, const FusedSe
     ThreshParams P;
     int rc = make_layer_table(c, &P.lt);
     if (rc) return rc;
+    int64_t max_region = 0;
     for (int l = 0; l < c->layers; ++l) {
         if (budgets[l] < 0) return fail(EPK_ERR_ARG, "select: negative budget");
         P.budget[l] = budgets[l];
+        max_region = std::max<int64_t>(max_region, P.lt.base[l + 1] - P.lt.base[l]);
     }
     P.head_off = c->head_off;
     P.head_len = c->head_len;
@@ -658,11 +788,15 @@ int launch_select_threshold(epk_ctx* ctx, const epk_cache_desc* c, const FusedSe
     P.hist_fine = fs->hist_fine;
     P.hist_coarse = fs->hist_coarse;
     P.thr = thr;
+    P.cand = fs->cand;
+    P.cand_n = fs->cand_n;
+    P.done = fs->done;
     P.kept_per_layer = kept;
     P.H = c->kv_heads;
+    P.parts = int(std::max<int64_t>(1, std::min<int64_t>(16, (max_region + 8191) / 8192)));
     P.err_flag = ctx->err_flag;
     EPK_PROF(ctx, "select");
-    select_threshold_kernel<<<c->layers, kSelThreads, 0, ctx->stream>>>(P);
+    select_threshold_kernel<<<dim3(P.parts, c->layers), kTSThreads, 0, ctx->stream>>>(P);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }
