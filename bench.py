@@ -458,14 +458,21 @@ def main():
     kernels = r["kernels"]
     G, p, d, L, H = c["Hq"] // c["H"], c["p"], c["d"], c["L"], c["H"]
     n_h, live, keep = step_sizes(c)
+    # per-kernel algorithmic work per step: bound, amount, unit, peak
+    sfu_peak = 4.63e12  # measured MUFU.EX2 rate (profiles/mufu_rate_r01.txt)
     work = {
-        "p1_rowstats": ("tensor", 2.0 * G * p * d * (live + L * H * p) / 1e12, "TFLOP/s", tc_sus),
+        "p1_rowstats": ("sfu", G * p * (live + L * H * p) / 1e12, "Tex2/s", sfu_peak / 1e12),
         "p2_colscore": ("tensor", 2.0 * G * p * d * live / 1e12, "TFLOP/s", tc_sus),
         "compact_gather": ("hbm", (4.0 * keep * d * 2 + 8.0 * keep + live) / 1e9, "GB/s", hbm),
-        "select": ("hbm", (4.0 * live + live) / 1e9, "GB/s", hbm),
-        "compact_count": ("hbm", live / 1e9, "GB/s", hbm),
+        "select": ("hbm", (4.0 * live) / 1e9, "GB/s", hbm),
+        "compact_count": ("hbm", (4.0 * live + live) / 1e9, "GB/s", hbm),
     }
-    dom = max((k for k in kernels if k in work), key=lambda k: kernels[k]["ms_per_step"], default=None)
+    for k, (bound, amount, unit, peak) in work.items():
+        if k in kernels and kernels[k]["ms_per_step"] > 0:
+            ach = amount / (kernels[k]["ms_per_step"] / 1000.0)
+            kernels[k].update({"bound": bound, "achieved": ach, "unit": unit, "peak": peak, "frac": ach / peak})
+    dom = max((k for k in kernels if k in work and work[k][0] in ("hbm", "tensor")),
+              key=lambda k: kernels[k]["ms_per_step"], default=None)
     roof = None
     if dom is not None:
         bound, amount, unit, peak = work[dom]
@@ -476,7 +483,7 @@ def main():
         roof = {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
                 "traffic": traffic_from_profiles(dom), "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"
                 if peak_src == "measured" else "fallback (B200_PROFILING.md)",
-                "algorithmic_per_launch": amount, "ms_per_launch": kms}
+                "algorithmic_per_launch": amount * (1e9 if unit == "GB/s" else 1e12), "ms_per_launch": kms}
     step_roof = {"bound": "hbm", "algorithmic_bytes": B, "achieved": B / (step_ms / 1000.0) / 1e9, "peak": hbm,
                  "unit": "GB/s", "frac": B / (step_ms / 1000.0) / 1e9 / hbm,
                  "tensor_flops_single_pass": F, "exps": X,

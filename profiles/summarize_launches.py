@@ -16,7 +16,7 @@ def main(path, out):
         n = r[i_name].split("(")[0].replace("void ", "").replace("epk::", "")
         n = n.replace("tc_score_kernel<0>", "tc_score_kernel<P1>").replace("tc_score_kernel<1>", "tc_score_kernel<P2>")
         agg.setdefault(n, []).append(float(r[i_val].replace(",", "")))
-    ours = {n: v for n, v in agg.items() if n.startswith(("tc_", "select", "compact", "f32_", "append"))}
+    ours = {n: v for n, v in agg.items() if n.startswith(("tc_", "select", "compact", "f32_", "append", "step_"))}
     tot = sum(sum(v) / len(v) for v in ours.values())
     with open(out, "w") as f:
         f.write(f"# source: {path}\n# ncu --metrics gpu__time_duration.sum --clock-control none: cold-cache, "
