@@ -254,6 +254,12 @@ __device__ float merge_lse2(const TcParams& P, int hk, int rq, int64_t T1) {
 
 // <= 128 registers (45K of the SM's 64K) and <= kSmemBudget of shared memory,
 // so the side stream's select/compaction CTAs can co-reside with a scorer CTA.
+#ifdef EPK_NO_BACKOFF
+#define mbar_wait_pm mbar_wait
+#else
+#define mbar_wait_pm mbar_wait_backoff
+#endif
+
 template <int MODE, int POLY>
 __global__ void __maxnreg__(128)
     tc_score_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tm_k,
@@ -339,7 +345,7 @@ __global__ void __maxnreg__(128)
                 if (resident && x.r != key) {
                     key = x.r;
                     for (int c = 0; c < x.nq; ++c) {
-                        mbar_wait(&q_empty[c], (qload[c] & 1) ^ 1);
+                        mbar_wait_pm(&q_empty[c], (qload[c] & 1) ^ 1);
                         if (leader) {
                             mbar_expect_tx(&q_full[c], 2 * kChunk * kRowB);
                             load_rows(sQ + c * kChunk * kRowB, q_half, &tm_q, &q_full[c], qrow0 + (x.c0 + c) * kChunk);
@@ -349,7 +355,7 @@ __global__ void __maxnreg__(128)
                     }
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
-                    mbar_wait(&k_empty[ks], kph ^ 1);
+                    mbar_wait_pm(&k_empty[ks], kph ^ 1);
                     if (leader) {
                         mbar_expect_tx(&k_full[ks], k_stage);
                         if (t < x.nc)
@@ -368,7 +374,7 @@ __global__ void __maxnreg__(128)
                         for (int j = 0; j < npairs; ++j, ++pj) {
                             const int slot = int(pj & 1);
                             const int nch = min(2, P.NQ - 2 * j);
-                            mbar_wait(&q_empty[slot], (qload[slot] & 1) ^ 1);
+                            mbar_wait_pm(&q_empty[slot], (qload[slot] & 1) ^ 1);
                             if (leader) {
                                 mbar_expect_tx(&q_full[slot], nch * 2 * kChunk * kRowB);
                                 for (int cc = 0; cc < nch; ++cc)
@@ -408,17 +414,17 @@ __global__ void __maxnreg__(128)
                     fresh = true;
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
-                    mbar_wait(&k_full[ks], kph);
+                    mbar_wait_pm(&k_full[ks], kph);
                     const uint32_t kst = k0 + uint32_t(ks) * k_stage;
                     if (MODE == MODE_STATS) {
                         for (int c = 0; c < x.nq; ++c, ++job) {
                             if (fresh && t == 0) {
-                                mbar_wait(&q_full[c], qload[c] & 1);
+                                mbar_wait_pm(&q_full[c], qload[c] & 1);
                                 ++qload[c];
                             }
                             if ((job & 1) != mw) continue;
                             const int ts = int(job & 3);  // four 128-column slots
-                            mbar_wait(&t_empty[ts], ((job >> 2) & 1) ^ 1);
+                            mbar_wait_pm(&t_empty[ts], ((job >> 2) & 1) ^ 1);
                             tc_fence_after();
                             if (leader) {
                                 mma_128xN(tmem + uint32_t(ts * 128), q0 + uint32_t(c * kChunk * kRowB), q_half, kst,
@@ -432,7 +438,7 @@ __global__ void __maxnreg__(128)
                             const int nch = min(2, x.nq - 2 * j);
                             if (resident && fresh && t == 0)
                                 for (int cc = 0; cc < nch; ++cc) {
-                                    mbar_wait(&q_full[2 * j + cc], qload[2 * j + cc] & 1);
+                                    mbar_wait_pm(&q_full[2 * j + cc], qload[2 * j + cc] & 1);
                                     ++qload[2 * j + cc];
                                 }
                             if ((job & 1) != mw) continue;
@@ -441,12 +447,12 @@ __global__ void __maxnreg__(128)
                             if (resident) {
                                 qb = q0 + uint32_t(2 * j * kChunk * kRowB);
                             } else {
-                                mbar_wait(&q_full[slot], qload[slot] & 1);
+                                mbar_wait_pm(&q_full[slot], qload[slot] & 1);
                                 ++qload[slot];
                                 qb = q0 + uint32_t(slot * 2 * kChunk * kRowB);
                             }
                             const int ts = int(mw);
-                            mbar_wait(&t_empty[ts], ((job >> 1) & 1) ^ 1);
+                            mbar_wait_pm(&t_empty[ts], ((job >> 1) & 1) ^ 1);
                             tc_fence_after();
                             if (leader) {
                                 mma_128xN(tmem + uint32_t(ts * 256), kst, k_half, qb, q_half,
