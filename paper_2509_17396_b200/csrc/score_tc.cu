@@ -56,9 +56,12 @@ namespace epk {
 
 using namespace sm100;
 
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 8;      // SCORE epilogue warps (two column halves)
+constexpr int kEpiWarpsStats = 12; // STATS epilogue warps: three job groups of four
+constexpr int kStatGroups = kEpiWarpsStats / 4;
 constexpr int kMmaWarps = 2;  // MMA issuers alternate jobs: one issues while the other synchronises
 constexpr int kThreads = 32 * (1 + kMmaWarps + kEpiWarps);
+constexpr int kThreadsStats = 32 * (1 + kMmaWarps + kEpiWarpsStats);
 constexpr int kMaxQRes = 4;  // resident query chunks (P1: per chunk group)
 
 enum { MODE_STATS = 0, MODE_SCORE = 1 };
@@ -174,7 +177,7 @@ __device__ __forceinline__ Seg seg_at(const TcParams& P, const int32_t* s_pre, i
     if (MODE == MODE_STATS) {
         x.c0 = x.cg * P.cg_chunks;
         x.nq = min(P.cg_chunks, P.NQ - x.c0);
-        x.slot = 2 * (int(blockIdx.x) - (part_cnt(T, gridDim.x, R0) - 1));
+        x.slot = kStatGroups * (int(blockIdx.x) - (part_cnt(T, gridDim.x, R0) - 1));
     } else {
         x.c0 = 0;
         x.nq = P.NQ;
@@ -210,13 +213,17 @@ __device__ __forceinline__ void flush_coarse(const TcParams& P, int layer, uint3
 // lse2 from a row's partials at the listed slots.
 __device__ __forceinline__ float merge_slots(const float* pm, const float* pz, const int* slot, int n) {
     float M = -INFINITY;
-    for (int i = 0; i < n; ++i) M = fmaxf(M, fmaxf(pm[slot[i]], pm[slot[i] + 1]));
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int u = 0; u < kStatGroups; ++u) M = fmaxf(M, pm[slot[i] + u]);
     if (M == -INFINITY) return INFINITY;
     float Z = 0.f;
     for (int i = 0; i < n; ++i) {
-        const float m0 = pm[slot[i]], m1 = pm[slot[i] + 1];
-        if (m0 != -INFINITY) Z += pz[slot[i]] * ex2(m0 - M);
-        if (m1 != -INFINITY) Z += pz[slot[i] + 1] * ex2(m1 - M);
+#pragma unroll
+        for (int u = 0; u < kStatGroups; ++u) {
+            const float mu = pm[slot[i] + u];
+            if (mu != -INFINITY) Z += pz[slot[i] + u] * ex2(mu - M);
+        }
     }
     return M + log2f(Z);
 }
@@ -236,17 +243,17 @@ __device__ float merge_lse2(const TcParams& P, int hk, int rq, int64_t T1) {
     for (int b = b0; b <= b1; ++b) {
         const int lo = max(R0, part_bound(T1, P.p1_grid, b)), hi = min(R1, part_bound(T1, P.p1_grid, b + 1));
         if (lo >= hi) continue;
-        const int s = 2 * (b - b0);
-        M = fmaxf(M, fmaxf(pm[s], pm[s + 1]));
+        const int s = kStatGroups * (b - b0);
+        for (int u = 0; u < kStatGroups; ++u) M = fmaxf(M, pm[s + u]);
     }
     if (M == -INFINITY) return INFINITY;
     float Z = 0.f;
     for (int b = b0; b <= b1; ++b) {
         const int lo = max(R0, part_bound(T1, P.p1_grid, b)), hi = min(R1, part_bound(T1, P.p1_grid, b + 1));
         if (lo >= hi) continue;
-        const int s = 2 * (b - b0);
+        const int s = kStatGroups * (b - b0);
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < kStatGroups; ++u)
             if (pm[s + u] != -INFINITY) Z += pz[s + u] * ex2(pm[s + u] - M);
     }
     return M + log2f(Z);
@@ -308,9 +315,9 @@ __global__ void __maxnreg__(128)
             }
             for (int s = 0; s < 4; ++s) {
                 mbar_init(&t_full[s], 1);
-                // STATS: a slot is drained by the 4 warps of its job parity;
+                // STATS: a slot is drained by the 4 warps of the job's group;
                 // SCORE: by all 8 (two column halves)
-                mbar_init(&t_empty[s], MODE == MODE_STATS ? kEpiWarps / 2 : kEpiWarps);
+                mbar_init(&t_empty[s], MODE == MODE_STATS ? 4 : kEpiWarps);
             }
             fence_barrier_init();
         }
@@ -475,7 +482,7 @@ __global__ void __maxnreg__(128)
     } else {  // ------------------------- epilogue (8 warps) -------------------------
         const int e = warp - 1 - kMmaWarps;
         const int quarter = warp & 3;  // TMEM lanes this warp may read
-        const int half = e >> 2;       // column half of every job
+        const int half = e >> 2;       // SCORE: column half of every job; STATS: job group (job % 3)
         const int r_local = quarter * 32 + lane;
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
         const int etid = e * 32 + lane;
@@ -502,7 +509,7 @@ __global__ void __maxnreg__(128)
 #pragma unroll
                     for (int c = 0; c < kMaxQRes; ++c) {
                         if (c >= x.nq) break;
-                        if (int(job & 1) != half) {
+                        if (int(job % kStatGroups) != half) {
                             ++job;
                             continue;
                         }
@@ -533,7 +540,7 @@ __global__ void __maxnreg__(128)
                 for (int cc = 0; cc < kMaxQRes; ++cc) {
                     if (cc < x.nq) {
                         const int rq = (x.c0 + cc) * kChunk + r_local;
-                        const int64_t o = (int64_t(x.hk) * (P.NQ * kChunk) + rq) * P.slots + x.slot + half;
+                        const int64_t o = (int64_t(x.hk) * (P.NQ * kChunk) + rq) * P.slots + x.slot + half;  // slot = 3 per CTA
                         P.part_m[o] = m[cc];
                         P.part_z[o] = z[cc];
                     }
@@ -553,7 +560,7 @@ __global__ void __maxnreg__(128)
                                 const int hi = min(R1, part_bound(T1, P.p1_grid, b + 1));
                                 if (lo >= hi) continue;
                                 if (n == kMaxSlots) n = -1;  // too many: rows take the general path
-                                else s_slot[etid * kMaxSlots + n++] = 2 * (b - b0);
+                                else s_slot[etid * kMaxSlots + n++] = kStatGroups * (b - b0);
                             }
                         }
                         s_nslot[etid] = n;
@@ -743,7 +750,7 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     if (smem_bytes(P, MODE_STATS) > limit) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
     P.p1_grid = grid;
     P.p1_runs = P.runs;
-    P.slots = 2 * grid;
+    P.slots = kStatGroups * grid;
     const int64_t rows = int64_t(P.L) * H * P.NQ * kChunk;
     rc = ws_require(ctx, 2 * rows * P.slots * 4 + int64_t(P.runs + 1) * 4 + 4096);
     if (rc) return rc;
@@ -755,7 +762,7 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
         fprintf(stderr, "P1: NQ=%d cg_chunks=%d cgroups=%d kstages=%d smem=%d limit=%d runs=%d\n", P.NQ, P.cg_chunks,
                 P.cgroups, P.kstages, smem_bytes(P, MODE_STATS), limit, P.runs);
     EPK_PROF(ctx, "p1_rowstats");
-    stats_fn<<<grid, kThreads, smem_bytes(P, MODE_STATS), ctx->stream>>>(P, tm_k, tm_q, tm_kp);
+    stats_fn<<<grid, kThreadsStats, smem_bytes(P, MODE_STATS), ctx->stream>>>(P, tm_k, tm_q, tm_kp);
     EPK_LAUNCH_CHECK(ctx);
 
     // P2: 128-row K tiles; all query chunks resident when they fit, else
