@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -59,6 +60,14 @@ void prof_begin(epk_ctx* ctx, const char* name) {
 }
 
 void prof_end(epk_ctx* ctx) {
+    static const bool trace_sync = std::getenv("EPK_DEBUG_SYNC") != nullptr;
+    if (trace_sync) {  // diagnostics: name and completion of every launch
+        std::fprintf(stderr, "[epk] launched %s\n", ctx->profiling && !ctx->prof.empty() ? ctx->prof.back().name : "?");
+        std::fflush(stderr);
+        cudaStreamSynchronize(ctx->stream);
+        std::fprintf(stderr, "[epk] done\n");
+        std::fflush(stderr);
+    }
     if (!ctx->profiling || ctx->prof.empty()) return;
     cudaEventRecord(ctx->prof.back().stop, ctx->stream);
 }
@@ -108,6 +117,14 @@ int launch_compact(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const
                    const uint64_t*, uint32_t*, uint32_t*);
 int launch_select_threshold(epk_ctx*, const epk_cache_desc*, const FusedSelect*, const int64_t*, uint64_t*, int32_t*);
 bool step_fused_supported(const epk_cache_desc*, int, int, int);
+int launch_step_tc_grouped(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const void*, const void*, int, int,
+                           int, const int64_t*, int, cudaStream_t, cudaEvent_t, int, float*, uint8_t*,
+                           const FusedSelect&, uint64_t*, int32_t*,
+                           int (*)(epk_ctx*, const epk_cache_desc*, const FusedSelect*, const int64_t*, uint64_t*,
+                                   int32_t*),
+                           int (*)(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*, int,
+                                   const uint32_t*, const uint64_t*, uint32_t*, uint32_t*),
+                           epk_cache_desc (*)(const epk_cache_desc*, int, int));
 int launch_step_fused(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const void*, const void*, int, int,
                       const int64_t*, int, int64_t, int, float*, uint32_t*, uint32_t*, uint32_t*, uint8_t*, uint64_t*,
                       int32_t*);
@@ -471,6 +488,25 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     const int64_t qlayer = int64_t(q_heads) * prompt_len * in->head_dim * dtype_size(in->dtype);
     const int64_t klayer = int64_t(in->kv_heads) * prompt_len * in->head_dim * dtype_size(in->dtype);
     cudaStream_t main = ctx->stream;
+    if (fused) {
+        // P1 over all layers, then per group: P2 -> threshold select (main)
+        // -> count/plan/gather (side stream when overlapping)
+        if (prompt_len <= 0) return fail(EPK_ERR_EMPTY_PROMPT, "score_with_prompt: empty prompt");
+        if (q_heads < in->kv_heads || q_heads % in->kv_heads != 0)
+            return fail(EPK_ERR_DIM, "score_with_prompt: attention grid shape mismatch");
+        if (aggregation != EPK_AGG_MAX && aggregation != EPK_AGG_AVG) return fail(EPK_ERR_ARG, "bad aggregation");
+        unsigned* cnt = reinterpret_cast<unsigned*>(sb + o_cnt);
+        const FusedSelect fs_all{keys, hist_f, hist_c, reinterpret_cast<uint4*>(sb + o_cand), cnt, cnt + kMaxLayers};
+        rc = launch_step_tc_grouped(ctx, in, out, q, kp, q_heads, prompt_len, aggregation == EPK_AGG_MAX, budgets, G,
+                                    overlap ? ctx->side : nullptr, ctx->ev_fork, out_slack, scores, keep, fs_all, thr,
+                                    kept, launch_select_threshold, launch_compact, layer_view);
+        if (rc) return rc;
+        if (overlap) {
+            EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->side));
+            EPK_CUDA_CHECK(cudaStreamWaitEvent(main, ctx->ev_join, 0));
+        }
+        return EPK_OK;
+    }
     for (int l0 = 0; l0 < L; l0 += G) {
         const int l1 = std::min(L, l0 + G);
         const epk_cache_desc vin = layer_view(in, l0, l1);

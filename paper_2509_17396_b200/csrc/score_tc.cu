@@ -57,8 +57,17 @@ namespace epk {
 using namespace sm100;
 
 constexpr int kEpiWarps = 8;      // SCORE epilogue warps (two column halves)
-constexpr int kEpiWarpsStats = 12; // STATS epilogue warps: three job groups of four
+constexpr int kEpiWarpsStats = 12;  // STATS epilogue warps: three job groups of four
 constexpr int kStatGroups = kEpiWarpsStats / 4;
+// STATS TMEM slots (128 columns each): a multiple of the group count so every
+// slot belongs to ONE epilogue group, and STATS jobs go to the MMA warp of
+// their SLOT (slot % kMmaWarps) -- every slot's full/empty barriers are then
+// waited on by one warp in phase order, so a parity wait can never alias two
+// phases apart (with slot = job % 4 and three groups a group could reach its
+// next job on a slot while another group's job there was still in flight; with
+// three slots and jobs alternating MMA warps an MMA warp could skip a phase).
+constexpr int kStatSlots = kStatGroups == 2 ? 4 : kStatGroups;
+static_assert(kStatSlots % kStatGroups == 0 && kStatSlots * 128 <= 512, "STATS TMEM slots");
 constexpr int kMmaWarps = 2;  // MMA issuers alternate jobs: one issues while the other synchronises
 constexpr int kThreads = 32 * (1 + kMmaWarps + kEpiWarps);
 constexpr int kThreadsStats = 32 * (1 + kMmaWarps + kEpiWarpsStats);
@@ -79,7 +88,8 @@ struct TcParams {
     int ptiles;     // STATS: causal prompt tiles per run
     int p1_grid;    // STATS grid (SCORE reads it to locate the partials)
     int p1_runs;    // STATS runs
-    int slots;      // partial slots per query row (2 per STATS CTA)
+    int slots;      // partial slots per query row (kStatGroups per STATS CTA)
+    int hk_base;    // SCORE: global (layer, head) index of this launch's first head (P1 ran on all layers)
     const int32_t* head_off;
     const int32_t* head_len;
     int32_t* p1_pre;  // [p1_runs + 1] STATS run prefix (written by STATS CTA 0)
@@ -429,9 +439,9 @@ __global__ void __maxnreg__(128)
                                 mbar_wait_pm(&q_full[c], qload[c] & 1);
                                 ++qload[c];
                             }
-                            if ((job & 1) != mw) continue;
-                            const int ts = int(job & 3);  // four 128-column slots
-                            mbar_wait_pm(&t_empty[ts], ((job >> 2) & 1) ^ 1);
+                            const int ts = int(job % kStatSlots);  // 128-column slots, one group each
+                            if (ts % kMmaWarps != int(mw)) continue;
+                            mbar_wait_pm(&t_empty[ts], ((job / kStatSlots) & 1) ^ 1);
                             tc_fence_after();
                             if (leader) {
                                 mma_128xN(tmem + uint32_t(ts * 128), q0 + uint32_t(c * kChunk * kRowB), q_half, kst,
@@ -519,8 +529,8 @@ __global__ void __maxnreg__(128)
                             lim = x.n_h - (x.t0 + t) * P.krows;
                         else
                             lim = min(P.p, rq % P.p + 1) - (x.p0 + t - x.nc) * P.krows;
-                        const int ts = int(job & 3);
-                        mbar_wait(&t_full[ts], (job >> 2) & 1);
+                        const int ts = int(job % kStatSlots);
+                        mbar_wait(&t_full[ts], (job / kStatSlots) & 1);
                         tc_fence_after();
                         {
                             float v[64];
@@ -550,7 +560,7 @@ __global__ void __maxnreg__(128)
                     named_bar_sync(1, 32 * kEpiWarps);
                     if (P.keys && lkey >= 0 && lkey / P.H != x.l) flush_coarse(P, lkey / P.H, s_coarse, etid);
                     if (etid < P.cgroups) {  // slot list of each P1 run (head, chunk group)
-                        const int run = x.hk * P.cgroups + etid;
+                        const int run = (x.hk + P.hk_base) * P.cgroups + etid;
                         const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
                         int n = 0;
                         if (R1 > R0) {
@@ -571,10 +581,10 @@ __global__ void __maxnreg__(128)
                         if (r < P.Gp) {
                             const int cg = (r / kChunk) / P.cg_chunks;
                             const int n = s_nslot[cg];
-                            const int64_t row = int64_t(x.hk) * (P.NQ * kChunk) + r;
+                            const int64_t row = int64_t(x.hk + P.hk_base) * (P.NQ * kChunk) + r;
                             v = n >= 0 ? merge_slots(P.part_m + row * P.slots, P.part_z + row * P.slots,
                                                      s_slot + cg * kMaxSlots, n)
-                                       : merge_lse2(P, x.hk, r, T1);
+                                       : merge_lse2(P, x.hk + P.hk_base, r, T1);
                         }
                         s_lse[r] = -v;  // negated: the epilogue adds it with FFMA2
                     }
@@ -652,9 +662,23 @@ static int smem_bytes(const TcParams& P, int mode) {
            (2 * P.kstages + 2 * kMaxQRes + 8) * 8 + 16 + (P.runs + 1) * 4;
 }
 
-int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const void* kp, int hq, int p, int agg_max,
-                    int64_t n_max, float* scores, const FusedSelect* fs) {
-    (void)n_max;  // the tile partition reads the live head lengths on the device
+// A tensor-core scoring launch plan: P1 over every layer of `c`, then P2 over
+// any layer range [l0, l1) (several ranges may follow one P1, so a step can
+// interleave the selection/compaction of finished layer groups with the
+// scoring of the next).
+struct TcPlan {
+    TcParams P1, P2;
+    CUtensorMap tm_k, tm_q, tm_kp;
+    int smem1, smem2;
+    void (*stats_fn)(TcParams, CUtensorMap, CUtensorMap, CUtensorMap);
+    void (*score_fn)(TcParams, CUtensorMap, CUtensorMap, CUtensorMap);
+    const void* q;
+    int64_t qlayer;  // bytes of one layer's query rows
+    epk_cache_desc c;
+};
+
+static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const void* kp, int hq, int p, int agg_max,
+                   float* scores, const FusedSelect* fs, TcPlan* out) {
     if (c->dtype != EPK_BF16) return fail(EPK_ERR_ARG, "score(tensor core): cache dtype must be BF16");
     if (c->head_dim != kD) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): head_dim must be 128");
     const int H = c->kv_heads;
@@ -681,10 +705,9 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     P.hist_fine = fs ? fs->hist_fine : nullptr;
     P.hist_coarse = fs ? fs->hist_coarse : nullptr;
     P.ptiles = (p + 127) / 128;
+    P.hk_base = 0;
     const int grid = ctx->num_sms;  // persistent: one CTA per SM, tile-balanced ranges
 
-    // Dynamic shared memory limit: the per-block opt-in maximum minus the
-    // kernel's static/reserved shared memory.
     // STATS kernels by exp2 split (POLY of every 4 column pairs on the FMA
     // pipe); EPK_TC_POLY picks one (default 0: measured on B200 the FFMA2
     // polynomial costs more issue than the SFU time it saves).
@@ -694,7 +717,8 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     const KernelFn score_fn = tc_score_kernel<MODE_SCORE, 0>;
     int poly = 0;
     if (const char* e = std::getenv("EPK_TC_POLY")) poly = std::max(0, std::min(3, std::atoi(e)));
-    const KernelFn stats_fn = stats_fns[poly];
+    // Dynamic shared memory limit: the per-block opt-in maximum minus the
+    // kernels' static shared memory.
     static int limit = 0;
     if (!limit) {
         int optin = 0;
@@ -714,17 +738,14 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
         EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(score_fn),
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
     }
-
     // Shared-memory budget: leave ~30 KB of the SM for co-resident side-stream
     // kernels (EPK_TC_SMEM_KB overrides, for experiments).
     int budget = std::min(limit, 200 * 1024);
     if (const char* e = std::getenv("EPK_TC_SMEM_KB")) budget = std::min(limit, std::atoi(e) * 1024);
-    CUtensorMap tm_k1, tm_k2, tm_q, tm_kp;
-    CUtensorMap& tm_k = tm_k1;
-    (void)tm_k2;
-    if ((rc = make_map(&tm_k, c->k, c->layer_base[c->layers], 128))) return rc;
-    if ((rc = make_map(&tm_q, q, int64_t(P.L) * hq * p, kChunk))) return rc;
-    if ((rc = make_map(&tm_kp, kp, int64_t(P.L) * H * p, 128))) return rc;
+    TcPlan& T = *out;
+    if ((rc = make_map(&T.tm_k, c->k, c->layer_base[c->layers], 128))) return rc;
+    if ((rc = make_map(&T.tm_q, q, int64_t(P.L) * hq * p, kChunk))) return rc;
+    if ((rc = make_map(&T.tm_kp, kp, int64_t(P.L) * H * p, 128))) return rc;
 
     // P1: 128-row K tiles (the MMA N = 128 is enough: P1 is bound by the
     // SFU exp2 rate, not the tensor pipe); query chunks in groups sized so
@@ -758,12 +779,12 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     P.part_m = carve.take<float>(rows * P.slots);
     P.part_z = carve.take<float>(rows * P.slots);
     P.p1_pre = carve.take<int32_t>(P.runs + 1);
+    T.P1 = P;
+    T.smem1 = smem_bytes(P, MODE_STATS);
+    T.stats_fn = stats_fns[poly];
     if (std::getenv("EPK_TC_VERBOSE"))
         fprintf(stderr, "P1: NQ=%d cg_chunks=%d cgroups=%d kstages=%d smem=%d limit=%d runs=%d\n", P.NQ, P.cg_chunks,
-                P.cgroups, P.kstages, smem_bytes(P, MODE_STATS), limit, P.runs);
-    EPK_PROF(ctx, "p1_rowstats");
-    stats_fn<<<grid, kThreadsStats, smem_bytes(P, MODE_STATS), ctx->stream>>>(P, tm_k, tm_q, tm_kp);
-    EPK_LAUNCH_CHECK(ctx);
+                P.cgroups, P.kstages, T.smem1, limit, P.runs);
 
     // P2: 128-row K tiles; all query chunks resident when they fit, else
     // streamed as chunk pairs through two 256-row slots.  cgroups/cg_chunks
@@ -782,12 +803,102 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     }
     if (P.kstages < 2) P.kstages = 2;  // over the co-residency budget: use the whole opt-in limit
     if (smem_bytes(P, MODE_SCORE) > limit) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
+    T.P2 = P;
+    T.smem2 = smem_bytes(P, MODE_SCORE);
+    T.score_fn = score_fn;
+    T.q = q;
+    T.qlayer = int64_t(hq) * p * kD * 2;
+    T.c = *c;
     if (std::getenv("EPK_TC_VERBOSE"))
-        fprintf(stderr, "P2: NQ=%d resident=%d kstages=%d smem=%d runs=%d\n", P.NQ, P.resident, P.kstages,
-                smem_bytes(P, MODE_SCORE), P.runs);
-    EPK_PROF(ctx, "p2_colscore");
-    score_fn<<<grid, kThreads, smem_bytes(P, MODE_SCORE), ctx->stream>>>(P, tm_k, tm_q, tm_kp);
+        fprintf(stderr, "P2: NQ=%d resident=%d kstages=%d smem=%d runs=%d\n", P.NQ, P.resident, P.kstages, T.smem2,
+                P.runs);
+    return EPK_OK;
+}
+
+static int tc_launch_p1(epk_ctx* ctx, const TcPlan& T) {
+    EPK_PROF(ctx, "p1_rowstats");
+    T.stats_fn<<<ctx->num_sms, kThreadsStats, T.smem1, ctx->stream>>>(T.P1, T.tm_k, T.tm_q, T.tm_kp);
     EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
+// P2 over layers [l0, l1) of the plan's cache (after tc_launch_p1).
+static int tc_launch_p2(epk_ctx* ctx, const TcPlan& T, int l0, int l1) {
+    TcParams P = T.P2;
+    CUtensorMap tm_q = T.tm_q;
+    if (l0 > 0 || l1 < P.L) {
+        epk_cache_desc v = T.c;
+        v.layers = l1 - l0;
+        v.layer_base = T.c.layer_base + l0;
+        int rc = make_layer_table(&v, &P.lt);
+        if (rc) return rc;
+        P.L = l1 - l0;
+        P.runs = P.L * P.H;
+        P.head_off = T.c.head_off + int64_t(l0) * (P.H + 1);
+        P.head_len = T.c.head_len + int64_t(l0) * P.H;
+        if (P.hist_fine) {
+            P.hist_fine += int64_t(l0) * 65536;
+            P.hist_coarse += int64_t(l0) * 256;
+        }
+        P.hk_base = l0 * P.H;
+        if ((rc = make_map(&tm_q, static_cast<const char*>(T.q) + l0 * T.qlayer, int64_t(P.L) * P.Hq * P.p, kChunk)))
+            return rc;
+    }
+    EPK_PROF(ctx, "p2_colscore");
+    T.score_fn<<<ctx->num_sms, kThreads, T.smem2, ctx->stream>>>(P, T.tm_k, tm_q, T.tm_kp);
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
+int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const void* kp, int hq, int p, int agg_max,
+                    int64_t n_max, float* scores, const FusedSelect* fs) {
+    (void)n_max;  // the tile partition reads the live head lengths on the device
+    TcPlan T;
+    int rc = tc_plan(ctx, c, q, kp, hq, p, agg_max, scores, fs, &T);
+    if (rc) return rc;
+    if ((rc = tc_launch_p1(ctx, T))) return rc;
+    return tc_launch_p2(ctx, T, 0, c->layers);
+}
+
+// One tensor-core block step with the fused selection: P1 over every layer,
+// then per layer group P2 -> threshold select on the context stream and
+// count/plan/gather on `side` (when given) so a group's compaction overlaps
+// the next group's P2 and select.
+int launch_step_tc_grouped(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const void* q,
+                           const void* kp, int hq, int p, int agg_max, const int64_t* budgets, int group,
+                           cudaStream_t side, cudaEvent_t ev_fork, int out_slack, float* scores, uint8_t* keep,
+                           const FusedSelect& fs_all, uint64_t* thr, int32_t* kept,
+                           int (*select_fn)(epk_ctx*, const epk_cache_desc*, const FusedSelect*, const int64_t*,
+                                            uint64_t*, int32_t*),
+                           int (*compact_fn)(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*,
+                                             int, const uint32_t*, const uint64_t*, uint32_t*, uint32_t*),
+                           epk_cache_desc (*view_fn)(const epk_cache_desc*, int, int)) {
+    TcPlan T;
+    int rc = tc_plan(ctx, in, q, kp, hq, p, agg_max, scores, &fs_all, &T);
+    if (rc) return rc;
+    if ((rc = tc_launch_p1(ctx, T))) return rc;
+    const int L = in->layers;
+    cudaStream_t main = ctx->stream;
+    for (int l0 = 0; l0 < L; l0 += group) {
+        const int l1 = std::min(L, l0 + group);
+        if ((rc = tc_launch_p2(ctx, T, l0, l1))) return rc;
+        const epk_cache_desc vin = view_fn(in, l0, l1), vout = view_fn(out, l0, l1);
+        const FusedSelect fs{fs_all.keys,
+                             fs_all.hist_fine + int64_t(l0) * 65536,
+                             fs_all.hist_coarse + int64_t(l0) * 256,
+                             fs_all.cand + int64_t(l0) * 1024,
+                             fs_all.cand_n + l0,
+                             fs_all.done + l0};
+        if ((rc = select_fn(ctx, &vin, &fs, budgets + l0, thr + 2 * l0, kept ? kept + l0 : nullptr))) return rc;
+        if (side) {
+            EPK_CUDA_CHECK(cudaEventRecord(ev_fork, main));
+            EPK_CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork, 0));
+            ctx->stream = side;
+        }
+        rc = compact_fn(ctx, &vin, &vout, keep, out_slack, fs.keys, thr + 2 * l0, fs.hist_fine, fs.hist_coarse);
+        ctx->stream = main;
+        if (rc) return rc;
+    }
     return EPK_OK;
 }
 
