@@ -57,13 +57,39 @@ CONFIGS = {
 }
 
 
+def _flatten(obj, path=""):
+    if isinstance(obj, dict):
+        for k, v in obj.items():
+            yield from _flatten(v, f"{path}.{k}".lower())
+    elif isinstance(obj, (int, float)) and not isinstance(obj, bool):
+        yield path, float(obj)
+
+
 def load_peaks():
+    """(hbm GB/s, bf16 TF/s sustained, bf16 TF/s burst, source).  The
+    driver-written MEASURED_PEAKS.json is read by key names (any nesting:
+    an 'hbm' number for bandwidth, 'bf16' numbers for the tensor pipe,
+    'sustained' preferred); TB/s values are converted.  Fallback: the
+    B200_PROFILING.md figures."""
+    hbm, tc_sus, tc_burst = 6650.0, 1400.0, 1590.0
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            pk = json.load(f)
-        return pk["hbm_gbs"], pk["bf16_tflops_sustained"], pk.get("bf16_tflops", 1640.6), "measured"
+            flat = list(_flatten(json.load(f)))
     except Exception:
-        return 6650.0, 1400.0, 1590.0, "fallback"
+        return hbm, tc_sus, tc_burst, "fallback"
+    hb = [(k, v) for k, v in flat if "hbm" in k or "copy" in k or "dram" in k]
+    bf = [(k, v) for k, v in flat if "bf16" in k or "tensor" in k or "tflop" in k]
+    if not hb and not bf:
+        return hbm, tc_sus, tc_burst, "fallback"
+    if hb:
+        k, v = max(hb, key=lambda kv: ("gb" in kv[0] or "bw" in kv[0] or "band" in kv[0], "burst" not in kv[0]))
+        hbm = v * 1000.0 if v < 100 else v  # TB/s -> GB/s
+    if bf:
+        sus = [kv for kv in bf if "sustain" in kv[0]] or bf
+        tc_sus = sus[0][1] * (1000.0 if sus[0][1] < 20 else 1.0)
+        burst = [kv for kv in bf if "sustain" not in kv[0]] or sus
+        tc_burst = max(v for _, v in burst) * (1000.0 if max(v for _, v in burst) < 20 else 1.0)
+    return hbm, tc_sus, tc_burst, "measured"
 
 
 class ClockSampler:

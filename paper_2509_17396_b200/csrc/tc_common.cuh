@@ -53,17 +53,19 @@ __device__ __forceinline__ void score_cols(const float (&v)[W], const float* nls
                                            float& best, float* s_avg, int r_local) {
     if (P.agg_max) {
         const uint64_t c2x2 = f2_pack(P.c2, P.c2);
-        float b0 = best, b1 = -INFINITY;
+        // four independent three-input-max chains (short dependency chains)
+        float b[4] = {best, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
         for (int i = 0; i < W; i += 4) {
             const float4 l4 = *reinterpret_cast<const float4*>(nlse + i);
             float a0, a1, a2, a3;
             f2_unpack(ffma2(f2_pack(v[i], v[i + 1]), c2x2, f2_pack(l4.x, l4.y)), a0, a1);
             f2_unpack(ffma2(f2_pack(v[i + 2], v[i + 3]), c2x2, f2_pack(l4.z, l4.w)), a2, a3);
-            b0 = fmaxf(fmaxf(b0, a0), a1);
-            b1 = fmaxf(fmaxf(b1, a2), a3);
+            const int j = (i / 4) & 1;
+            b[2 * j] = fmaxf(fmaxf(b[2 * j], a0), a1);
+            b[2 * j + 1] = fmaxf(fmaxf(b[2 * j + 1], a2), a3);
         }
-        best = fmaxf(b0, b1);
+        best = fmaxf(fmaxf(b[0], b[1]), fmaxf(b[2], b[3]));
     } else {
         float acc = 0.f;
         int gcur = r0 / P.p;
@@ -92,8 +94,21 @@ template <int W, int POLY>
 __device__ __forceinline__ void stats_cols(float (&v)[W], int lim, float c2, float& m, float& z) {
     float mx = -INFINITY;
     if (lim >= W) {
+        // max as eight independent three-input-max chains + a tree, not one
+        // W-deep dependency chain (the chain was the epilogue's top stall)
+        constexpr int C = W >= 16 ? 8 : W / 2;
+        float t[C];
 #pragma unroll
-        for (int i = 0; i < W; ++i) mx = fmaxf(mx, v[i]);
+        for (int j = 0; j < C; ++j) t[j] = fmaxf(v[2 * j], v[2 * j + 1]);
+#pragma unroll
+        for (int i = 2 * C; i < W; i += 2 * C)
+#pragma unroll
+            for (int j = 0; j < C; ++j) t[j] = fmaxf(fmaxf(t[j], v[i + 2 * j]), v[i + 2 * j + 1]);
+#pragma unroll
+        for (int w = C / 2; w >= 1; w /= 2)
+#pragma unroll
+            for (int j = 0; j < w; ++j) t[j] = fmaxf(t[j], t[j + w]);
+        mx = t[0];
     } else {
 #pragma unroll
         for (int i = 0; i < W; ++i) {
