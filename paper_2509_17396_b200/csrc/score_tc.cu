@@ -61,16 +61,25 @@ constexpr int kEpiWarpsStats = 12;  // STATS epilogue warps: three job groups of
 constexpr int kStatGroups = kEpiWarpsStats / 4;
 // STATS TMEM slots (128 columns each): a multiple of the group count so every
 // slot belongs to ONE epilogue group, and STATS jobs go to the MMA warp of
-// their SLOT (slot % kMmaWarps) -- every slot's full/empty barriers are then
+// their SLOT (slot % kMmaWarpsStats) -- every slot's full/empty barriers are then
 // waited on by one warp in phase order, so a parity wait can never alias two
 // phases apart (with slot = job % 4 and three groups a group could reach its
 // next job on a slot while another group's job there was still in flight; with
 // three slots and jobs alternating MMA warps an MMA warp could skip a phase).
 constexpr int kStatSlots = kStatGroups == 2 ? 4 : kStatGroups;
 static_assert(kStatSlots % kStatGroups == 0 && kStatSlots * 128 <= 512, "STATS TMEM slots");
-constexpr int kMmaWarps = 2;  // MMA issuers alternate jobs: one issues while the other synchronises
+constexpr int kMmaWarps = 2;  // SCORE: MMA issuers alternate jobs: one issues while the other synchronises
+#ifndef EPK_STATS_MMA_WARPS
+#define EPK_STATS_MMA_WARPS 3
+#endif
+// STATS: one MMA issuer per TMEM slot, so a slot whose group lags never
+// holds back the MMA of another slot (no head-of-line blocking; 16 warps x 128
+// registers = the whole register file; P1 0.285 -> 0.277 ms at cfg2)
+constexpr int kMmaWarpsStats = EPK_STATS_MMA_WARPS;
+template <int MODE>
+constexpr int mma_warps() { return MODE == 0 ? kMmaWarpsStats : kMmaWarps; }
 constexpr int kThreads = 32 * (1 + kMmaWarps + kEpiWarps);
-constexpr int kThreadsStats = 32 * (1 + kMmaWarps + kEpiWarpsStats);
+constexpr int kThreadsStats = 32 * (1 + kMmaWarpsStats + kEpiWarpsStats);
 constexpr int kMaxQRes = 4;  // resident query chunks (P1: per chunk group)
 
 enum { MODE_STATS = 0, MODE_SCORE = 1 };
@@ -271,6 +280,11 @@ __device__ float merge_lse2(const TcParams& P, int hk, int rq, int64_t T1) {
 
 // <= 128 registers (45K of the SM's 64K) and <= kSmemBudget of shared memory,
 // so the side stream's select/compaction CTAs can co-reside with a scorer CTA.
+#ifdef EPK_P1_PROF
+#define P1PROF(...) __VA_ARGS__
+#else
+#define P1PROF(...)
+#endif
 #ifdef EPK_NO_BACKOFF
 #define mbar_wait_pm mbar_wait
 #else
@@ -317,11 +331,11 @@ __global__ void __maxnreg__(128)
             if (MODE == MODE_STATS) tma_prefetch(&tm_kp);
             for (int s = 0; s < P.kstages; ++s) {
                 mbar_init(&k_full[s], 1);
-                mbar_init(&k_empty[s], kMmaWarps);  // every MMA warp releases every stage
+                mbar_init(&k_empty[s], mma_warps<MODE>());  // every MMA warp releases every stage
             }
             for (int s = 0; s < kMaxQRes; ++s) {
                 mbar_init(&q_full[s], 1);
-                mbar_init(&q_empty[s], resident ? kMmaWarps : 1);  // streamed slots belong to one MMA warp
+                mbar_init(&q_empty[s], resident ? mma_warps<MODE>() : 1);  // streamed slots belong to one MMA warp
             }
             for (int s = 0; s < 4; ++s) {
                 mbar_init(&t_full[s], 1);
@@ -405,7 +419,7 @@ __global__ void __maxnreg__(128)
                 }
             }
         }
-    } else if (warp <= kMmaWarps) {
+    } else if (warp <= mma_warps<MODE>()) {
         // MMA warp mw issues the jobs with (job & 1) == mw into TMEM slot mw;
         // both walk the same segment/tile sequence and both release every K stage.
         const uint32_t mw = uint32_t(warp - 1);
@@ -440,7 +454,7 @@ __global__ void __maxnreg__(128)
                                 ++qload[c];
                             }
                             const int ts = int(job % kStatSlots);  // 128-column slots, one group each
-                            if (ts % kMmaWarps != int(mw)) continue;
+                            if (ts % mma_warps<MODE>() != int(mw)) continue;
                             mbar_wait_pm(&t_empty[ts], ((job / kStatSlots) & 1) ^ 1);
                             tc_fence_after();
                             if (leader) {
@@ -490,7 +504,7 @@ __global__ void __maxnreg__(128)
             }
         }
     } else {  // ------------------------- epilogue (8 warps) -------------------------
-        const int e = warp - 1 - kMmaWarps;
+        const int e = warp - 1 - mma_warps<MODE>();
         const int quarter = warp & 3;  // TMEM lanes this warp may read
         const int half = e >> 2;       // SCORE: column half of every job; STATS: job group (job % 3)
         const int r_local = quarter * 32 + lane;
@@ -500,6 +514,8 @@ __global__ void __maxnreg__(128)
         int lkey = -1;
         const float inv_p = 1.0f / float(P.p);
         const int64_t T1 = MODE == MODE_SCORE ? int64_t(P.p1_pre[P.p1_runs]) : 0;
+        P1PROF(long long pw = 0, pl = 0, pc = 0, pj = 0, po = 0, pfirst = 0; const long long p_beg = clock64(); long long c_prev = p_beg;
+               uint64_t g_beg; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_beg)));
         for (int g = it_beg; g < it_end;) {
             const Seg x = seg_at<MODE>(P, s_pre, g, it_end, T);
             g += x.ntiles();
@@ -530,17 +546,24 @@ __global__ void __maxnreg__(128)
                         else
                             lim = min(P.p, rq % P.p + 1) - (x.p0 + t - x.nc) * P.krows;
                         const int ts = int(job % kStatSlots);
+                        P1PROF(long long c_0 = clock64(); po += c_0 - c_prev);
                         mbar_wait(&t_full[ts], (job / kStatSlots) & 1);
                         tc_fence_after();
                         {
                             float v[64];
+                            P1PROF(long long c_1 = clock64());
                             tmem_ld64(tmem + lane_addr + uint32_t(ts * 128), v);
+                            P1PROF(long long c_2 = clock64());
                             stats_cols<64, POLY>(v, lim, P.c2, m[c], z[c]);
+                            P1PROF(long long c_3 = clock64());
                             tmem_ld64(tmem + lane_addr + uint32_t(ts * 128 + 64), v);
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&t_empty[ts]);  // slot free: values are in registers
+                            P1PROF(long long c_4 = clock64());
                             stats_cols<64, POLY>(v, lim - 64, P.c2, m[c], z[c]);
+                            P1PROF(long long c_5 = clock64(); pw += c_1 - c_0; pl += (c_2 - c_1) + (c_4 - c_3);
+                                   pc += (c_3 - c_2) + (c_5 - c_4); if (pj == 0) pfirst = c_1 - p_beg; ++pj; c_prev = c_5);
                         }
                         ++job;
                     }
@@ -646,6 +669,14 @@ __global__ void __maxnreg__(128)
             named_bar_sync(1, 32 * kEpiWarps);
             flush_coarse(P, lkey / P.H, s_coarse, etid);
         }
+        P1PROF(uint64_t g_end; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end)); const long long p_end = clock64();
+               if (MODE == MODE_STATS && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
+                   printf("P1PROF cta %d warp %2d jobs %lld total %lld wait %lld ld %lld compute %lld between %lld first %lld\n",
+                          blockIdx.x, warp, pj, p_end - p_beg, pw, pl, pc, po, pfirst);
+               if (MODE == MODE_STATS && lane == 0 && warp == 3) {
+                   uint32_t smid; asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                   printf("P1GT %d %llu %llu %u %lld %lld %lld %d %d\n", blockIdx.x, (unsigned long long)g_beg, (unsigned long long)g_end, smid, pj, pw, p_end - p_beg, it_beg, it_end);
+               });
     }
     tc_fence_before();
     __syncthreads();
