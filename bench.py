@@ -473,9 +473,12 @@ def main():
     ap.add_argument("--layer-group", type=int, default=0, help="layers per step group (0 = auto, L2-sized)")
     ap.add_argument("--no-overlap", action="store_true", help="compaction on the main stream")
     ap.add_argument("--fused", action="store_true", help="single-kernel fused step (EPK_OPT_FUSED, experimental)")
+    ap.add_argument("--layers", type=int, default=0, help=argparse.SUPPRESS)  # experiments: override L
     ap.add_argument("--timeline", default=None, help="write one profiled step's kernel timeline to this file")
     args = ap.parse_args()
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.layers:  # experiments only: the metric/config of record is the full config
+        c["L"] = args.layers
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
