@@ -214,6 +214,55 @@ inline TokenScoreMap score_with_prompt(const ForwardTrace& prompt_trace, Aggrega
     return map;
 }
 
+/// keydiff_scores (scoring.hpp:186) on the GPU, bit-exact (fp64 keys,
+/// sequential sums, no FMA): the KeyDiff baseline's scores for every layer.
+inline TokenScoreMap keydiff_scores(const EpisodicCache& cache) {
+    TokenScoreMap map;
+    map.layers.resize(cache.layers.size());
+    epk_ctx* c = detail::ctx();
+    for (std::size_t l = 0; l < cache.layers.size(); ++l) {
+        const LayerCache& layer = cache.layers[l];
+        const std::size_t H = layer.heads.size();
+        map.layers[l].resize(H);
+        std::vector<int32_t> pos, off(H + 1, 0), len(H, 0);
+        std::vector<double> keys;
+        std::size_t dim = 0;
+        for (const auto& head : layer.heads)
+            for (const KVEntry& e : head) dim = std::max(dim, e.key.size());
+        if (dim == 0) {
+            for (std::size_t h = 0; h < H; ++h)
+                for (const KVEntry& e : layer.heads[h]) map.layers[l][h].emplace(e.position, 0.0);
+            continue;
+        }
+        for (std::size_t h = 0; h < H; ++h) {
+            for (const KVEntry& e : layer.heads[h]) {
+                if (e.key.size() != dim) throw DimensionError("keydiff_scores: key dimension mismatch");
+                pos.push_back(int32_t(e.position & 0x7fffffff));
+                keys.insert(keys.end(), e.key.begin(), e.key.end());
+            }
+            len[h] = int32_t(layer.heads[h].size());
+            off[h + 1] = off[h] + len[h];
+        }
+        const std::size_t n = pos.size();
+        if (n == 0) continue;
+        detail::DBuf<int32_t> d_pos(n), d_off(H + 1), d_len(H);
+        detail::DBuf<double> d_k(n * dim), d_out(n);
+        d_pos.upload(pos.data(), n);
+        d_off.upload(off.data(), H + 1);
+        d_len.upload(len.data(), H);
+        d_k.upload(keys.data(), keys.size());
+        const int64_t base[2] = {0, int64_t(n)};
+        epk_cache_desc desc{1, int32_t(H), int32_t(dim), EPK_F64, d_k.p, d_k.p, d_pos.p, d_off.p, d_len.p, base};
+        detail::check(epk_score_keydiff(c, &desc, d_out.p));
+        std::vector<double> out(n);
+        d_out.download(out.data(), n);
+        std::size_t r = 0;
+        for (std::size_t h = 0; h < H; ++h)
+            for (const KVEntry& e : layer.heads[h]) map.layers[l][h].emplace(e.position, out[r++]);
+    }
+    return map;
+}
+
 /// kmeans (clustering.hpp:148) on the GPU, bit-exact (fp64, same RNG stream).
 inline KMeansResult kmeans(const std::vector<Vec>& points, std::size_t k, std::uint64_t seed,
                            std::size_t max_iters = 64) {
@@ -289,8 +338,8 @@ inline SensitivityProfile measure_sensitivity(const Model& model, std::span<cons
 /// The toy-model forwards (block and prompt) are the reference's own, on the
 /// host; every block's prompt grids are scored by the GPU reduction and every
 /// layer is evicted by the GPU selection, so the result is bit-identical to
-/// the reference.  Supports the patched, snapkv, kvzip, infinipot and
-/// streaming scorers (KeyDiff stays on the reference path).
+/// the reference.  Supports every scorer: patched, snapkv, kvzip, infinipot
+/// (GPU prompt scoring), keydiff (GPU KeyDiff scores) and streaming.
 inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> context,
                                    const BlockPrefillConfig& config, std::size_t episode_id = 0,
                                    std::span<const std::size_t> positions = {}) {
@@ -300,7 +349,6 @@ inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> 
         throw Error("block_prefill: budget and block size must be >= 1");
     if (config.scorer == ScorerKind::patched && !config.prompt_provider)
         throw Error("block_prefill: patched scorer needs a prompt provider");
-    if (config.scorer == ScorerKind::keydiff) return epikv::block_prefill(model, context, config, episode_id, positions);
     std::vector<std::size_t> default_positions;
     if (positions.empty()) {
         default_positions.resize(context.size());
@@ -368,6 +416,8 @@ inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> 
             report.occupancy.record(OccupancyKind::PromptResident, entries(report.cache),
                                     std::vector<std::size_t>(cfg.layers, cfg.kv_heads * prompt.tokens.size()));
             scores = gpu::score_with_prompt(prompt_trace, config.aggregation);
+        } else if (config.scorer == ScorerKind::keydiff) {
+            scores = gpu::keydiff_scores(report.cache);
         } else {
             scores.layers.resize(report.cache.layers.size());
             for (std::size_t l = 0; l < report.cache.layers.size(); ++l) {

@@ -27,6 +27,7 @@
  *                        score -> per-layer evict, all layers
  *   epk_kmeans*          kmeans (clustering.hpp:148-260)
  *   epk_key_cosine_sigma measure_sensitivity reduction (allocation.hpp:80-100)
+ *   epk_score_keydiff    keydiff_scores (scoring.hpp:186-221), the KeyDiff baseline
  */
 #ifndef EPK_EPK_H
 #define EPK_EPK_H
@@ -212,6 +213,15 @@ int epk_kmeans_sq_dist(epk_ctx* ctx, const double* points, int64_t n, int64_t di
 int epk_kmeans(epk_ctx* ctx, const double* points, int64_t n, int64_t dim, int64_t k,
                uint64_t seed, int64_t max_iters, int64_t* assign_out, double* centroids_out,
                int64_t* iterations_out, double* sse_out);
+
+/* ---- K6: KeyDiff baseline scorer ------------------------------------------ *
+ * scores[layer_base[l] + r] = -cosine(key_r, mean key of r's (layer, head)),
+ * or 0 when either norm is zero (keydiff_scores, scoring.hpp:186-221), fp64
+ * [dev] in cache row order; gap rows are not written.  Bit-exact with the
+ * reference (fp64, sequential sums, no FMA).  Feed the scores to
+ * epk_select_pooled (score_dtype EPK_F64) + epk_compact.  Cache dtype F32,
+ * BF16 or F64 (keys only are read), head_dim <= 256.  Asynchronous. */
+int epk_score_keydiff(epk_ctx* ctx, const epk_cache_desc* cache, double* scores);
 
 /* ---- K5: layer sensitivity ------------------------------------------------ *
  * sigma[l] = mean over (h, t) of cosine(k_full, k_block), zero-norm pairs

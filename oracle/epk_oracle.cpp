@@ -435,6 +435,41 @@ void sensitivity(int layers, int hkv, i64 ntok, int d, const double* kf, const d
     *skipped = skip;
 }
 
+// §8(f) rank 1, KeyDiff baseline: keydiff_scores (scoring.hpp:186-221).  Per
+// (layer, kv-head) the anchor is the mean key (per-dimension sum in entry
+// order, then / n); each entry scores -cosine(key, anchor) (numerics.hpp:
+// 52-87: sequential dot and norms, clamp to [-1, 1]), or 0 when the anchor or
+// the key has zero norm.  One layer: rows of head h are [head_off[h],
+// head_off[h+1]), keys [rows][d].
+// ---------------------------------------------------------------------------
+void keydiff_layer(int hkv, int d, const i64* head_off, const double* k, double* out) {
+    std::vector<double> anchor(static_cast<size_t>(d));
+    for (int h = 0; h < hkv; ++h) {
+        const i64 r0 = head_off[h], r1 = head_off[h + 1];
+        if (r1 <= r0) continue;
+        std::fill(anchor.begin(), anchor.end(), 0.0);
+        for (i64 r = r0; r < r1; ++r)
+            for (int i = 0; i < d; ++i) anchor[size_t(i)] += k[r * d + i];
+        for (int i = 0; i < d; ++i) anchor[size_t(i)] /= double(r1 - r0);
+        double nb = 0.0;
+        for (int i = 0; i < d; ++i) nb += anchor[size_t(i)] * anchor[size_t(i)];
+        nb = std::sqrt(nb);
+        for (i64 r = r0; r < r1; ++r) {
+            const double* a = k + r * d;
+            double na = 0.0, dot = 0.0;
+            for (int i = 0; i < d; ++i) na += a[i] * a[i];
+            na = std::sqrt(na);
+            double score = 0.0;
+            if (nb != 0.0 && na != 0.0) {
+                for (int i = 0; i < d; ++i) dot += a[i] * anchor[size_t(i)];
+                score = -std::clamp(dot / (na * nb), -1.0, 1.0);
+            }
+            out[r] = score;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // a11: allocate (allocation.hpp:120-198).  Returns 0, or -1 on error.
 int allocate(const double* sens, int layers, i64 per_head_budget, double alpha, i64* budgets_out,
              double* weights_out) {
@@ -569,6 +604,10 @@ int orc_kmeans(const double* pts, i64 n, i64 dim, i64 k, std::uint64_t seed, i64
 void orc_sensitivity(int layers, int hkv, i64 ntok, int d, const double* kf, const double* kb,
                      double* sigma, i64* skipped) {
     sensitivity(layers, hkv, ntok, d, kf, kb, sigma, skipped);
+}
+
+void orc_keydiff_layer(int hkv, int d, const i64* head_off, const double* k, double* out) {
+    keydiff_layer(hkv, d, head_off, k, out);
 }
 
 int orc_allocate(const double* sens, int layers, i64 per_head_budget, double alpha,

@@ -62,6 +62,8 @@ def orc():
         lib.orc_kmeans.restype = C.c_int
         lib.orc_sensitivity.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _f64p, _f64p, _f64p, _i64p]
         lib.orc_allocate.argtypes = [_f64p, C.c_int, C.c_int64, C.c_double, _i64p, _f64p]
+        lib.orc_keydiff_layer.argtypes = [C.c_int, C.c_int, _i64p, _f64p, _f64p]
+        lib.orc_keydiff_layer.restype = None
         lib.orc_allocate.restype = C.c_int
         _orc = lib
     return _orc
@@ -92,6 +94,8 @@ def ref():
         lib.ref_top_k_indices.argtypes = [_f64p, C.c_int64, C.c_int64, _i64p]
         lib.ref_top_k_indices.restype = C.c_int64
         lib.ref_cosine.argtypes = [_f64p, _f64p, C.c_int64]
+        lib.ref_keydiff_layer.argtypes = [C.c_int, C.c_int, _i64p, _i64p, _f64p, _f64p]
+        lib.ref_keydiff_layer.restype = C.c_int
         lib.ref_cosine.restype = C.c_double
         lib.ref_kmeans.argtypes = [_f64p, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int64,
                                    _i64p, _f64p, _i64p, _f64p]
@@ -222,6 +226,15 @@ def sensitivity(kf, kb):
     return sigma, int(skipped[0])
 
 
+def keydiff_layer(k, head_off):
+    """KeyDiff scores of one layer (scoring.hpp:186-221), rows in cache order."""
+    k = _c(k, np.float64)
+    ho = _c(head_off, np.int64)
+    out = np.zeros(k.shape[0], np.float64)
+    orc().orc_keydiff_layer(len(ho) - 1, k.shape[1], ho, k.reshape(-1), out)
+    return out
+
+
 def allocate(sens, per_head_budget, alpha):
     sens = _c(sens, np.float64)
     b = np.zeros(sens.size, np.int64)
@@ -298,6 +311,14 @@ def ref_top_k_indices(scores, k):
     out = np.zeros(max(scores.size, 1), np.int64)
     m = ref().ref_top_k_indices(scores, scores.size, int(k), out)
     return out[:m]
+
+
+def ref_keydiff_layer(k, head_off, pos):
+    k = _c(k, np.float64)
+    ho = _c(head_off, np.int64)
+    out = np.zeros(k.shape[0], np.float64)
+    _check(ref().ref_keydiff_layer(len(ho) - 1, k.shape[1], ho, _c(pos, np.int64), k.reshape(-1), out))
+    return out
 
 
 def ref_cosine(a, b):

@@ -222,6 +222,21 @@ i64 ref_top_k_indices(const double* scores, i64 n, i64 k, i64* out) {
     return i64(idx.size());
 }
 
+// keydiff_scores (scoring.hpp:186) over a one-layer EpisodicCache.
+int ref_keydiff_layer(int hkv, int d, const i64* head_off, const i64* pos, const double* k, double* out) {
+    try {
+        std::vector<double> v(size_t(head_off[hkv]) * size_t(d), 0.0);
+        epikv::EpisodicCache cache;
+        cache.layers.push_back(build_layer(hkv, 0, d, head_off, pos, k, v.data()));
+        const epikv::TokenScoreMap map = epikv::keydiff_scores(cache);
+        for (int h = 0; h < hkv; ++h)
+            for (i64 r = head_off[h]; r < head_off[h + 1]; ++r) out[r] = map.at(0, size_t(h), size_t(pos[r]));
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exception(e);
+    }
+}
+
 double ref_cosine(const double* a, const double* b, i64 d) {
     try {
         return epikv::cosine(std::span<const double>(a, size_t(d)), std::span<const double>(b, size_t(d)));

@@ -70,6 +70,7 @@ _SIGS = {
     "epk_kmeans_sq_dist": (C.c_int, [vp, vp, i64, i64, vp, vp, vp]),
     "epk_kmeans": (C.c_int, [vp, vp, i64, i64, i64, u64, i64, vp, vp, vp, vp]),
     "epk_key_cosine_sigma": (C.c_int, [vp, vp, vp, i32, i32, i32, i64, i32, vp, vp]),
+    "epk_score_keydiff": (C.c_int, [vp, vp, vp]),
     "epk_debug_expf": (C.c_int, [vp, vp, vp, i64]),
     "epk_debug_tma_stream": (C.c_int, [vp, vp, i64, i32, i32, i32]),
     "epk_debug_mma_rate": (C.c_int, [vp, i32, i32, i32]),

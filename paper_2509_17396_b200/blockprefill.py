@@ -22,7 +22,7 @@ import torch
 from .context import default_context
 from .errors import DimensionError, Error
 from .kvcache import EpisodeCache, compact, select_pooled, append_to_cache
-from .scoring import score_with_prompt
+from .scoring import keydiff_scores, score_with_prompt
 
 
 class StateProvider(Protocol):
@@ -38,7 +38,7 @@ class BlockPrefillConfig:
     """BlockPrefillConfig (blockprefill.hpp:27-35)."""
     budget_per_head: int = 64
     block_size: int = 16
-    scorer: str = "patched"        # patched | streaming
+    scorer: str = "patched"        # patched | keydiff | streaming
     aggregation: str = "max"       # max | avg
     layer_budgets: list | None = None  # BudgetAllocation.layer_budgets, or None for uniform
     streaming_sink: int = 128
@@ -99,7 +99,7 @@ def block_prefill(provider: StateProvider, layers: int, q_heads: int, kv_heads: 
         if config.layer_budgets is not None and any(config.streaming_sink > b for b in budgets):
             raise Error("block_prefill: streaming sink exceeds an allocated layer budget")
         pins = set(range(config.streaming_sink))
-    elif config.scorer != "patched":
+    elif config.scorer not in ("patched", "keydiff"):
         raise Error(f"block_prefill: scorer '{config.scorer}' not supported on the GPU path")
 
     device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -131,6 +131,8 @@ def block_prefill(provider: StateProvider, layers: int, q_heads: int, kv_heads: 
             report.occupancy.append(OccupancySample(len(report.occupancy), "prompt", before,
                                                     [kv_heads * p] * layers))
             sc = score_with_prompt(bufs[cur], q, kp, config.aggregation, config.mode, ctx=ctx)
+        elif config.scorer == "keydiff":
+            sc = keydiff_scores(bufs[cur], ctx=ctx)  # keydiff_scores (scoring.hpp:186-221)
         else:
             sc = bufs[cur].pos.to(torch.float64)  # streaming_scores (blockprefill.hpp:70-82)
         nxt = 1 - cur

@@ -140,6 +140,7 @@ int launch_km_sums(epk_ctx*, const double*, int64_t, int64_t, const int64_t*, in
 int launch_km_finalize(epk_ctx*, const double*, const int64_t*, int64_t, int64_t, double*);
 int launch_km_sqdist(epk_ctx*, const double*, int64_t, int64_t, const double*, const int64_t*, double*);
 int launch_key_cosine(epk_ctx*, const void*, const void*, int, int, int, int64_t, int, double*, int64_t*);
+int launch_keydiff(epk_ctx*, const epk_cache_desc*, double*);
 
 static int check_ctx(epk_ctx* ctx) {
     if (!ctx) return fail(EPK_ERR_ARG, "null context");
@@ -733,6 +734,14 @@ int epk_key_cosine_sigma(epk_ctx* ctx, const void* kf, const void* kb, int32_t d
     if (layers < 1 || H < 1 || ntok < 1 || dim < 1) return fail(EPK_ERR_ARG, "key_cosine: empty input");
     if (dtype != EPK_F32 && dtype != EPK_BF16 && dtype != EPK_F64) return fail(EPK_ERR_ARG, "key_cosine: bad dtype");
     return launch_key_cosine(ctx, kf, kb, dtype, layers, H, ntok, dim, sigma, skipped);
+}
+
+int epk_score_keydiff(epk_ctx* ctx, const epk_cache_desc* cache, double* scores) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(cache))) return rc;
+    if (!scores) return fail(EPK_ERR_ARG, "keydiff: null scores");
+    return launch_keydiff(ctx, cache, scores);
 }
 
 // ---- diagnostics ---------------------------------------------------------------

@@ -83,6 +83,20 @@ def score_grids(grids, head_off, q_heads: int, aggregation: str = "max", ctx: Co
     return out.cpu().numpy()
 
 
+def keydiff_scores(cache: EpisodeCache, out: torch.Tensor | None = None, ctx: Context | None = None) -> torch.Tensor:
+    """keydiff_scores (scoring.hpp:186-221): per (layer, kv-head) every live
+    entry scores -cosine(key, mean key), 0 on a zero norm.  fp64 [cache.rows]
+    in cache row order (gap rows unspecified), bit-exact with the reference;
+    feed it to select_pooled + compact like any other score."""
+    ctx = ctx or default_context(cache.device.index)
+    if cache.dtype not in (torch.bfloat16, torch.float32, torch.float64):
+        raise Error("keydiff_scores: cache dtype must be bf16, fp32 or fp64")
+    out = out if out is not None else torch.zeros(cache.rows, dtype=torch.float64, device=cache.device)
+    d = cache.desc()
+    _lib.call("epk_score_keydiff", ctx.handle, C.byref(d), ptr(out))
+    return out
+
+
 def debug_expf(x: torch.Tensor, ctx: Context | None = None) -> torch.Tensor:
     """The device epk_expf (EPK-F32 v1), for the bitwise parity test."""
     ctx = ctx or default_context(x.device.index)

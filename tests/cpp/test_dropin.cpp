@@ -214,6 +214,7 @@ static void test_block_prefill() {
     const Case cases[] = {{1, 1, 1, 9, 1, 3, ScorerKind::patched},   {2, 2, 2, 120, 8, 16, ScorerKind::patched},
                           {2, 4, 2, 100, 5, 12, ScorerKind::snapkv}, {2, 2, 1, 90, 6, 10, ScorerKind::kvzip},
                           {2, 2, 2, 70, 6, 16, ScorerKind::infinipot}, {2, 2, 2, 80, 8, 16, ScorerKind::streaming},
+                          {2, 2, 2, 90, 7, 16, ScorerKind::keydiff},
                           {3, 6, 3, 200, 10, 24, ScorerKind::patched}};
     for (const Case& c : cases) {
         const Model model = init_model(small(c.layers, c.q, c.kv));

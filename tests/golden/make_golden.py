@@ -74,6 +74,18 @@ def main():
     g["bp_alloc_counts"] = counts.sum(axis=1)
     series, ev, nb, counts, _ = O.ref_block_prefill(2, 4, 2, 8, 3, 120, 5, 8, 16, [7, 21, 42])
     g["bp_120_series"], g["bp_120_evictions"], g["bp_120_counts"] = series, ev, counts
+    # KeyDiff scores (keydiff_scores, scoring.hpp:186), own RNG stream: ragged
+    # heads, an empty head, a zero key, a zero-anchor head
+    krng = np.random.default_rng(186)
+    for i, (d, counts) in enumerate([(8, [5, 0, 9, 3]), (16, [40, 33]), (128, [64, 1, 17]), (4, [6, 6])]):
+        ho, pos, k, _ = random_layer(krng, len(counts), counts, d)
+        if i == 0:
+            k[2] = 0.0
+        if i == 3:
+            k[6:12] = 0.0
+        g[f"kd{i}_head_off"], g[f"kd{i}_pos"], g[f"kd{i}_k"] = ho, pos, k
+        g[f"kd{i}_scores"] = O.ref_keydiff_layer(k, ho, pos)
+    g["kd_count"] = 4
     np.savez_compressed(OUT, **g)
     print(OUT, os.path.getsize(OUT), "bytes")
 

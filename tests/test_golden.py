@@ -48,6 +48,12 @@ def test_sensitivity_fixture(orc, g):
     assert np.array_equal(sigma, g["sens_sigma"]) and skipped == int(g["sens_skipped"])
 
 
+def test_keydiff_fixtures_bitwise(orc, g):
+    for i in range(int(g["kd_count"])):
+        s = orc.keydiff_layer(g[f"kd{i}_k"], g[f"kd{i}_head_off"])
+        assert np.array_equal(s, g[f"kd{i}_scores"]), i
+
+
 def test_trace_fixture(g):
     assert g["bp_c2_series"].tolist() == [3, 1, 4, 1, 4, 1]
     assert g["bp_alloc_counts"].tolist() == [4, 12]

@@ -166,3 +166,22 @@ def test_block_prefill_trace_c2(ref):
     # acceptance C2 / test_blockprefill.cpp:70-79
     series, ev, nb, counts, _ = ref.ref_block_prefill(1, 1, 1, 8, 3, 9, 2, 1, 3, [7, 21, 42])
     assert series.tolist() == [3, 1, 4, 1, 4, 1] and nb == 3
+
+
+def test_keydiff_bitwise(ref):
+    """KeyDiff restatement (scoring.hpp:186-221) vs the reference: ragged heads,
+    empty head, zero key, zero-anchor head, bf16-valued keys."""
+    import torch
+    rng = np.random.default_rng(7)
+    for trial in range(12):
+        H = int(rng.integers(1, 9))
+        counts = rng.integers(0, 300, H)
+        d = int(rng.choice([4, 64, 128]))
+        ho, pos, k, _ = random_layer(rng, H, counts, d)
+        if trial % 3 == 1:
+            k = torch.as_tensor(k, dtype=torch.float32).bfloat16().double().numpy()
+        if trial % 4 == 2 and len(pos):
+            k[rng.integers(0, len(pos))] = 0.0
+        if trial % 5 == 3 and counts[0] > 0:
+            k[ho[0]:ho[1]] = 0.0
+        assert np.array_equal(ref.keydiff_layer(k, ho), ref.ref_keydiff_layer(k, ho, pos)), trial
