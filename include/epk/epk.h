@@ -28,6 +28,7 @@
  *   epk_kmeans*          kmeans (clustering.hpp:148-260)
  *   epk_key_cosine_sigma measure_sensitivity reduction (allocation.hpp:80-100)
  *   epk_score_keydiff    keydiff_scores (scoring.hpp:186-221), the KeyDiff baseline
+ *   epk_serialize_epkv   persist (kvcache.hpp:281-317), the episodic cache store's writer
  */
 #ifndef EPK_EPK_H
 #define EPK_EPK_H
@@ -222,6 +223,20 @@ int epk_kmeans(epk_ctx* ctx, const double* points, int64_t n, int64_t dim, int64
  * epk_select_pooled (score_dtype EPK_F64) + epk_compact.  Cache dtype F32,
  * BF16 or F64 (keys only are read), head_dim <= 256.  Asynchronous. */
 int epk_score_keydiff(epk_ctx* ctx, const epk_cache_desc* cache, double* scores);
+
+/* ---- K7: episodic cache store (.epkv) --------------------------------------- *
+ * Serialises `cache` into the byte stream persist (kvcache.hpp:281-317) writes:
+ * header (magic "EPKV", version 1, episode_id, layer / head counts, provenance
+ * scorer string, budget_per_head, layer_budgets [host, n_layer_budgets]), then
+ * per layer its budget (layer_budgets[l], else budget_per_head) and heads, per
+ * head its entry count, per entry position (u64), dim (u32) and key + value
+ * widened to fp64 (bitwise the reference's reals).  out [dev, 16-byte aligned]
+ * receives the file's bytes at out + *offset_out (0..15 leading pad bytes),
+ * *total_out bytes long; out = NULL only computes the two sizes.  Capacity
+ * must be >= offset + total.  Synchronous (reads the head lengths). */
+int epk_serialize_epkv(epk_ctx* ctx, const epk_cache_desc* cache, uint64_t episode_id, const char* scorer,
+                       uint64_t budget_per_head, const int64_t* layer_budgets, int32_t n_layer_budgets,
+                       uint8_t* out, int64_t capacity, int64_t* offset_out, int64_t* total_out);
 
 /* ---- K5: layer sensitivity ------------------------------------------------ *
  * sigma[l] = mean over (h, t) of cosine(k_full, k_block), zero-norm pairs

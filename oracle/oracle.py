@@ -96,6 +96,11 @@ def ref():
         lib.ref_cosine.argtypes = [_f64p, _f64p, C.c_int64]
         lib.ref_keydiff_layer.argtypes = [C.c_int, C.c_int, _i64p, _i64p, _f64p, _f64p]
         lib.ref_keydiff_layer.restype = C.c_int
+        lib.ref_persist.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, _i64p, C.c_int, C.c_int, C.c_int,
+                                    C.c_int, _i64p, _i64p, _f64p, _f64p, _i64p]
+        lib.ref_persist.restype = C.c_int64
+        lib.ref_load_repersist.argtypes = [C.c_char_p, C.c_char_p]
+        lib.ref_load_repersist.restype = C.c_int64
         lib.ref_cosine.restype = C.c_double
         lib.ref_kmeans.argtypes = [_f64p, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int64,
                                    _i64p, _f64p, _i64p, _f64p]
@@ -319,6 +324,36 @@ def ref_keydiff_layer(k, head_off, pos):
     out = np.zeros(k.shape[0], np.float64)
     _check(ref().ref_keydiff_layer(len(ho) - 1, k.shape[1], ho, _c(pos, np.int64), k.reshape(-1), out))
     return out
+
+
+def ref_persist(path, per_layer, episode_id=0, scorer="patched", budget_per_head=0, layer_budgets=(),
+                layer_budget_fields=None):
+    """persist (kvcache.hpp:281) of per_layer[l] = (head_counts, pos, k, v) (fp64)."""
+    L = len(per_layer)
+    H = len(per_layer[0][0])
+    d = per_layer[0][2].shape[1]
+    ho, rows = [], 0
+    for counts, _, _, _ in per_layer:
+        c = np.concatenate([[0], np.cumsum(counts)]) + rows
+        ho.append(c)
+        rows = int(c[-1])
+    pos = np.concatenate([p for _, p, _, _ in per_layer]).astype(np.int64)
+    k = np.concatenate([x for _, _, x, _ in per_layer]).astype(np.float64)
+    v = np.concatenate([x for _, _, _, x in per_layer]).astype(np.float64)
+    lb = _c(np.asarray(list(layer_budgets) or [0], np.int64), np.int64)
+    fields = _c(np.asarray(layer_budget_fields if layer_budget_fields is not None else [budget_per_head] * L,
+                           np.int64), np.int64)
+    n = ref().ref_persist(str(path).encode(), int(episode_id), scorer.encode(), int(budget_per_head), lb,
+                          len(list(layer_budgets)), L, H, d, _c(np.concatenate(ho), np.int64), _c(pos, np.int64),
+                          _c(k, np.float64), _c(v, np.float64), fields)
+    _check(n)
+    return int(n)
+
+
+def ref_load_repersist(src, dst):
+    n = ref().ref_load_repersist(str(src).encode(), str(dst).encode())
+    _check(n)
+    return int(n)
 
 
 def ref_cosine(a, b):

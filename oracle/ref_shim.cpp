@@ -237,6 +237,36 @@ int ref_keydiff_layer(int hkv, int d, const i64* head_off, const i64* pos, const
     }
 }
 
+// persist (kvcache.hpp:281) of an EpisodicCache built from flat arrays:
+// layer l's heads are rows [head_off[l*(H+1)+h], head_off[l*(H+1)+h+1]) of
+// pos / k / v ([rows][d] fp64).  Returns the byte count or a negative code.
+i64 ref_persist(const char* path, std::uint64_t episode_id, const char* scorer, std::uint64_t budget_per_head,
+                const i64* layer_budgets, int n_layer_budgets, int layers, int hkv, int d, const i64* head_off,
+                const i64* pos, const double* k, const double* v, const i64* layer_budget_fields) {
+    try {
+        epikv::EpisodicCache cache;
+        cache.episode_id = episode_id;
+        cache.provenance.scorer = scorer;
+        cache.provenance.budget_per_head = budget_per_head;
+        for (int i = 0; i < n_layer_budgets; ++i) cache.provenance.layer_budgets.push_back(size_t(layer_budgets[i]));
+        for (int l = 0; l < layers; ++l)
+            cache.layers.push_back(build_layer(hkv, layer_budget_fields[l], d, head_off + i64(l) * (hkv + 1), pos, k, v));
+        return i64(epikv::persist(cache, path));
+    } catch (const std::exception& e) {
+        return map_exception(e);
+    }
+}
+
+// load_cache (kvcache.hpp:321) of `in`, persisted again to `out`: the
+// reference reads our files (round trip).  Returns the bytes written.
+i64 ref_load_repersist(const char* in, const char* out) {
+    try {
+        return i64(epikv::persist(epikv::load_cache(in), out));
+    } catch (const std::exception& e) {
+        return map_exception(e);
+    }
+}
+
 double ref_cosine(const double* a, const double* b, i64 d) {
     try {
         return epikv::cosine(std::span<const double>(a, size_t(d)), std::span<const double>(b, size_t(d)));

@@ -13,5 +13,7 @@ from .clustering import KMeansResult, kmeans, kmeans_sharded  # noqa: F401
 from .allocation import (BudgetAllocation, SensitivityProfile, allocate, sensitivity_from_keys,  # noqa: F401
                          uniform_allocation)
 from .context import Context, default_context  # noqa: F401
+from .store import (CacheMeta, CacheStore, SessionState, centroid_similarity, load_cache, manifest_json,  # noqa: F401
+                    persist, route, serialize)
 
 __version__ = "0.1.0"

@@ -141,6 +141,8 @@ int launch_km_finalize(epk_ctx*, const double*, const int64_t*, int64_t, int64_t
 int launch_km_sqdist(epk_ctx*, const double*, int64_t, int64_t, const double*, const int64_t*, double*);
 int launch_key_cosine(epk_ctx*, const void*, const void*, int, int, int, int64_t, int, double*, int64_t*);
 int launch_keydiff(epk_ctx*, const epk_cache_desc*, double*);
+int launch_serialize_epkv(epk_ctx*, const epk_cache_desc*, uint64_t, const char*, uint64_t, const int64_t*, int32_t,
+                          uint8_t*, int64_t, int64_t*, int64_t*);
 
 static int check_ctx(epk_ctx* ctx) {
     if (!ctx) return fail(EPK_ERR_ARG, "null context");
@@ -742,6 +744,17 @@ int epk_score_keydiff(epk_ctx* ctx, const epk_cache_desc* cache, double* scores)
     if ((rc = check_cache(cache))) return rc;
     if (!scores) return fail(EPK_ERR_ARG, "keydiff: null scores");
     return launch_keydiff(ctx, cache, scores);
+}
+
+int epk_serialize_epkv(epk_ctx* ctx, const epk_cache_desc* cache, uint64_t episode_id, const char* scorer,
+                       uint64_t budget_per_head, const int64_t* layer_budgets, int32_t n_layer_budgets,
+                       uint8_t* out, int64_t capacity, int64_t* offset_out, int64_t* total_out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(cache))) return rc;
+    if (n_layer_budgets < 0) return fail(EPK_ERR_ARG, "persist: negative layer budget count");
+    return launch_serialize_epkv(ctx, cache, episode_id, scorer, budget_per_head, layer_budgets, n_layer_budgets, out,
+                                 capacity, offset_out, total_out);
 }
 
 // ---- diagnostics ---------------------------------------------------------------

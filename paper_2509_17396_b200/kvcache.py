@@ -72,23 +72,26 @@ class EpisodeCache:
         self.head_off.copy_(torch.from_numpy(off.astype(np.int32)))
         self.head_len.zero_()
 
-    def load_layers(self, per_layer) -> None:
+    def load_layers(self, per_layer, slack: int = 0) -> None:
         """Fills the cache from host data.  per_layer[l] = (head_counts[H], pos[n], k[n,d], v[n,d]),
-        rows head-major and position-sorted within each head; stored dense (no slack)."""
+        rows head-major and position-sorted within each head; every head is
+        followed by `slack` free rows (0: stored dense)."""
         offs = np.zeros((self.layers, self.kv_heads + 1), np.int32)
         lens = np.zeros((self.layers, self.kv_heads), np.int32)
         for l, (counts, pos, k, v) in enumerate(per_layer):
             counts = np.asarray(counts, np.int64)
             n = int(counts.sum())
-            if n > self.capacity[l]:
-                raise Error(f"load_layers: layer {l} has {n} rows > capacity {self.capacity[l]}")
-            offs[l, 1:] = np.cumsum(counts)
+            if n + slack * self.kv_heads > self.capacity[l]:
+                raise Error(f"load_layers: layer {l} has {n} rows (+ slack) > capacity {self.capacity[l]}")
+            offs[l, 1:] = np.cumsum(counts + slack)
             lens[l] = counts
             b = int(self.layer_base[l])
             if n:
-                self.pos[b:b + n] = torch.as_tensor(np.asarray(pos, np.int32), device=self.device)
-                self.k[b:b + n] = torch.as_tensor(np.asarray(k), device=self.device).to(self.dtype)
-                self.v[b:b + n] = torch.as_tensor(np.asarray(v), device=self.device).to(self.dtype)
+                dst = np.concatenate([np.arange(offs[l, h], offs[l, h] + counts[h]) for h in range(self.kv_heads)]) + b
+                it = torch.as_tensor(dst, device=self.device, dtype=torch.int64)
+                self.pos[it] = torch.as_tensor(np.asarray(pos, np.int32), device=self.device)
+                self.k[it] = torch.as_tensor(np.asarray(k), device=self.device).to(self.dtype)
+                self.v[it] = torch.as_tensor(np.asarray(v), device=self.device).to(self.dtype)
         self.head_off.copy_(torch.from_numpy(offs))
         self.head_len.copy_(torch.from_numpy(lens))
 

@@ -86,6 +86,21 @@ def main():
         g[f"kd{i}_head_off"], g[f"kd{i}_pos"], g[f"kd{i}_k"] = ho, pos, k
         g[f"kd{i}_scores"] = O.ref_keydiff_layer(k, ho, pos)
     g["kd_count"] = 4
+    # a .epkv file written by the reference's persist (kvcache.hpp:281)
+    import tempfile
+    erng = np.random.default_rng(281)
+    pl = []
+    for l, counts in enumerate([[3, 0, 2], [1, 4, 1]]):
+        c = np.asarray(counts, np.int64)
+        n = int(c.sum())
+        pos = np.concatenate([np.sort(erng.choice(100, int(x), replace=False)) for x in c]).astype(np.int64)
+        pl.append((c, pos, erng.standard_normal((n, 8)), erng.standard_normal((n, 8))))
+        g[f"epkv_counts{l}"], g[f"epkv_pos{l}"], g[f"epkv_k{l}"], g[f"epkv_v{l}"] = pl[-1]
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "e.epkv")
+        O.ref_persist(path, pl, episode_id=5, scorer="keydiff", budget_per_head=3, layer_budgets=[2, 4],
+                      layer_budget_fields=[2, 4])
+        g["epkv_bytes"] = np.frombuffer(open(path, "rb").read(), np.uint8)
     np.savez_compressed(OUT, **g)
     print(OUT, os.path.getsize(OUT), "bytes")
 
