@@ -190,6 +190,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_gather_kernel(const
     int32_t run = P.chunk_prefix[layer * P.max_chunks + chunk];
     const int rv = P.row_vec;
     const int hl = lane >> 4, cl = lane & 15;
+    // the chunk's first head and where the next one starts (a chunk rarely
+    // crosses a head boundary: rows past it take the binary search)
+    const int h0 = P.slack ? head_of_row(off, P.H, r0) : 0;
+    const int64_t h0_end = P.slack ? int64_t(off[h0 + 1]) : 0;
     for (int sc = 0; sc < kChunkRows / 32; ++sc) {
         const int64_t rs = r0 + sc * 32;
         if (rs >= rows) break;
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_gather_kernel(const
         int64_t dst = 0;
         if (k) {
             dst = out_base + run + __popc(bal & ((1u << lane) - 1u));
-            if (P.slack) dst += int64_t(P.slack) * head_of_row(off, P.H, r);
+            if (P.slack) dst += int64_t(P.slack) * (r < h0_end ? h0 : head_of_row(off, P.H, r));
             P.out_pos[dst] = P.in_pos[in_base + r];
         }
         run += __popc(bal);

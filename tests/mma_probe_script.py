@@ -5,7 +5,7 @@ import paper_2509_17396_b200 as epk
 from paper_2509_17396_b200 import _lib
 ctx = epk.default_context(0)
 iters = 4000
-for n in ():
+for n in (128, 256):
     for drain in (0, 1):
         ctx.profile(True)
         for _ in range(4):
