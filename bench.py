@@ -329,12 +329,16 @@ def run_e2e(args, c, epk, torch, device, ctx, dist):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    # device-timed like the kernel-only value: events on the compute stream
+    # bracket every step's H2D wait, append + evict step and D2H of its result
+    e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_a.record(comp)
     for i in range(nwarm, nwarm + steps):
         one(i)
-    t1 = time.perf_counter()
+    e_b.record(comp)
+    e_b.synchronize()
     copy_s.synchronize()
-    tt = torch.tensor([t1 - t0], device=device, dtype=torch.float64)
+    tt = torch.tensor([e_a.elapsed_time(e_b) / 1000.0], device=device, dtype=torch.float64)
     if dist is not None:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     world = dist.get_world_size() if dist is not None else 1
@@ -492,11 +496,17 @@ def main():
 
     import torch
     dist = None
-    device = torch.device("cuda", local)
+    # EPK_BENCH_SHARE_GPU=1 (plumbing tests only): ranks share the visible GPUs
+    # round-robin and talk over gloo, so the N>1 path runs on a 1-GPU box
+    share = os.environ.get("EPK_BENCH_SHARE_GPU") == "1"
+    device = torch.device("cuda", local % torch.cuda.device_count() if share else local)
     torch.cuda.set_device(device)
     if world > 1:
         import torch.distributed as td
-        td.init_process_group("nccl", device_id=device)
+        if share:
+            td.init_process_group("gloo")
+        else:
+            td.init_process_group("nccl", device_id=device)
         dist = td
     r = run_ours(args, c, rank, world, device, torch, dist)
     hbm, tc_sus, tc_burst, peak_src = load_peaks()
