@@ -134,8 +134,9 @@ int epk_ctx_profile_timeline(epk_ctx* ctx, int64_t index, char* name_out, float*
  * scores[layer_base[l] + r] = score of live row r of layer l (fp32 [dev]).
  *   q_prompt [dev] [layers][q_heads][prompt_len][head_dim]  (dtype of cache)
  *   k_prompt [dev] [layers][kv_heads][prompt_len][head_dim]
- * mode EPK_SCORE_EXACT_F32 needs dtype F32; EPK_SCORE_TC_BF16 needs dtype BF16
- * and head_dim 128.  n_max_per_head [host] bounds every head's live count
+ * mode EPK_SCORE_EXACT_F32 needs dtype F32; EPK_SCORE_TC_BF16 needs dtype BF16,
+ * head_dim 128, prompt_len <= 256 and (q_heads/kv_heads)*prompt_len <= 2048
+ * (longer prompts, e.g. KVzip's block repetition: epk_score_grids).  n_max_per_head [host] bounds every head's live count
  * (grid sizing only).  Asynchronous. */
 int epk_score(epk_ctx* ctx, const epk_cache_desc* cache, const void* q_prompt,
               const void* k_prompt, int32_t q_heads, int32_t prompt_len, int32_t aggregation,

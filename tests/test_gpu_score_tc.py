@@ -47,6 +47,7 @@ def _inputs(rng, L, Hq, H, p, counts):
     (1, 4, 4, 1, [0, 129, 5, 256]),   # p = 1, empty head, partial tiles
     (1, 12, 2, 200, [700, 333]),      # two prompt tiles, G*p = 1200 (streamed Q)
     (1, 28, 4, 128, [2100, 1900, 17, 4096]),  # Qwen GQA (G = 7, NQ = 7)
+    (1, 16, 2, 256, [600, 450]),      # the kernel's prompt limits: p = 256, G*p = 2048 (NQ = 16, streamed)
 ])
 def test_tc_scores_vs_fp64_oracle(gpu, orc, cfg, agg):
     L, Hq, H, p, counts = cfg
