@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(192, 1) mma_rate_kernel(int iters, int drain, 
     uint8_t* sA = smem;                  // 128 x 128 bf16 (two swizzled halves)
     uint8_t* sB = smem + 32768;          // N x 128
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + N * 256);
-    uint64_t* empty = full + 4;
-    uint32_t* holder = reinterpret_cast<uint32_t*>(empty + 4);
+    uint64_t* empty = full + 8;
+    uint32_t* holder = reinterpret_cast<uint32_t*>(empty + 8);
     constexpr int kSlots = 512 / N;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < (32768 + N * 256) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
@@ -158,16 +158,23 @@ __global__ void __launch_bounds__(192, 1) mma_rate_kernel(int iters, int drain, 
 }
 
 int launch_mma_rate(epk_ctx* ctx, int n, int iters, int drain) {
-    const int smem = 1024 + 32768 + n * 256 + 128;
+    const int smem = 1024 + 32768 + n * 256 + 256;
     unsigned* sink = reinterpret_cast<unsigned*>(ctx->err_flag);
-    EPK_PROF(ctx, n == 256 ? "mma_rate_n256" : "mma_rate_n128");
-    if (n == 256) {
-        EPK_CUDA_CHECK(cudaFuncSetAttribute(mma_rate_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        mma_rate_kernel<256><<<ctx->num_sms, 192, smem, ctx->stream>>>(iters, drain, sink);
-    } else {
-        EPK_CUDA_CHECK(cudaFuncSetAttribute(mma_rate_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        mma_rate_kernel<128><<<ctx->num_sms, 192, smem, ctx->stream>>>(iters, drain, sink);
+    EPK_PROF(ctx, "mma_rate");
+    auto run = [&](auto kern) -> int {
+        EPK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        kern<<<ctx->num_sms, 192, smem, ctx->stream>>>(iters, drain, sink);
+        return EPK_OK;
+    };
+    int rc;
+    switch (n) {
+        case 64: rc = run(mma_rate_kernel<64>); break;
+        case 128: rc = run(mma_rate_kernel<128>); break;
+        case 192: rc = run(mma_rate_kernel<192>); break;
+        case 256: rc = run(mma_rate_kernel<256>); break;
+        default: return fail(EPK_ERR_ARG, "mma_rate: n must be 64, 128, 192 or 256");
     }
+    if (rc) return rc;
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }
