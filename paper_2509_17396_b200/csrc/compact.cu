@@ -224,15 +224,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_gather_kernel(const
                 for (int u = 0; u < 4; ++u) {
                     if (ok[u]) {
                         const int64_t src = (in_base + rs + k0 + 2 * u + hl) * rv + c;
-                        kv[u] = __ldcs(P.in_k + src);
-                        vv[u] = __ldcs(P.in_v + src);
+                        kv[u] = __ldg(P.in_k + src);
+                        vv[u] = __ldg(P.in_v + src);
                     }
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     if (ok[u]) {
-                        __stcs(P.out_k + dsts[u] * rv + c, kv[u]);
-                        __stcs(P.out_v + dsts[u] * rv + c, vv[u]);
+                        P.out_k[dsts[u] * rv + c] = kv[u];
+                        P.out_v[dsts[u] * rv + c] = vv[u];
                     }
                 }
             }

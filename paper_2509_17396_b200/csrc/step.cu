@@ -994,8 +994,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
                                 const int srcl = E.gsrc[ew][i & 1][rank];
                                 dd[v] = E.gdst[ew][i & 1][rank];
                                 const int64_t src = (base + r_beg + g * 32 + srcl) * 16 + cl;
-                                kk[v] = __ldcs(P.in_k + src);
-                                vv2[v] = __ldcs(P.in_v + src);
+                                kk[v] = __ldg(P.in_k + src);
+                                vv2[v] = __ldg(P.in_v + src);
                             }
                         }
                     };
@@ -1005,8 +1005,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
 #pragma unroll
                         for (int v = 0; v < 8; ++v) {
                             if (dd[v] >= 0) {
-                                __stcs(ok + int64_t(dd[v]) * 16, kk[v]);
-                                __stcs(ov + int64_t(dd[v]) * 16, vv2[v]);
+                                ok[int64_t(dd[v]) * 16] = kk[v];
+                                ov[int64_t(dd[v]) * 16] = vv2[v];
                             }
                         }
                     };
