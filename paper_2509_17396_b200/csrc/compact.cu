@@ -89,12 +89,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_count_kernel(const 
         const bool all = (t0 >> 32) != 0;
         const uint32_t T = uint32_t(t0);
         uint8_t* kp = P.keep_out + base;
+        // the chunk's first head (warp-uniform) and where the next starts: the
+        // per-row binary search only past a head boundary
+        const int h0 = head_of_row(off, P.H, r0);
+        const int64_t h0_end = off[h0 + 1];
 #pragma unroll
         for (int i = 0; i < kChunkRows / 32; ++i) {
             const int64_t r = r0 + i * 32 + lane;
             uint8_t k = 0;
             if (r < rows) {
-                const int h = head_of_row(off, P.H, r);
+                const int h = r < h0_end ? h0 : head_of_row(off, P.H, r);
                 if (r - off[h] < P.in_len[layer * P.H + h]) {
                     const uint32_t key = __ldcg(P.keys + base + r);
                     k = (all || key < T ||
