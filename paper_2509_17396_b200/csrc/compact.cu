@@ -10,10 +10,10 @@
 // Three launches per call, all free of shared memory so their small CTAs can
 // co-reside on an SM with a scorer CTA of the next layer group (the step
 // overlaps HBM-bound compaction with tensor/SFU-bound scoring):
-//   count   one warp per 256-row chunk: kept rows in the chunk;
+//   count   one warp per 128-row chunk: kept rows in the chunk;
 //   plan    one CTA per layer: exclusive scan of the chunk counts and the kept
 //           count in front of every head region -> output head_off/head_len;
-//   gather  one warp per 256-row chunk: ballot prefix per 32 rows, then
+//   gather  one warp per 128-row chunk: ballot prefix per 32 rows, then
 //           16-byte vector copies of K and V (8 in flight per lane) and the
 //           positions.
 // keep[] must be 0 on gap rows (both select modes guarantee it).
@@ -23,7 +23,7 @@
 
 namespace epk {
 
-constexpr int kChunkRows = 256;   // rows per warp chunk
+constexpr int kChunkRows = 128;   // rows per warp chunk
 constexpr int kWarpsPerCta = 4;
 
 struct CompactParams {
