@@ -153,18 +153,22 @@ __global__ void __launch_bounds__(256) compact_plan_kernel(const __grid_constant
     }
     __syncthreads();
     const uint8_t* kp = P.keep + P.in_lt.base[layer];
-    for (int h = threadIdx.x; h <= H; h += blockDim.x) {
+    // kept rows before every head start: the chunk prefix plus a warp-wide
+    // count of the kept rows in [chunk start, head start)
+    for (int h = warp; h <= H; h += blockDim.x / 32) {
         const int64_t x = off[h];
         const int64_t c = x / kChunkRows;
         int64_t v;
         if (c >= nchunks) {
-            v = int64_t(pre[nchunks - 1]) + cnt[nchunks - 1];
-            if (nchunks == 0) v = 0;
+            v = nchunks == 0 ? 0 : int64_t(pre[nchunks - 1]) + cnt[nchunks - 1];
         } else {
-            v = pre[c];
-            for (int64_t r = c * kChunkRows; r < x; ++r) v += kp[r] ? 1 : 0;
+            int part = 0;
+            for (int64_t r = c * kChunkRows + lane; r < x; r += 32) part += kp[r] ? 1 : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            v = int64_t(pre[c]) + part;
         }
-        s_head_prefix[h] = v;
+        if (lane == 0) s_head_prefix[h] = v;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
