@@ -66,6 +66,7 @@ __device__ __forceinline__ int head_of_row(const int32_t* off, int H, int64_t r)
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_count_kernel(const __grid_constant__ CompactParams P) {
+    pdl_wait();
     const int layer = blockIdx.y;
     if (P.hist_fine) {  // threshold mode: this CTA's share of the layer's histogram reset
         const int per = (65536 / 4 + gridDim.x - 1) / gridDim.x;
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_count_kernel(const 
 // One CTA per layer: exclusive scan of the chunk counts, then the kept count
 // in front of every head-region start -> output head offsets and lengths.
 __global__ void __launch_bounds__(256) compact_plan_kernel(const __grid_constant__ CompactParams P) {
+    pdl_wait();
     const int layer = blockIdx.x;
     const int H = P.H;
     __shared__ int32_t s_warp[8];
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(256) compact_plan_kernel(const __grid_constant
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_gather_kernel(const __grid_constant__ CompactParams P) {
+    pdl_wait();
     const int layer = blockIdx.y;
     const int chunk = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -293,13 +296,13 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     P.chunk_prefix = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
     dim3 grid((P.max_chunks + kWarpsPerCta - 1) / kWarpsPerCta, in->layers);
     EPK_PROF(ctx, "compact_count");
-    compact_count_kernel<<<grid, 32 * kWarpsPerCta, 0, ctx->stream>>>(P);
+    EPK_CUDA_CHECK(launch_pdl(compact_count_kernel, grid, dim3(32 * kWarpsPerCta), 0, ctx->stream, P));
     EPK_LAUNCH_CHECK(ctx);
     EPK_PROF(ctx, "compact_plan");
-    compact_plan_kernel<<<in->layers, 256, 0, ctx->stream>>>(P);
+    EPK_CUDA_CHECK(launch_pdl(compact_plan_kernel, dim3(in->layers), dim3(256), 0, ctx->stream, P));
     EPK_LAUNCH_CHECK(ctx);
     EPK_PROF(ctx, "compact_gather");
-    compact_gather_kernel<<<grid, 32 * kWarpsPerCta, 0, ctx->stream>>>(P);
+    EPK_CUDA_CHECK(launch_pdl(compact_gather_kernel, grid, dim3(32 * kWarpsPerCta), 0, ctx->stream, P));
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }

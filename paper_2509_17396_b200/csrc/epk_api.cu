@@ -144,6 +144,11 @@ int launch_keydiff(epk_ctx*, const epk_cache_desc*, double*);
 int launch_serialize_epkv(epk_ctx*, const epk_cache_desc*, uint64_t, const char*, uint64_t, const int64_t*, int32_t,
                           uint8_t*, int64_t, int64_t*, int64_t*);
 
+bool pdl_enabled() {
+    static const bool on = std::getenv("EPK_NO_PDL") == nullptr;
+    return on;
+}
+
 static int check_ctx(epk_ctx* ctx) {
     if (!ctx) return fail(EPK_ERR_ARG, "null context");
     int dev = -1;

@@ -298,6 +298,7 @@ __global__ void __maxnreg__(128)
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte aligned (SWIZZLE_128B atoms), derived from smem_raw by pointer
     // arithmetic so the compiler keeps shared-space (LDS/STS) addressing.
+    pdl_wait();  // every input may come from the previous kernel in the stream
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t q_half = uint32_t(P.qcap) * kRowB;   // Q d-half stride
     const uint32_t k_half = uint32_t(P.krows) * kRowB;  // K d-half stride
@@ -848,7 +849,8 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
 
 static int tc_launch_p1(epk_ctx* ctx, const TcPlan& T) {
     EPK_PROF(ctx, "p1_rowstats");
-    T.stats_fn<<<ctx->num_sms, kThreadsStats, T.smem1, ctx->stream>>>(T.P1, T.tm_k, T.tm_q, T.tm_kp);
+    EPK_CUDA_CHECK(launch_pdl(T.stats_fn, dim3(ctx->num_sms), dim3(kThreadsStats), T.smem1, ctx->stream, T.P1, T.tm_k,
+                              T.tm_q, T.tm_kp));
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }
@@ -876,7 +878,8 @@ static int tc_launch_p2(epk_ctx* ctx, const TcPlan& T, int l0, int l1) {
             return rc;
     }
     EPK_PROF(ctx, "p2_colscore");
-    T.score_fn<<<ctx->num_sms, kThreads, T.smem2, ctx->stream>>>(P, T.tm_k, tm_q, T.tm_kp);
+    EPK_CUDA_CHECK(launch_pdl(T.score_fn, dim3(ctx->num_sms), dim3(kThreads), T.smem2, ctx->stream, P, T.tm_k, tm_q,
+                              T.tm_kp));
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }

@@ -616,6 +616,7 @@ __device__ void ts_find_bucket(TSShared& S, const uint32_t* tot, int nbins, int6
 }
 
 __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __grid_constant__ ThreshParams P) {
+    pdl_wait();
     __shared__ TSShared S;
     const int l = blockIdx.y, part = blockIdx.x;
     const int H = P.H;
@@ -798,7 +799,7 @@ int launch_select_threshold(epk_ctx* ctx, const epk_cache_desc* c, const FusedSe
     P.parts = int(std::max<int64_t>(1, std::min<int64_t>(64, (max_region + 4095) / 4096)));
     P.err_flag = ctx->err_flag;
     EPK_PROF(ctx, "select");
-    select_threshold_kernel<<<dim3(P.parts, c->layers), kTSThreads, 0, ctx->stream>>>(P);
+    EPK_CUDA_CHECK(launch_pdl(select_threshold_kernel, dim3(P.parts, c->layers), dim3(kTSThreads), 0, ctx->stream, P));
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }
