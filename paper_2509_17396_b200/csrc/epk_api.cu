@@ -234,6 +234,11 @@ int epk_ctx_destroy(epk_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
     prof_clear(ctx);
+    if (ctx->hi) {
+        cudaStreamSynchronize(ctx->hi);
+        cudaStreamDestroy(ctx->hi);
+        cudaEventDestroy(ctx->ev_hi);
+    }
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
@@ -489,9 +494,15 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     const bool overlap = ctx->overlap && G < L;
     if (overlap && !ctx->side) {
         if (capturing) return fail(EPK_ERR_ARG, "run one step before capturing a graph");
-        EPK_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        // compaction at the lowest priority, the scoring / select chain at the
+        // highest: when SM slots free up, the latency-critical select CTAs go first
+        int least = 0, greatest = 0;
+        EPK_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        EPK_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, least));
+        EPK_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, greatest));
         EPK_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
         EPK_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+        EPK_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_hi, cudaEventDisableTiming));
     }
     const int64_t qlayer = int64_t(q_heads) * prompt_len * in->head_dim * dtype_size(in->dtype);
     const int64_t klayer = int64_t(in->kv_heads) * prompt_len * in->head_dim * dtype_size(in->dtype);
@@ -505,13 +516,25 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
         if (aggregation != EPK_AGG_MAX && aggregation != EPK_AGG_AVG) return fail(EPK_ERR_ARG, "bad aggregation");
         unsigned* cnt = reinterpret_cast<unsigned*>(sb + o_cnt);
         const FusedSelect fs_all{keys, hist_f, hist_c, reinterpret_cast<uint4*>(sb + o_cand), cnt, cnt + kMaxLayers};
+        static const bool no_hi = std::getenv("EPK_NO_HI_STREAM") != nullptr;  // A/B
+        const bool use_hi = overlap && !no_hi;
+        if (use_hi) {  // fork the user's stream onto the high-priority one
+            EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_hi, main));
+            EPK_CUDA_CHECK(cudaStreamWaitEvent(ctx->hi, ctx->ev_hi, 0));
+            ctx->stream = ctx->hi;
+        }
         rc = launch_step_tc_grouped(ctx, in, out, q, kp, q_heads, prompt_len, aggregation == EPK_AGG_MAX, budgets, G,
                                     overlap ? ctx->side : nullptr, ctx->ev_fork, out_slack, scores, keep, fs_all, thr,
                                     kept, launch_select_threshold, launch_compact, layer_view);
+        ctx->stream = main;
         if (rc) return rc;
         if (overlap) {
             EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->side));
             EPK_CUDA_CHECK(cudaStreamWaitEvent(main, ctx->ev_join, 0));
+        }
+        if (use_hi) {
+            EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_hi, ctx->hi));
+            EPK_CUDA_CHECK(cudaStreamWaitEvent(main, ctx->ev_hi, 0));
         }
         return EPK_OK;
     }

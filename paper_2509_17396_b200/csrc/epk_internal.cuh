@@ -27,6 +27,8 @@ struct epk_ctx {
     void* ws2 = nullptr;  // grow-only workspace (compaction; may run on `side`)
     int64_t ws2_bytes = 0;
     cudaStream_t side = nullptr;  // second stream: compaction overlaps the next layer group's scoring
+    cudaStream_t hi = nullptr;    // overlap mode: scoring + select at the highest stream priority
+    cudaEvent_t ev_hi = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int layer_group = 0;  // layers per group in epk_evict_step (0 = auto: group K fits in L2)
     int overlap = 1;      // run each group's compaction on `side`
