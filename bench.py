@@ -474,7 +474,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--layer-group", type=int, default=0, help="layers per step group (0 = auto, L2-sized)")
+    ap.add_argument("--layer-group", type=int, default=0, help="layers per P2/select/compaction group (0 = all layers)")
     ap.add_argument("--no-overlap", action="store_true", help="compaction on the main stream")
     ap.add_argument("--fused", action="store_true", help="single-kernel fused step (EPK_OPT_FUSED, experimental)")
     ap.add_argument("--layers", type=int, default=0, help=argparse.SUPPRESS)  # experiments: override L
