@@ -261,6 +261,8 @@ int epk_debug_tma_stream(epk_ctx* ctx, const void* k, int64_t rows, int32_t box_
  * or 256) from resident shared memory; drain != 0 adds epilogue warps that
  * tcgen05.ld every result before its TMEM slot is reused. */
 int epk_debug_mma_rate(epk_ctx* ctx, int32_t n, int32_t iters, int32_t drain);
+/* Two-SM (cta_group::2, M = 256) MMA issue ceiling, n = 128 or 256 (probe). */
+int epk_debug_mma2sm_rate(epk_ctx* ctx, int32_t n, int32_t iters);
 /* P1 pipeline without the softmax: TMA-streamed 256-row K stages x nq
  * resident 128-row chunks, 128 x 256 x 128 MMAs, optional TMEM drain. */
 int epk_debug_mma_stream(epk_ctx* ctx, const void* k, int64_t rows, int32_t nq, int32_t stages, int32_t drain);

@@ -75,6 +75,7 @@ _SIGS = {
     "epk_debug_expf": (C.c_int, [vp, vp, vp, i64]),
     "epk_debug_tma_stream": (C.c_int, [vp, vp, i64, i32, i32, i32]),
     "epk_debug_mma_rate": (C.c_int, [vp, i32, i32, i32]),
+    "epk_debug_mma2sm_rate": (C.c_int, [vp, i32, i32]),
     "epk_debug_mma_stream": (C.c_int, [vp, vp, i64, i32, i32, i32]),
 }
 

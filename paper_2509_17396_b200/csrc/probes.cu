@@ -179,6 +179,111 @@ int launch_mma_rate(epk_ctx* ctx, int n, int iters, int drain) {
     return EPK_OK;
 }
 
+// Two-SM variant: tcgen05.mma.cta_group::2 (M = 256: each CTA of the pair
+// supplies its 128 A rows and N/2 B rows from its own shared memory at the
+// same offsets; D lands in both CTAs' TMEM, 128 lanes x N each).  The leader
+// CTA issues; commits multicast to both CTAs' barriers.  Measures whether
+// the pair runs N = 128 / 256 jobs at the tensor pipe's rate (the one-SM
+// N = 128 jobs reach 69 %, see mma_rate_kernel).
+template <int N>
+__global__ void __launch_bounds__(64, 1) mma2sm_rate_kernel(int iters, unsigned* sink) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;          // 128 x 128 bf16 (this CTA's half of A)
+    uint8_t* sB = smem + 32768;  // N/2 x 128 (this CTA's half of B)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + (N / 2) * 256);
+    uint32_t* holder = reinterpret_cast<uint32_t*>(full + 8);
+    constexpr int kSlots = 512 / N;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    for (int i = threadIdx.x; i < (32768 + (N / 2) * 256) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSlots; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(holder))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+    const uint32_t tmem = *holder;
+    constexpr uint32_t idesc = idesc_bf16_f32(256, N);
+    if (rank == 0 && warp == 0 && lane == 0) {
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+        for (int it = 0; it < iters; ++it) {
+            const int s = it % kSlots;
+            if (it >= kSlots) mbar_wait(&full[s], ((it / kSlots) & 1) ^ 1);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t aoff = uint32_t((kk >> 2) * 16384 + (kk & 3) * 32);
+                const uint32_t boff = uint32_t((kk >> 2) * ((N / 2) * 128) + (kk & 3) * 32);
+                const uint64_t ad = sdesc_k_sw128(a0 + aoff), bd = sdesc_k_sw128(b0 + boff);
+                const uint32_t acc = kk > 0 ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + uint32_t(s * N)),
+                    "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+                    : "memory");
+            }
+            asm volatile(
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                    smem_u32(&full[s])),
+                "h"(uint16_t(3))
+                : "memory");
+        }
+        // drain: the last commit of every slot
+        for (int it = iters; it < iters + kSlots; ++it) {
+            const int s = it % kSlots;
+            if (it >= kSlots) mbar_wait(&full[s], ((it / kSlots) & 1) ^ 1);
+        }
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if (threadIdx.x == 0 && iters < 0) *sink = tmem;
+}
+
+int launch_mma2sm_rate(epk_ctx* ctx, int n, int iters) {
+    const int smem = 1024 + 32768 + (n / 2) * 256 + 256;
+    unsigned* sink = reinterpret_cast<unsigned*>(ctx->err_flag);
+    auto run = [&](auto kern) -> int {
+        EPK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ctx->num_sms & ~1);
+        cfg.blockDim = dim3(64);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        EPK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, iters, sink));
+        return EPK_OK;
+    };
+    EPK_PROF(ctx, "mma2sm_rate");
+    int rc;
+    switch (n) {
+        case 128: rc = run(mma2sm_rate_kernel<128>); break;
+        case 256: rc = run(mma2sm_rate_kernel<256>); break;
+        default: return fail(EPK_ERR_ARG, "mma2sm_rate: n must be 128 or 256");
+    }
+    if (rc) return rc;
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
 // TMA-streamed 256-row K stages (`stages`-deep ring) feeding `nq` resident
 // 128-row A chunks: per stage nq MMAs of 128 x 256 x 128 into two TMEM slots,
 // drained by 8 epilogue warps (tcgen05.ld, no math).  The P1 pipeline
@@ -319,6 +424,10 @@ extern "C" int epk_debug_mma_stream(epk_ctx* ctx, const void* k, int64_t rows, i
 
 extern "C" int epk_debug_mma_rate(epk_ctx* ctx, int32_t n, int32_t iters, int32_t drain) {
     return epk::launch_mma_rate(ctx, n, iters, drain);
+}
+
+extern "C" int epk_debug_mma2sm_rate(epk_ctx* ctx, int32_t n, int32_t iters) {
+    return epk::launch_mma2sm_rate(ctx, n, iters);
 }
 
 extern "C" int epk_debug_tma_stream(epk_ctx* ctx, const void* base, int64_t rows, int32_t box_rows, int32_t stages,
