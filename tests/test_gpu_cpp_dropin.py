@@ -18,3 +18,15 @@ def test_cpp_dropin_matches_reference(gpu):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "0 failed" in r.stdout
+
+
+C_BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_build", "abi_c_step")
+
+
+def test_plain_c_abi_step(gpu):
+    """include/epk/epk.h from plain C (gcc, no C++ / torch): one bf16 block step."""
+    assert os.path.exists(C_BIN), "tests/cpp/_build/abi_c_step not built (tests/cpp/Makefile)"
+    r = subprocess.run([C_BIN], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "abi_c_step ok" in r.stdout
