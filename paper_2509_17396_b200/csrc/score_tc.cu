@@ -306,8 +306,8 @@ __global__ void __maxnreg__(128)
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + 2 * q_half;
     float* s_lse = reinterpret_cast<float*>(sK + P.kstages * k_stage);  // SCORE: NQ*128 lse2
-    float* s_pair = s_lse + (MODE == MODE_SCORE ? P.NQ * kChunk : 0);  // SCORE: 128 half maxima
-    float* s_avg = s_pair + (MODE == MODE_SCORE ? kChunk : 0);         // SCORE avg: G*128 sums
+    float* s_pair = s_lse + (MODE == MODE_SCORE ? P.NQ * kChunk : 0);  // SCORE: [2][128] half maxima
+    float* s_avg = s_pair + (MODE == MODE_SCORE ? 2 * kChunk : 0);     // SCORE avg: G*128 sums
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_avg + (MODE == MODE_SCORE && !P.agg_max ? P.G * kChunk : 0));
     uint64_t* k_full = bars;
     uint64_t* k_empty = k_full + P.kstages;
@@ -512,6 +512,7 @@ __global__ void __maxnreg__(128)
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
         const int etid = e * 32 + lane;
         uint32_t job = 0;
+        uint32_t tcount = 0;  // SCORE: tiles done (emitting half, partial buffer)
         int lkey = -1;
         const float inv_p = 1.0f / float(P.p);
         const int64_t T1 = MODE == MODE_SCORE ? int64_t(P.p1_pre[P.p1_runs]) : 0;
@@ -646,11 +647,17 @@ __global__ void __maxnreg__(128)
                     // combine the two column halves of each cache row
                     const int jrow = (x.t0 + t) * P.krows + r_local;
                     if (P.agg_max) {
-                        if (half == 1) s_pair[r_local] = best;
+                        // the halves take turns emitting (tile parity) and the
+                        // partials are double-buffered, so one barrier per tile
+                        // suffices: buffer b is rewritten two tiles later, past
+                        // a barrier the reading half reaches only after its read
+                        const int em = int(tcount & 1);
+                        float* sp = s_pair + em * kChunk;
+                        if (half != em) sp[r_local] = best;
                         named_bar_sync(2 + quarter, 64);
-                        if (half == 0 && jrow < x.n_h)
-                            emit_score(P, x.l, x.krow0 + jrow, ex2(fmaxf(best, s_pair[r_local])), s_coarse);
-                        named_bar_sync(2 + quarter, 64);
+                        if (half == em && jrow < x.n_h)
+                            emit_score(P, x.l, x.krow0 + jrow, ex2(fmaxf(best, sp[r_local])), s_coarse);
+                        ++tcount;
                     } else {
                         named_bar_sync(2 + quarter, 64);
                         if (half == 0) {
@@ -690,7 +697,7 @@ __global__ void __maxnreg__(128)
 // ---------------------------------------------------------------------------
 static int smem_bytes(const TcParams& P, int mode) {
     return 1024 + 2 * P.qcap * kRowB + P.kstages * 2 * P.krows * kRowB +
-           (mode == MODE_SCORE ? (P.NQ + 1 + (P.agg_max ? 0 : P.G)) * kChunk * 4 : 0) +
+           (mode == MODE_SCORE ? (P.NQ + 2 + (P.agg_max ? 0 : P.G)) * kChunk * 4 : 0) +
            (2 * P.kstages + 2 * kMaxQRes + 8) * 8 + 16 + (P.runs + 1) * 4;
 }
 
