@@ -9,10 +9,10 @@
 // bits.  The k-means++ seeding and the empty-cluster
 // repair consume the reference RNG stream and stay on the host (epk_api.cu).
 //
-// K5 restates the reduction of measure_sensitivity (allocation.hpp:80-100):
+// K5 restates the reduction of measure_sensitivity (allocation.hpp:80-100), bit-exact:
 // sigma_l = mean over (h, t) of clamp(cos(k_full, k_block)), zero-norm pairs
-// skipped.  HBM-bound; one warp per key row, fixed-order block partials then
-// a fixed-order per-layer reduction (deterministic, fp64).
+// skipped: per-pair cosines in the reference's operation order, then each
+// layer's (h, t)-ordered running sum (see cosine_pair_kernel / cosine_mean_kernel).
 #include <algorithm>
 
 #include "epk_internal.cuh"
@@ -158,105 +158,96 @@ __device__ __forceinline__ double to_d<double>(double x) { return x; }
 template <>
 __device__ __forceinline__ double to_d<__nv_bfloat16>(__nv_bfloat16 x) { return double(__bfloat162float(x)); }
 
-constexpr int kCosThreads = 256;
-constexpr int kCosRowsPerBlock = 64;
-
-// partial[layer][blk] = (sum of cosines, counted, skipped) over a block of rows.
+// K5, bit-exact with the reference's loop order (allocation.hpp:80-100 with
+// cosine / l2_norm / dot of numerics.hpp:52-87, -ffp-contract=off):
+//   pair  one thread per (layer, h, t): |a|^2, |b|^2 and a.b as sequential
+//         chains over the dimensions (explicit __dmul_rn / __dadd_rn, no FMA),
+//         correctly rounded sqrt and division, clamp to [-1, 1]; a zero-norm
+//         pair is stored as NaN (skipped).
+//   mean  one thread per layer: the (h, t)-ordered running sum of the pair
+//         cosines -- the reference's sequential accumulation -- with a
+//         64-deep rotating register prefetch so the dependent fp64 adds, not
+//         the loads, set the pace; sigma = sum / counted (1 when none count).
 template <typename T>
-__global__ void __launch_bounds__(kCosThreads) cosine_partial_kernel(const T* __restrict__ kf, const T* __restrict__ kb,
-                                                                     int64_t rows_per_layer, int dim,
-                                                                     int blocks_per_layer, double* psum,
-                                                                     int64_t* pcnt, int64_t* pskip) {
-    const int layer = blockIdx.y;
-    const int blk = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ double s_cos[kCosRowsPerBlock];
-    __shared__ int s_ok[kCosRowsPerBlock];
-    const int64_t row0 = int64_t(blk) * kCosRowsPerBlock;
-    for (int rr = warp; rr < kCosRowsPerBlock; rr += kCosThreads / 32) {
-        const int64_t row = row0 + rr;
-        double na = 0.0, nb = 0.0, dot = 0.0;
-        if (row < rows_per_layer) {
-            const T* a = kf + (int64_t(layer) * rows_per_layer + row) * dim;
-            const T* b = kb + (int64_t(layer) * rows_per_layer + row) * dim;
-            for (int i = lane; i < dim; i += 32) {
-                const double x = to_d(a[i]), y = to_d(b[i]);
-                na += x * x;
-                nb += y * y;
-                dot += x * y;
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            na += __shfl_xor_sync(0xffffffffu, na, o);
-            nb += __shfl_xor_sync(0xffffffffu, nb, o);
-            dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        }
-        if (lane == 0) {
-            if (row >= rows_per_layer) {
-                s_ok[rr] = -1;
-                s_cos[rr] = 0.0;
-            } else {
-                const double sa = sqrt(na), sb = sqrt(nb);
-                if (sa == 0.0 || sb == 0.0) {
-                    s_ok[rr] = 0;
-                    s_cos[rr] = 0.0;
-                } else {
-                    s_ok[rr] = 1;
-                    s_cos[rr] = fmin(1.0, fmax(-1.0, dot / (sa * sb)));
-                }
-            }
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        int64_t c = 0, sk = 0;
-        for (int i = 0; i < kCosRowsPerBlock; ++i) {
-            if (s_ok[i] == 1) {
-                s += s_cos[i];
-                ++c;
-            } else if (s_ok[i] == 0) {
-                ++sk;
-            }
-        }
-        const int64_t o = int64_t(layer) * blocks_per_layer + blk;
-        psum[o] = s;
-        pcnt[o] = c;
-        pskip[o] = sk;
-    }
+__device__ __forceinline__ void cos_vec(const T* p, int j, double (&x)[16 / sizeof(T)]) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(p) + j);
+    const T* e = reinterpret_cast<const T*>(&w);
+#pragma unroll
+    for (int u = 0; u < int(16 / sizeof(T)); ++u) x[u] = to_d(e[u]);
 }
 
-// One CTA per layer: fixed-order strided partial sums, then a fixed smem tree
-// (deterministic run to run).  Skipped counts land in skipped_per_layer.
-__global__ void __launch_bounds__(256) cosine_final_kernel(const double* psum, const int64_t* pcnt,
-                                                           const int64_t* pskip, int blocks_per_layer,
-                                                           double* sigma, int64_t* skipped_per_layer) {
-    const int l = blockIdx.x;
-    __shared__ double s_s[256];
-    __shared__ long long s_c[256], s_k[256];
-    double s = 0.0;
-    long long c = 0, sk = 0;
-    for (int b = threadIdx.x; b < blocks_per_layer; b += 256) {
-        s += psum[int64_t(l) * blocks_per_layer + b];
-        c += pcnt[int64_t(l) * blocks_per_layer + b];
-        sk += pskip[int64_t(l) * blocks_per_layer + b];
-    }
-    s_s[threadIdx.x] = s;
-    s_c[threadIdx.x] = c;
-    s_k[threadIdx.x] = sk;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) {
-            s_s[threadIdx.x] += s_s[threadIdx.x + w];
-            s_c[threadIdx.x] += s_c[threadIdx.x + w];
-            s_k[threadIdx.x] += s_k[threadIdx.x + w];
+template <typename T>
+__global__ void __launch_bounds__(256) cosine_pair_kernel(const T* __restrict__ kf, const T* __restrict__ kb,
+                                                          int64_t rows_per_layer, int dim, double* cosv) {
+    const int layer = blockIdx.y;
+    const int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (row >= rows_per_layer) return;
+    const int64_t g = int64_t(layer) * rows_per_layer + row;
+    const T* a = kf + g * dim;
+    const T* b = kb + g * dim;
+    double na = 0.0, nb = 0.0, dot = 0.0;
+    constexpr int V = 16 / sizeof(T);
+    if ((dim * int(sizeof(T))) % 16 == 0) {
+        for (int j = 0; j < dim / V; ++j) {
+            double x[V], y[V];
+            cos_vec<T>(a, j, x);
+            cos_vec<T>(b, j, y);
+#pragma unroll
+            for (int u = 0; u < V; ++u) {
+                na = __dadd_rn(na, __dmul_rn(x[u], x[u]));
+                nb = __dadd_rn(nb, __dmul_rn(y[u], y[u]));
+                dot = __dadd_rn(dot, __dmul_rn(x[u], y[u]));
+            }
         }
-        __syncthreads();
+    } else {
+        for (int i = 0; i < dim; ++i) {
+            const double x = to_d(a[i]), y = to_d(b[i]);
+            na = __dadd_rn(na, __dmul_rn(x, x));
+            nb = __dadd_rn(nb, __dmul_rn(y, y));
+            dot = __dadd_rn(dot, __dmul_rn(x, y));
+        }
     }
-    if (threadIdx.x == 0) {
-        sigma[l] = s_c[0] > 0 ? s_s[0] / double(s_c[0]) : 1.0;
-        skipped_per_layer[l] = s_k[0];
+    na = __dsqrt_rn(na);
+    nb = __dsqrt_rn(nb);
+    double c;
+    if (na == 0.0 || nb == 0.0) {
+        c = __longlong_as_double(0x7ff8000000000000ll);  // skipped (zero norm)
+    } else {
+        c = __ddiv_rn(dot, __dmul_rn(na, nb));
+        c = c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
     }
+    cosv[g] = c;
+}
+
+__global__ void __launch_bounds__(32) cosine_mean_kernel(const double* __restrict__ cosv, int64_t rows,
+                                                         double* sigma, int64_t* skipped_per_layer) {
+    if (threadIdx.x != 0) return;
+    const int l = blockIdx.x;
+    const double* v = cosv + int64_t(l) * rows;
+    constexpr int D = 64;
+    double buf[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) buf[j] = j < rows ? __ldcg(v + j) : 0.0;
+    double acc = 0.0;
+    long long cnt = 0, sk = 0;
+    for (int64_t b0 = 0; b0 < rows; b0 += D) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const int64_t i = b0 + j;
+            if (i < rows) {
+                const double x = buf[j];
+                if (x == x) {
+                    acc = __dadd_rn(acc, x);
+                    ++cnt;
+                } else {
+                    ++sk;
+                }
+            }
+            buf[j] = i + D < rows ? __ldcg(v + i + D) : 0.0;
+        }
+    }
+    sigma[l] = cnt > 0 ? __ddiv_rn(acc, double(cnt)) : 1.0;
+    skipped_per_layer[l] = sk;
 }
 
 __global__ void cosine_skip_total_kernel(const int64_t* per_layer, int layers, int64_t* skipped) {
@@ -270,30 +261,25 @@ __global__ void cosine_skip_total_kernel(const int64_t* per_layer, int layers, i
 int launch_key_cosine(epk_ctx* ctx, const void* kf, const void* kb, int dtype, int layers, int H, int64_t ntok,
                       int dim, double* sigma, int64_t* skipped) {
     const int64_t rows = int64_t(H) * ntok;
-    const int bpl = int((rows + kCosRowsPerBlock - 1) / kCosRowsPerBlock);
-    const int64_t np = int64_t(layers) * bpl;
-    int rc = ws_require(ctx, np * 24 + int64_t(layers) * 8 + 2048);
+    int rc = ws_require(ctx, int64_t(layers) * rows * 8 + int64_t(layers) * 8 + 1024);
     if (rc) return rc;
     WsCarver carve(ctx->ws);
-    double* psum = carve.take<double>(np);
-    int64_t* pcnt = carve.take<int64_t>(np);
-    int64_t* pskip = carve.take<int64_t>(np);
+    double* cosv = carve.take<double>(int64_t(layers) * rows);
     int64_t* skl = carve.take<int64_t>(layers);
-    dim3 g(bpl, layers);
-    EPK_PROF(ctx, "cosine_partial");
+    const dim3 g(unsigned((rows + 255) / 256), layers);
+    EPK_PROF(ctx, "cosine_pair");
     if (dtype == EPK_F64)
-        cosine_partial_kernel<double><<<g, kCosThreads, 0, ctx->stream>>>(
-            static_cast<const double*>(kf), static_cast<const double*>(kb), rows, dim, bpl, psum, pcnt, pskip);
+        cosine_pair_kernel<double><<<g, 256, 0, ctx->stream>>>(static_cast<const double*>(kf),
+                                                               static_cast<const double*>(kb), rows, dim, cosv);
     else if (dtype == EPK_F32)
-        cosine_partial_kernel<float><<<g, kCosThreads, 0, ctx->stream>>>(
-            static_cast<const float*>(kf), static_cast<const float*>(kb), rows, dim, bpl, psum, pcnt, pskip);
+        cosine_pair_kernel<float><<<g, 256, 0, ctx->stream>>>(static_cast<const float*>(kf),
+                                                              static_cast<const float*>(kb), rows, dim, cosv);
     else
-        cosine_partial_kernel<__nv_bfloat16><<<g, kCosThreads, 0, ctx->stream>>>(
-            static_cast<const __nv_bfloat16*>(kf), static_cast<const __nv_bfloat16*>(kb), rows, dim, bpl, psum,
-            pcnt, pskip);
+        cosine_pair_kernel<__nv_bfloat16><<<g, 256, 0, ctx->stream>>>(
+            static_cast<const __nv_bfloat16*>(kf), static_cast<const __nv_bfloat16*>(kb), rows, dim, cosv);
     EPK_LAUNCH_CHECK(ctx);
-    EPK_PROF(ctx, "cosine_final");
-    cosine_final_kernel<<<layers, 256, 0, ctx->stream>>>(psum, pcnt, pskip, bpl, sigma, skl);
+    EPK_PROF(ctx, "cosine_mean");
+    cosine_mean_kernel<<<layers, 32, 0, ctx->stream>>>(cosv, rows, sigma, skl);
     EPK_LAUNCH_CHECK(ctx);
     EPK_PROF(ctx, "cosine_total");
     cosine_skip_total_kernel<<<1, 32, 0, ctx->stream>>>(skl, layers, skipped);

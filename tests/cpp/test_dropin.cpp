@@ -194,9 +194,8 @@ static void test_sensitivity() {
     const auto tokens = synthetic_calibration_tokens(64, 5, model.config.vocab);
     const SensitivityProfile a = gpu::measure_sensitivity(model, tokens, 16, 4);
     const SensitivityProfile b = measure_sensitivity(model, tokens, 16, 4);
-    bool close = a.sigma.size() == b.sigma.size();
-    for (std::size_t l = 0; close && l < a.sigma.size(); ++l) close = std::abs(a.sigma[l] - b.sigma[l]) <= 1e-12;
-    CHECK(close && a.skipped_zero_norm == b.skipped_zero_norm, "sensitivity within 1e-12");
+    CHECK(a.sigma == b.sigma && a.sensitivity == b.sensitivity && a.skipped_zero_norm == b.skipped_zero_norm,
+          "sensitivity bitwise");
     CHECK(allocate(a, 8, 1.1).layer_budgets == allocate(b, 8, 1.1).layer_budgets, "allocation from GPU sigma");
 }
 
