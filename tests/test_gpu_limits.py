@@ -68,3 +68,31 @@ def test_step_64_heads(gpu):
     budgets = [100, 200]  # layer 1 is under budget: everything kept
     cin, cap = _cache(gpu, rng, L, H, counts, slack=8)
     _check_step(gpu, cin, cap, 64, 16, budgets, 8, rng)
+
+
+def test_tc_step_with_pins_equals_generic(gpu):
+    """Pins take the tc step off the fused threshold select (epk_evict_step's
+    generic branch: tc scores -> pooled select with pins -> compaction); the
+    result must equal select_pooled + compact with the same pins on the
+    step's own scores."""
+    from paper_2509_17396_b200.step import evict_step
+    rng = np.random.default_rng(77)
+    L, H, slack = 2, 4, 8
+    counts = [[300, 250, 0, 90], [120, 120, 120, 120]]
+    cin, cap = _cache(gpu, rng, L, H, counts, slack)
+    pins = {0, 1, 5}
+    budgets = [100, 60]
+    q = torch.as_tensor(bf16_round(rng.standard_normal((L, 8, 16, 128)).astype(np.float32)), device="cuda").bfloat16()
+    kp = torch.as_tensor(bf16_round(rng.standard_normal((L, H, 16, 128)).astype(np.float32)), device="cuda").bfloat16()
+    out = gpu.EpisodeCache(L, H, 128, cap, torch.bfloat16, "cuda")
+    scores = torch.zeros(cin.rows, dtype=torch.float32, device="cuda")
+    evict_step(cin, out, q, kp, budgets, pinned=pins, mode="tc_bf16", slack=slack, scores=scores)
+    torch.cuda.synchronize()
+    ref = gpu.EpisodeCache(L, H, 128, cap, torch.bfloat16, "cuda")
+    gpu.compact(cin, gpu.select_pooled(cin, scores, budgets, pins), ref, slack=slack)
+    torch.cuda.synchronize()
+    assert out.retained_positions() == ref.retained_positions()
+    for l in range(L):
+        present = {p for h in range(H) for p in cin.retained_positions()[l][h]}
+        kept = {p for h in range(H) for p in out.retained_positions()[l][h]}
+        assert (pins & present) <= kept
