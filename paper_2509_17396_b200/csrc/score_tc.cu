@@ -26,8 +26,8 @@
 //
 // Work partition (tile-balanced): a mode's work is the sequence of RUNS
 // (STATS: (layer, kv-head, query-chunk group); SCORE: (layer, kv-head)), each
-// a run of K tiles (STATS: ceil(n_h/256) cache tiles + the causal prompt
-// tiles; SCORE: ceil(n_h/128)).  Every CTA computes the run prefix from the
+// a run of 128-row K tiles (STATS: ceil(n_h/128) cache tiles + the causal
+// prompt tiles; SCORE: ceil(n_h/128)).  Every CTA computes the run prefix from the
 // device-resident head lengths (ragged after pooled eviction) and takes the
 // contiguous global tile range [T b/grid, T (b+1)/grid); a run cut by a CTA
 // boundary becomes two segments whose softmax partials P2 combines.  So the
@@ -36,12 +36,14 @@
 //
 // Shared memory keeps Q as [d-half][all query rows] (128-byte swizzled rows,
 // 8-row groups 1024 B apart) so any two consecutive 128-row chunks form one
-// 256-row B operand.  TMEM (512 columns): STATS four 128-column accumulator
-// slots (each epilogue warp group double-buffers), SCORE two 256-column slots.
-// Warp roles (352 threads): warp 0 TMA producer, warps 1-2 MMA issuers (one
-// elected lane each; they alternate jobs, warp 1 also owns the TMEM
-// allocation), warps 3-10 epilogue (warp e: TMEM lane quarter warp & 3,
-// column half of every job).
+// 256-row B operand.  TMEM (512 columns): STATS three 128-column accumulator
+// slots, each owned by one epilogue group and one MMA warp (job j -> slot
+// j mod 3); SCORE two 256-column slots.
+// Warp roles: warp 0 TMA producer; STATS (512 threads): warps 1-3 MMA issuers
+// (one per slot), warps 4-15 epilogue in three groups of four; SCORE (352
+// threads): warps 1-2 MMA issuers (alternate jobs), warps 3-10 epilogue
+// (warp e: TMEM lane quarter warp & 3, column half of every job).  Warp 1
+// owns the TMEM allocation.  One elected lane issues per MMA warp.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -421,8 +423,9 @@ __global__ void __maxnreg__(128)
             }
         }
     } else if (warp <= mma_warps<MODE>()) {
-        // MMA warp mw issues the jobs with (job & 1) == mw into TMEM slot mw;
-        // both walk the same segment/tile sequence and both release every K stage.
+        // STATS: MMA warp mw issues the jobs of slot mw (job % 3); SCORE: the
+        // jobs with (job & 1) == mw.  All MMA warps walk the same segment/tile
+        // sequence and each releases every K stage.
         const uint32_t mw = uint32_t(warp - 1);
         const bool leader = elect_one_sync();
         {  // ------------------------- MMA issuers (warp-wide, one lane issues) ------------
@@ -504,7 +507,7 @@ __global__ void __maxnreg__(128)
                 }
             }
         }
-    } else {  // ------------------------- epilogue (8 warps) -------------------------
+    } else {  // ------------------------- epilogue warps -------------------------
         const int e = warp - 1 - mma_warps<MODE>();
         const int quarter = warp & 3;  // TMEM lanes this warp may read
         const int half = e >> 2;       // SCORE: column half of every job; STATS: job group (job % 3)
@@ -528,11 +531,10 @@ __global__ void __maxnreg__(128)
                     m[c] = -INFINITY;
                     z[c] = 0.f;
                 }
-                // Warps of parity `half` take the jobs (tile, chunk) with
-                // (job & 1) == half -- i.e. TMEM slot `half` -- whole (128
-                // columns), so the two epilogue warps sharing an SM
-                // sub-partition work on different jobs and their max / exp2
-                // phases interleave on the SFU.
+                // Group `half` takes the jobs (tile, chunk) with job % 3 ==
+                // half -- TMEM slot `half` -- whole (128 columns), so the three
+                // epilogue warps sharing an SM sub-partition work on different
+                // jobs and their max / exp2 phases interleave on the SFU.
                 for (int t = 0; t < x.ntiles(); ++t) {
 #pragma unroll
                     for (int c = 0; c < kMaxQRes; ++c) {
