@@ -344,7 +344,8 @@ def run_e2e(args, c, epk, torch, device, ctx, dist):
     world = dist.get_world_size() if dist is not None else 1
     h2d = (dev_k[0].numel() + dev_v[0].numel() + dev_q[0].numel() + dev_kp[0].numel()) * 2 + 0  # positions on device
     d2h = out_pos.numel() * 4 + out_len.numel() * 4
-    return {"value": world * live * steps / float(tt.item()), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+    units = getattr(args, "total_live", None) or world * live  # layer sharding: the episode's units
+    return {"value": units * steps / float(tt.item()), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
             "ms_per_step": 1000.0 * float(tt.item()) / steps,
             "path": "paper_2509_17396_b200.append_to_cache + step.evict_step (C ABI epk_append/epk_evict_step), "
@@ -477,6 +478,9 @@ def main():
     ap.add_argument("--layer-group", type=int, default=0, help="layers per P2/select/compaction group (0 = all layers)")
     ap.add_argument("--no-overlap", action="store_true", help="compaction on the main stream")
     ap.add_argument("--fused", action="store_true", help="single-kernel fused step (EPK_OPT_FUSED, experimental)")
+    ap.add_argument("--shard-layers", action="store_true",
+                    help="N>1: split ONE episode's layers over the ranks (strong scaling) instead of one episode "
+                         "per rank (weak scaling, the default)")
     ap.add_argument("--layers", type=int, default=0, help=argparse.SUPPRESS)  # experiments: override L
     ap.add_argument("--timeline", default=None, help="write one profiled step's kernel timeline to this file")
     args = ap.parse_args()
@@ -508,12 +512,20 @@ def main():
         else:
             td.init_process_group("nccl", device_id=device)
         dist = td
+    # episodes are the natural shard (one per rank, weak scaling);
+    # --shard-layers splits one episode's layers instead (strong scaling)
+    shard = args.shard_layers and world > 1
+    c_total = c
+    if shard:
+        l0, l1 = c["L"] * rank // world, c["L"] * (rank + 1) // world
+        c = dict(c, L=max(1, l1 - l0))
+    args.total_live = step_sizes(c_total)[1] if shard else None
     r = run_ours(args, c, rank, world, device, torch, dist)
     hbm, tc_sus, tc_burst, peak_src = load_peaks()
-    B, F, X = algorithmic(c)
+    B, F, X = algorithmic(c)  # per GPU
     ms = r["ms"]
     step_ms = ms / args.steps
-    value = world * r["live"] * args.steps / (ms / 1000.0)
+    value = (args.total_live or world * r["live"]) * args.steps / (ms / 1000.0)
     # dominant kernel (largest share of the step) and its roofline
     kernels = r["kernels"]
     G, p, d, L, H = c["Hq"] // c["H"], c["p"], c["d"], c["L"], c["H"]
@@ -559,12 +571,15 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": c["desc"], "layers": L, "q_heads": c["Hq"], "kv_heads": H, "head_dim": d,
+            "config": {"workload": c["desc"], "layers": c_total["L"], "q_heads": c["Hq"], "kv_heads": H, "head_dim": d,
                        "context": c["N"], "block": c["block"], "budget_per_head": c["M"], "prompt_len": p,
-                       "live_entries_per_step": live, "kept_per_step": keep, "score_mode": "tc_bf16",
-                       "aggregation": "max", "episodes_per_gpu": 1, "parallelism": f"episodes x{world}",
+                       "live_entries_per_step": step_sizes(c_total)[1], "kept_per_step": step_sizes(c_total)[2],
+                       "score_mode": "tc_bf16", "aggregation": "max",
+                       "episodes_per_gpu": 1 if not shard else 1.0 / world,
+                       "parallelism": f"layers x{world} (one episode)" if shard else f"episodes x{world}",
                        "l2": "inputs larger than L2: 3 rotating steady-state caches of "
                              f"{2 * live * d * 2 / 1e9:.2f} GB K+V each"},
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels, "cpu_baseline": cpu,
