@@ -261,6 +261,11 @@ int epk_debug_tma_stream(epk_ctx* ctx, const void* k, int64_t rows, int32_t box_
  * or 256) from resident shared memory; drain != 0 adds epilogue warps that
  * tcgen05.ld every result before its TMEM slot is reused. */
 int epk_debug_mma_rate(epk_ctx* ctx, int32_t n, int32_t iters, int32_t drain);
+/* TMA gather (probe): rows (multiple of 128) bf16 [rows][128] k/v [dev], keep [dev] u8 [rows],
+ * prefix [dev] int32 [rows/128] kept rows before each 128-row chunk; kept rows -> kout/vout
+ * (contiguous) using tile::gather4 loads and 1-D bulk stores on `sms` CTAs. */
+int epk_debug_tma_gather(epk_ctx* ctx, const void* k, const void* v, int64_t rows, const uint8_t* keep,
+                         const int32_t* prefix, void* kout, void* vout, int32_t sms);
 /* Two-SM (cta_group::2, M = 256) MMA issue ceiling, n = 128 or 256 (probe). */
 int epk_debug_mma2sm_rate(epk_ctx* ctx, int32_t n, int32_t iters);
 /* P1 pipeline without the softmax: TMA-streamed 256-row K stages x nq

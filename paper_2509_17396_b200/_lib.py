@@ -76,6 +76,7 @@ _SIGS = {
     "epk_debug_tma_stream": (C.c_int, [vp, vp, i64, i32, i32, i32]),
     "epk_debug_mma_rate": (C.c_int, [vp, i32, i32, i32]),
     "epk_debug_mma2sm_rate": (C.c_int, [vp, i32, i32]),
+    "epk_debug_tma_gather": (C.c_int, [vp, vp, vp, i64, vp, vp, vp, vp, i32]),
     "epk_debug_mma_stream": (C.c_int, [vp, vp, i64, i32, i32, i32]),
 }
 

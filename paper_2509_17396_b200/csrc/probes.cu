@@ -9,6 +9,7 @@
 
 #include "epk_internal.cuh"
 #include "sm100.cuh"
+#include "tc_common.cuh"
 
 namespace epk {
 using namespace sm100;
@@ -284,6 +285,114 @@ int launch_mma2sm_rate(epk_ctx* ctx, int n, int iters) {
     return EPK_OK;
 }
 
+// TMA gather (round-2 evidence for an overlapped compaction): `sms` CTAs of 4
+// warps walk 128-row chunks; the kept rows' indices (from keep[]) feed
+// tile::gather4 loads (4 arbitrary rows of K / V per op) into a packed shared
+// buffer, and one 1-D bulk store per tensor writes the chunk's kept rows to
+// their contiguous destination (prefix[chunk]).  Two buffers: a chunk's
+// stores drain while the next chunk's gathers land.  No registers hold the
+// bytes in flight, so a few SMs can keep HBM busy.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar, int col, int r0, int r1,
+                                            int r2, int r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_store_1d(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(dst)),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(128) tma_gather_kernel(const __grid_constant__ CUtensorMap tk,
+                                                         const __grid_constant__ CUtensorMap tv,
+                                                         const uint8_t* keep, const int32_t* prefix, int nchunks,
+                                                         uint8_t* kout, uint8_t* vout) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t* buf = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // [2][K 32 KB | V 32 KB]
+    __shared__ uint64_t full[2];
+    __shared__ int s_idx[2][128];
+    __shared__ int s_n[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    int it = 0;
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        const int b = it & 1;
+        // kept row indices of the chunk, in order (warp w: rows 32w..32w+31)
+        const int r = c * 128 + warp * 32 + lane;
+        const bool k = keep[r] != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, k);
+        __shared__ int s_wc[4];
+        if (lane == 0) s_wc[warp] = __popc(bal);
+        __syncthreads();
+        int base = 0;
+        for (int w = 0; w < warp; ++w) base += s_wc[w];
+        if (k) s_idx[b][base + __popc(bal & ((1u << lane) - 1u))] = r;
+        if (threadIdx.x == 0) s_n[b] = s_wc[0] + s_wc[1] + s_wc[2] + s_wc[3];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int n = s_n[b];
+            uint8_t* sk = buf + b * 65536;
+            uint8_t* sv = sk + 32768;
+            // buffer b was last stored two chunks ago: its reads must be done
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            const int groups = (n + 3) / 4;
+            if (groups) {
+                mbar_expect_tx(&full[b], uint32_t(groups * 4 * 256 * 2));
+                for (int g = 0; g < groups; ++g) {
+                    const int* ix = s_idx[b] + 4 * g;
+                    const int i0 = ix[0], i1 = 4 * g + 1 < n ? ix[1] : i0, i2 = 4 * g + 2 < n ? ix[2] : i0,
+                              i3 = 4 * g + 3 < n ? ix[3] : i0;
+                    tma_gather4(sk + g * 1024, &tk, &full[b], 0, i0, i1, i2, i3);
+                    tma_gather4(sv + g * 1024, &tv, &full[b], 0, i0, i1, i2, i3);
+                }
+                mbar_wait(&full[b], uint32_t((it >> 1) & 1));
+                const int64_t dst = int64_t(prefix[c]) * 256;
+                bulk_store_1d(kout + dst, sk, uint32_t(n * 256));
+                bulk_store_1d(vout + dst, sv, uint32_t(n * 256));
+            } else {
+                // keep the barrier phases aligned with `it` (arrive with no bytes)
+                mbar_expect_tx(&full[b], 0);
+                mbar_wait(&full[b], uint32_t((it >> 1) & 1));
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+int launch_tma_gather(epk_ctx* ctx, const void* k, const void* v, int64_t rows, const uint8_t* keep,
+                      const int32_t* prefix, void* kout, void* vout, int sms) {
+    auto enc = get_encode();
+    if (!enc) return fail(EPK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap mk, mv;
+    cuuint64_t dims[2] = {128, cuuint64_t(rows)};
+    cuuint64_t strides[1] = {256};
+    cuuint32_t box[2] = {128, 1};
+    cuuint32_t es[2] = {1, 1};
+    for (int t = 0; t < 2; ++t) {
+        CUresult r = enc(t ? &mv : &mk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(t ? v : k), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(EPK_ERR_CUDA, "tma_gather: tensor map (" + std::to_string(int(r)) + ")");
+    }
+    const int smem = 2 * 65536 + 128;
+    EPK_CUDA_CHECK(cudaFuncSetAttribute(tma_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    EPK_PROF(ctx, "tma_gather");
+    tma_gather_kernel<<<std::max(1, std::min(sms, ctx->num_sms)), 128, smem, ctx->stream>>>(
+        mk, mv, keep, prefix, int(rows / 128), static_cast<uint8_t*>(kout), static_cast<uint8_t*>(vout));
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
 // TMA-streamed 256-row K stages (`stages`-deep ring) feeding `nq` resident
 // 128-row A chunks: per stage nq MMAs of 128 x 256 x 128 into two TMEM slots,
 // drained by 8 epilogue warps (tcgen05.ld, no math).  The P1 pipeline
@@ -424,6 +533,11 @@ extern "C" int epk_debug_mma_stream(epk_ctx* ctx, const void* k, int64_t rows, i
 
 extern "C" int epk_debug_mma_rate(epk_ctx* ctx, int32_t n, int32_t iters, int32_t drain) {
     return epk::launch_mma_rate(ctx, n, iters, drain);
+}
+
+extern "C" int epk_debug_tma_gather(epk_ctx* ctx, const void* k, const void* v, int64_t rows, const uint8_t* keep,
+                                    const int32_t* prefix, void* kout, void* vout, int32_t sms) {
+    return epk::launch_tma_gather(ctx, k, v, rows, keep, prefix, kout, vout, sms);
 }
 
 extern "C" int epk_debug_mma2sm_rate(epk_ctx* ctx, int32_t n, int32_t iters) {
