@@ -306,45 +306,50 @@ __device__ __forceinline__ void bulk_store_1d(void* dst, const void* src, uint32
                  : "memory");
 }
 
+template <int NB>
 __global__ void __launch_bounds__(128) tma_gather_kernel(const __grid_constant__ CUtensorMap tk,
                                                          const __grid_constant__ CUtensorMap tv,
                                                          const uint8_t* keep, const int32_t* prefix, int nchunks,
                                                          uint8_t* kout, uint8_t* vout) {
+    // NB chunks in flight per CTA: chunk i's gathers are issued, then chunk
+    // i-(NB-1)'s (long landed) rows are stored
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    uint8_t* buf = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // [2][K 32 KB | V 32 KB]
-    __shared__ uint64_t full[2];
-    __shared__ int s_idx[2][128];
-    __shared__ int s_n[2];
+    uint8_t* buf = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // [NB][K 32 KB | V 32 KB]
+    __shared__ uint64_t full[NB];
+    __shared__ int s_idx[NB][128];
+    __shared__ int s_n[NB], s_c[NB];
+    __shared__ int s_wc[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
+        for (int i = 0; i < NB; ++i) mbar_init(&full[i], 1);
         fence_barrier_init();
     }
     __syncthreads();
-    int it = 0;
-    for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
-        const int b = it & 1;
-        // kept row indices of the chunk, in order (warp w: rows 32w..32w+31)
-        const int r = c * 128 + warp * 32 + lane;
-        const bool k = keep[r] != 0;
-        const unsigned bal = __ballot_sync(0xffffffffu, k);
-        __shared__ int s_wc[4];
-        if (lane == 0) s_wc[warp] = __popc(bal);
-        __syncthreads();
-        int base = 0;
-        for (int w = 0; w < warp; ++w) base += s_wc[w];
-        if (k) s_idx[b][base + __popc(bal & ((1u << lane) - 1u))] = r;
-        if (threadIdx.x == 0) s_n[b] = s_wc[0] + s_wc[1] + s_wc[2] + s_wc[3];
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int n = s_n[b];
-            uint8_t* sk = buf + b * 65536;
-            uint8_t* sv = sk + 32768;
-            // buffer b was last stored two chunks ago: its reads must be done
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            const int groups = (n + 3) / 4;
-            if (groups) {
+    const int mine = nchunks > int(blockIdx.x) ? (nchunks - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+    for (int it = 0; it < mine + NB - 1; ++it) {
+        const int b = it % NB;
+        if (it < mine) {
+            const int c = int(blockIdx.x) + it * int(gridDim.x);
+            const int r = c * 128 + warp * 32 + lane;
+            const bool k = keep[r] != 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, k);
+            if (lane == 0) s_wc[warp] = __popc(bal);
+            __syncthreads();
+            int base = 0;
+            for (int w = 0; w < warp; ++w) base += s_wc[w];
+            if (k) s_idx[b][base + __popc(bal & ((1u << lane) - 1u))] = r;
+            if (threadIdx.x == 0) {
+                s_n[b] = s_wc[0] + s_wc[1] + s_wc[2] + s_wc[3];
+                s_c[b] = c;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const int n = s_n[b];
+                uint8_t* sk = buf + b * 65536;
+                uint8_t* sv = sk + 32768;
+                // buffer b's previous stores (chunk it-NB) must have read it
+                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NB - 2) : "memory");
+                const int groups = (n + 3) / 4;
                 mbar_expect_tx(&full[b], uint32_t(groups * 4 * 256 * 2));
                 for (int g = 0; g < groups; ++g) {
                     const int* ix = s_idx[b] + 4 * g;
@@ -353,14 +358,17 @@ __global__ void __launch_bounds__(128) tma_gather_kernel(const __grid_constant__
                     tma_gather4(sk + g * 1024, &tk, &full[b], 0, i0, i1, i2, i3);
                     tma_gather4(sv + g * 1024, &tv, &full[b], 0, i0, i1, i2, i3);
                 }
-                mbar_wait(&full[b], uint32_t((it >> 1) & 1));
-                const int64_t dst = int64_t(prefix[c]) * 256;
-                bulk_store_1d(kout + dst, sk, uint32_t(n * 256));
-                bulk_store_1d(vout + dst, sv, uint32_t(n * 256));
-            } else {
-                // keep the barrier phases aligned with `it` (arrive with no bytes)
-                mbar_expect_tx(&full[b], 0);
-                mbar_wait(&full[b], uint32_t((it >> 1) & 1));
+            }
+        }
+        const int jt = it - (NB - 1);  // the chunk whose rows are stored now
+        if (threadIdx.x == 0 && jt >= 0) {
+            const int bj = jt % NB;
+            mbar_wait(&full[bj], uint32_t((jt / NB) & 1));
+            const int n = s_n[bj];
+            if (n) {
+                const int64_t dst = int64_t(prefix[s_c[bj]]) * 256;
+                bulk_store_1d(kout + dst, buf + bj * 65536, uint32_t(n * 256));
+                bulk_store_1d(vout + dst, buf + bj * 65536 + 32768, uint32_t(n * 256));
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
@@ -384,10 +392,11 @@ int launch_tma_gather(epk_ctx* ctx, const void* k, const void* v, int64_t rows, 
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(EPK_ERR_CUDA, "tma_gather: tensor map (" + std::to_string(int(r)) + ")");
     }
-    const int smem = 2 * 65536 + 128;
-    EPK_CUDA_CHECK(cudaFuncSetAttribute(tma_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    constexpr int NB = 3;
+    const int smem = NB * 65536 + 128;
+    EPK_CUDA_CHECK(cudaFuncSetAttribute(tma_gather_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     EPK_PROF(ctx, "tma_gather");
-    tma_gather_kernel<<<std::max(1, std::min(sms, ctx->num_sms)), 128, smem, ctx->stream>>>(
+    tma_gather_kernel<NB><<<std::max(1, std::min(sms, ctx->num_sms)), 128, smem, ctx->stream>>>(
         mk, mv, keep, prefix, int(rows / 128), static_cast<uint8_t*>(kout), static_cast<uint8_t*>(vout));
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
