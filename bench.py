@@ -181,7 +181,7 @@ def run_ours(args, c, rank, world, device, torch, dist):
     from paper_2509_17396_b200.step import StepPlan, evict_step
 
     ctx = epk.default_context(device.index)
-    ctx.set_option(layer_group=args.layer_group, overlap=not args.no_overlap, fused=args.fused)
+    ctx.set_option(layer_group=args.layer_group, overlap=not args.no_overlap)
     n_h, live, keep = step_sizes(c)
     R = 3
     caches, qs, kps, out = make_inputs(epk, torch, c, R, device, 1234 + rank)
@@ -477,7 +477,6 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layer-group", type=int, default=0, help="layers per P2/select/compaction group (0 = all layers)")
     ap.add_argument("--no-overlap", action="store_true", help="compaction on the main stream")
-    ap.add_argument("--fused", action="store_true", help="single-kernel fused step (EPK_OPT_FUSED, experimental)")
     ap.add_argument("--shard-layers", action="store_true",
                     help="N>1: split ONE episode's layers over the ranks (strong scaling) instead of one episode "
                          "per rank (weak scaling, the default)")

@@ -107,14 +107,9 @@ int epk_version(void);
  *                        all layers in one group)
  *   EPK_OPT_OVERLAP      1 (default): with more than one group, each group's
  *                        select + compaction runs on a second stream,
- *                        overlapping the next group's scoring
- *   EPK_OPT_FUSED        0 (default) / 1: tensor-core steps without pins run as
- *                        ONE persistent cooperative kernel (score, threshold
- *                        select and compaction of every layer, compaction
- *                        overlapping later layers' scoring); experimental */
+ *                        overlapping the next group's scoring */
 #define EPK_OPT_LAYER_GROUP 1
 #define EPK_OPT_OVERLAP 2
-#define EPK_OPT_FUSED 3
 int epk_ctx_set_option(epk_ctx* ctx, int32_t option, int64_t value);
 /* Number of kernels this library launched on the context since creation. */
 int64_t epk_ctx_launch_count(epk_ctx* ctx);
@@ -136,8 +131,12 @@ int epk_ctx_profile_timeline(epk_ctx* ctx, int64_t index, char* name_out, float*
  *   k_prompt [dev] [layers][kv_heads][prompt_len][head_dim]
  * mode EPK_SCORE_EXACT_F32 needs dtype F32; EPK_SCORE_TC_BF16 needs dtype BF16,
  * head_dim 128, prompt_len <= 256 and (q_heads/kv_heads)*prompt_len <= 2048
- * (longer prompts, e.g. KVzip's block repetition: epk_score_grids).  n_max_per_head [host] bounds every head's live count
- * (grid sizing only).  Asynchronous. */
+ * (longer prompts, e.g. KVzip's block repetition: epk_score_grids).
+ * n_max_per_head [host] must bound every head's live count: the exact-f32
+ * scorer sizes its logits scratch with it and refuses a longer head (deferred
+ * EPK_ERR_ARG, epk_ctx_poll_error; that head's scores are not written); the
+ * tensor-core scorer reads the live lengths on the device and needs no bound.
+ * Asynchronous. */
 int epk_score(epk_ctx* ctx, const epk_cache_desc* cache, const void* q_prompt,
               const void* k_prompt, int32_t q_heads, int32_t prompt_len, int32_t aggregation,
               int32_t mode, int64_t n_max_per_head, float* scores);
@@ -177,10 +176,14 @@ int epk_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* ou
                 const uint8_t* keep, int32_t slack);
 
 /* ---- append_to_cache ------------------------------------------------------ *
- * Writes a block of new rows into the slack after each head:
+ * Writes a block of new rows into the free rows after each head's live rows:
  *   k_new, v_new [dev] [layers][kv_heads][len][head_dim], positions [dev] [len]
- * and advances head_off so the heads stay contiguous (the gap after the last
- * row of head h must be >= len; the caller sized it with `slack`).  Async. */
+ * and advances head_len (head_off is unchanged).  `slack` is the gap the
+ * caller left after every head (the out_slack of the compaction that built
+ * the cache): len > slack > 0 fails at once with EPK_ERR_ARG; slack = 0 skips
+ * that host check.  On the device every head's actual gap is checked; a head
+ * whose gap is too small is left unchanged and EPK_ERR_ARG is deferred to
+ * epk_ctx_poll_error.  Asynchronous. */
 int epk_append(epk_ctx* ctx, const epk_cache_desc* cache, const void* k_new, const void* v_new,
                const int32_t* positions, int32_t len, int32_t slack);
 
@@ -252,25 +255,6 @@ int epk_key_cosine_sigma(epk_ctx* ctx, const void* k_full, const void* k_block, 
  * y[i] = epk_expf(x[i]) as the EPK-F32 v1 kernels compute it ([dev] fp32),
  * for the bitwise host/device parity test. */
 int epk_debug_expf(epk_ctx* ctx, const float* x, float* y, int64_t n);
-/* TMA streaming probe: reads rows x 128 bf16 through the scorer's K-tile
- * producer (box_rows x 64 boxes, `stages`-deep ring, `grid` CTAs) with a
- * trivial consumer; time it with epk_ctx_profile to size the K ring. */
-int epk_debug_tma_stream(epk_ctx* ctx, const void* k, int64_t rows, int32_t box_rows, int32_t stages,
-                         int32_t grid);
-/* tcgen05 issue-rate probe: `iters` 128 x n x 128 bf16 MMAs per SM (n = 128
- * or 256) from resident shared memory; drain != 0 adds epilogue warps that
- * tcgen05.ld every result before its TMEM slot is reused. */
-int epk_debug_mma_rate(epk_ctx* ctx, int32_t n, int32_t iters, int32_t drain);
-/* TMA gather (probe): rows (multiple of 128) bf16 [rows][128] k/v [dev], keep [dev] u8 [rows],
- * prefix [dev] int32 [rows/128] kept rows before each 128-row chunk; kept rows -> kout/vout
- * (contiguous) using tile::gather4 loads and 1-D bulk stores on `sms` CTAs. */
-int epk_debug_tma_gather(epk_ctx* ctx, const void* k, const void* v, int64_t rows, const uint8_t* keep,
-                         const int32_t* prefix, void* kout, void* vout, int32_t sms);
-/* Two-SM (cta_group::2, M = 256) MMA issue ceiling, n = 128 or 256 (probe). */
-int epk_debug_mma2sm_rate(epk_ctx* ctx, int32_t n, int32_t iters);
-/* P1 pipeline without the softmax: TMA-streamed 256-row K stages x nq
- * resident 128-row chunks, 128 x 256 x 128 MMAs, optional TMEM drain. */
-int epk_debug_mma_stream(epk_ctx* ctx, const void* k, int64_t rows, int32_t nq, int32_t stages, int32_t drain);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,7 @@
 #include <cstring>
 #include <limits>
 #include <random>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -203,6 +204,113 @@ void score_layer_f32(int hq, int hkv, int d, int p, const i64* head_off, const f
                 if (!agg_max) a = a / float(p);
                 float& slot = out[head_off[h] + j];
                 if (a > slot) slot = a;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Multi-threaded forms of the two restatements above, for the parity tests at
+// benchmark scale (a cfg5 layer is ~640 M dot products).  Same arithmetic:
+// every logit is the same sequential-d chain, every row's max / exp /
+// denominator the same sequence; only (a) four prompt rows' dot products are
+// interleaved (independent chains, identical bits) and (b) query heads run on
+// separate threads, each into its own window accumulator, combined afterwards
+// in query-head order exactly as the single-threaded loops do.
+// ---------------------------------------------------------------------------
+template <typename T>
+void qhead_window(int qh, int group, int d, int p, const i64* head_off, const T* q, const T* k, const T* kp,
+                  int agg_max, T* acc_col) {
+    const int h = qh / group;
+    const i64 n = head_off[h + 1] - head_off[h];
+    const T* kh = k + head_off[h] * d;
+    const T* kph = kp + i64(h) * p * d;
+    const T scale = T(1.0 / std::sqrt(double(d)));
+    const T kNegInf = -std::numeric_limits<T>::infinity();
+    std::vector<T> lg(size_t(4) * size_t(n + p));
+    std::vector<float> scratch;
+    for (i64 j = 0; j < n; ++j) acc_col[j] = agg_max ? kNegInf : T(0);
+    for (int t0 = 0; t0 < p; t0 += 4) {
+        const int nt = std::min(4, p - t0);
+        const i64 vis_max = n + t0 + nt;
+        const T* qv[4];
+        for (int u = 0; u < 4; ++u) qv[u] = q + (i64(qh) * p + t0 + std::min(u, nt - 1)) * d;
+        for (i64 j = 0; j < vis_max; ++j) {
+            const T* kv = j < n ? kh + j * d : kph + (j - n) * d;
+            T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            for (int dd = 0; dd < d; ++dd) {
+                const T x = kv[dd];
+                a0 = a0 + qv[0][dd] * x;
+                a1 = a1 + qv[1][dd] * x;
+                a2 = a2 + qv[2][dd] * x;
+                a3 = a3 + qv[3][dd] * x;
+            }
+            lg[size_t(0 * (n + p) + j)] = a0 * scale;
+            lg[size_t(1 * (n + p) + j)] = a1 * scale;
+            lg[size_t(2 * (n + p) + j)] = a2 * scale;
+            lg[size_t(3 * (n + p) + j)] = a3 * scale;
+        }
+        for (int u = 0; u < nt; ++u) {
+            T* e = lg.data() + size_t(u) * size_t(n + p);
+            const i64 visible = n + t0 + u + 1;
+            T m = kNegInf;
+            for (i64 j = 0; j < visible; ++j)
+                if (e[j] > m) m = e[j];
+            T den;
+            if constexpr (sizeof(T) == 8) {
+                den = 0.0;
+                for (i64 j = 0; j < visible; ++j) {
+                    const T x = std::exp(e[j] - m);
+                    e[j] = x;
+                    den += x;
+                }
+            } else {
+                for (i64 j = 0; j < visible; ++j) e[j] = epk_expf(e[j] - m);
+                den = tree_sum_chunks(e, visible, scratch);
+            }
+            for (i64 j = 0; j < n; ++j) {
+                const T w = e[j] / den;
+                if (agg_max) {
+                    if constexpr (sizeof(T) == 8) acc_col[j] = std::max(acc_col[j], w);
+                    else if (w > acc_col[j]) acc_col[j] = w;
+                } else {
+                    acc_col[j] = acc_col[j] + w;
+                }
+            }
+        }
+    }
+}
+
+template <typename T>
+void score_layer_mt(int hq, int hkv, int d, int p, const i64* head_off, const T* q, const T* k, const T* kp,
+                    int agg_max, T* out, int threads) {
+    const int group = hq / hkv;
+    std::vector<i64> acc_off(size_t(hq) + 1, 0);
+    for (int qh = 0; qh < hq; ++qh) acc_off[qh + 1] = acc_off[qh] + (head_off[qh / group + 1] - head_off[qh / group]);
+    std::vector<T> acc(size_t(acc_off[hq]));
+    if (threads <= 0) threads = int(std::max(1u, std::thread::hardware_concurrency()));
+    threads = std::min(threads, hq);
+    std::vector<std::thread> pool;
+    for (int w = 0; w < threads; ++w)
+        pool.emplace_back([&, w] {
+            for (int qh = w; qh < hq; qh += threads)
+                qhead_window<T>(qh, group, d, p, head_off, q, k, kp, agg_max, acc.data() + acc_off[qh]);
+        });
+    for (auto& th : pool) th.join();
+    for (int h = 0; h < hkv; ++h) {
+        const i64 n = head_off[h + 1] - head_off[h];
+        for (int g = 0; g < group; ++g) {
+            const T* a_col = acc.data() + acc_off[h * group + g];
+            for (i64 j = 0; j < n; ++j) {
+                T a = a_col[j];
+                if (!agg_max) a = a / T(p);
+                T& slot = out[head_off[h] + j];
+                if (sizeof(T) == 8) {
+                    if (g == 0 || a > slot) slot = a;  // scoring.hpp:118-123
+                } else {
+                    if (g == 0) slot = -std::numeric_limits<T>::infinity();
+                    if (a > slot) slot = a;
+                }
             }
         }
     }
@@ -535,6 +643,16 @@ void orc_score_layer_f64(int hq, int hkv, int d, int p, const i64* head_off, con
 void orc_score_layer_f32(int hq, int hkv, int d, int p, const i64* head_off, const float* q,
                          const float* k, const float* kp, int agg_max, float* out) {
     score_layer_f32(hq, hkv, d, p, head_off, q, k, kp, agg_max, out);
+}
+
+void orc_score_layer_f64_mt(int hq, int hkv, int d, int p, const i64* head_off, const double* q,
+                            const double* k, const double* kp, int agg_max, double* out, int threads) {
+    score_layer_mt<double>(hq, hkv, d, p, head_off, q, k, kp, agg_max, out, threads);
+}
+
+void orc_score_layer_f32_mt(int hq, int hkv, int d, int p, const i64* head_off, const float* q,
+                            const float* k, const float* kp, int agg_max, float* out, int threads) {
+    score_layer_mt<float>(hq, hkv, d, p, head_off, q, k, kp, agg_max, out, threads);
 }
 
 // The restated attention grids themselves (toymodel.hpp:327-391): grids for

@@ -47,6 +47,10 @@ def orc():
         lib.orc_score_layer_f64.restype = None
         lib.orc_score_layer_f32.argtypes = [C.c_int] * 4 + [_i64p, _f32p, _f32p, _f32p, C.c_int, _f32p]
         lib.orc_score_layer_f32.restype = None
+        lib.orc_score_layer_f64_mt.argtypes = [C.c_int] * 4 + [_i64p, _f64p, _f64p, _f64p, C.c_int, _f64p, C.c_int]
+        lib.orc_score_layer_f64_mt.restype = None
+        lib.orc_score_layer_f32_mt.argtypes = [C.c_int] * 4 + [_i64p, _f32p, _f32p, _f32p, C.c_int, _f32p, C.c_int]
+        lib.orc_score_layer_f32_mt.restype = None
         lib.orc_prompt_grids_f64.argtypes = [C.c_int] * 4 + [_i64p, _f64p, _f64p, _f64p, _f64p]
         lib.orc_prompt_grids_f64.restype = None
         lib.orc_expf.argtypes = [C.c_float]
@@ -144,6 +148,26 @@ def score_layer_f64(q, k, kp, head_off, agg_max=True):
     out = np.empty(k.shape[0], np.float64)
     orc().orc_score_layer_f64(hq, hkv, d, p, _c(head_off, np.int64), _c(q, np.float64), _c(k, np.float64),
                               _c(kp, np.float64), int(agg_max), out)
+    return out
+
+
+def score_layer_f64_mt(q, k, kp, head_off, agg_max=True, threads=0):
+    """score_layer_f64 on `threads` host threads (0: all cores); same bits."""
+    hq, p, d = q.shape
+    hkv = kp.shape[0]
+    out = np.empty(k.shape[0], np.float64)
+    orc().orc_score_layer_f64_mt(hq, hkv, d, p, _c(head_off, np.int64), _c(q, np.float64), _c(k, np.float64),
+                                 _c(kp, np.float64), int(agg_max), out, int(threads))
+    return out
+
+
+def score_layer_f32_mt(q, k, kp, head_off, agg_max=True, threads=0):
+    """score_layer_f32 (EPK-F32 v1) on `threads` host threads; same bits."""
+    hq, p, d = q.shape
+    hkv = kp.shape[0]
+    out = np.empty(k.shape[0], np.float32)
+    orc().orc_score_layer_f32_mt(hq, hkv, d, p, _c(head_off, np.int64), _c(q, np.float32), _c(k, np.float32),
+                                 _c(kp, np.float32), int(agg_max), out, int(threads))
     return out
 
 

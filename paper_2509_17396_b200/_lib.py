@@ -73,11 +73,6 @@ _SIGS = {
     "epk_score_keydiff": (C.c_int, [vp, vp, vp]),
     "epk_serialize_epkv": (C.c_int, [vp, vp, C.c_uint64, C.c_char_p, C.c_uint64, vp, i32, vp, i64, vp, vp]),
     "epk_debug_expf": (C.c_int, [vp, vp, vp, i64]),
-    "epk_debug_tma_stream": (C.c_int, [vp, vp, i64, i32, i32, i32]),
-    "epk_debug_mma_rate": (C.c_int, [vp, i32, i32, i32]),
-    "epk_debug_mma2sm_rate": (C.c_int, [vp, i32, i32]),
-    "epk_debug_tma_gather": (C.c_int, [vp, vp, vp, i64, vp, vp, vp, vp, i32]),
-    "epk_debug_mma_stream": (C.c_int, [vp, vp, i64, i32, i32, i32]),
 }
 
 _lib = None

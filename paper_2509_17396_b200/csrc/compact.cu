@@ -46,6 +46,7 @@ struct CompactParams {
     int32_t* out_len;
     int32_t* chunk_cnt;     // [layers][max_chunks]
     int32_t* chunk_prefix;  // [layers][max_chunks]
+    int32_t* layer_bad;     // [layers] plan: kept rows + slack exceed the output layer (gather skips it)
     int* err_flag;
     // threshold mode (the tensor-core step): keep[] is derived here from the
     // scorer's keys and the per-layer threshold (select_threshold_kernel)
@@ -87,7 +88,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_count_kernel(const 
         const int64_t base = P.in_lt.base[layer];
         const int32_t* off = P.in_off + layer * (P.H + 1);
         const uint64_t t0 = P.thr[2 * layer], U = P.thr[2 * layer + 1];
-        const bool all = (t0 >> 32) != 0;
+        const bool all = ((t0 >> 32) & 1) != 0;
+        const bool none = ((t0 >> 33) & 1) != 0;  // layer budget 0
         const uint32_t T = uint32_t(t0);
         uint8_t* kp = P.keep_out + base;
         // the chunk's first head (warp-uniform) and where the next starts: the
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_count_kernel(const 
             uint8_t k = 0;
             if (r < rows) {
                 const int h = r < h0_end ? h0 : head_of_row(off, P.H, r);
-                if (r - off[h] < P.in_len[layer * P.H + h]) {
+                if (!none && r - off[h] < P.in_len[layer * P.H + h]) {
                     const uint32_t key = __ldcg(P.keys + base + r);
                     k = (all || key < T ||
                          (key == T && ((uint64_t(uint32_t(P.in_pos[base + r])) << 8) | uint64_t(h)) <= U)) ? 1 : 0;
@@ -176,7 +178,15 @@ __global__ void __launch_bounds__(256) compact_plan_kernel(const __grid_constant
     if (threadIdx.x == 0) {
         const int64_t cap = P.out_lt.base[layer + 1] - P.out_lt.base[layer];
         const int64_t need = s_head_prefix[H] + int64_t(P.slack) * H;
-        if (need > cap) atomicCAS(P.err_flag, 0, EPK_ERR_ARG);
+        P.layer_bad[layer] = need > cap;
+        if (need > cap) {
+            // the output layer cannot hold the kept rows: flag it, leave the
+            // layer empty and let the gather skip it (no store past the layer)
+            atomicCAS(P.err_flag, 0, EPK_ERR_ARG);
+            for (int h = 0; h <= H; ++h) P.out_off[layer * (H + 1) + h] = 0;
+            for (int h = 0; h < H; ++h) P.out_len[layer * H + h] = 0;
+            return;
+        }
         for (int h = 0; h < H; ++h) {
             P.out_off[layer * (H + 1) + h] = int32_t(s_head_prefix[h] + int64_t(P.slack) * h);
             P.out_len[layer * H + h] = int32_t(s_head_prefix[h + 1] - s_head_prefix[h]);
@@ -190,7 +200,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_gather_kernel(const
     const int layer = blockIdx.y;
     const int chunk = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (chunk >= P.max_chunks) return;
+    if (chunk >= P.max_chunks || P.layer_bad[layer]) return;
     const int32_t* off = P.in_off + layer * (P.H + 1);
     const int64_t rows = off[P.H];
     const int64_t r0 = int64_t(chunk) * kChunkRows;
@@ -288,12 +298,13 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     P.keep_out = const_cast<uint8_t*>(keep);
     P.hist_fine = hist_fine;
     P.hist_coarse = hist_coarse;
-    const int64_t ws = 2 * int64_t(in->layers) * P.max_chunks * 4 + 1024;
+    const int64_t ws = 2 * int64_t(in->layers) * P.max_chunks * 4 + int64_t(in->layers) * 4 + 1024;
     rc = ws2_require(ctx, ws);
     if (rc) return rc;
     WsCarver carve(ctx->ws2);
     P.chunk_cnt = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
     P.chunk_prefix = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
+    P.layer_bad = carve.take<int32_t>(in->layers);
     dim3 grid((P.max_chunks + kWarpsPerCta - 1) / kWarpsPerCta, in->layers);
     EPK_PROF(ctx, "compact_count");
     EPK_CUDA_CHECK(launch_pdl(compact_count_kernel, grid, dim3(32 * kWarpsPerCta), 0, ctx->stream, P));

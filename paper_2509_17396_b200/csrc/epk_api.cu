@@ -116,7 +116,6 @@ int launch_select(epk_ctx*, const epk_cache_desc*, const void*, int, const int64
 int launch_compact(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*, int, const uint32_t*,
                    const uint64_t*, uint32_t*, uint32_t*);
 int launch_select_threshold(epk_ctx*, const epk_cache_desc*, const FusedSelect*, const int64_t*, uint64_t*, int32_t*);
-bool step_fused_supported(const epk_cache_desc*, int, int, int);
 int launch_step_tc_grouped(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const void*, const void*, int, int,
                            int, const int64_t*, int, cudaStream_t, cudaEvent_t, int, float*, uint8_t*,
                            const FusedSelect&, uint64_t*, int32_t*,
@@ -125,9 +124,6 @@ int launch_step_tc_grouped(epk_ctx*, const epk_cache_desc*, const epk_cache_desc
                            int (*)(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*, int,
                                    const uint32_t*, const uint64_t*, uint32_t*, uint32_t*),
                            epk_cache_desc (*)(const epk_cache_desc*, int, int));
-int launch_step_fused(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const void*, const void*, int, int,
-                      const int64_t*, int, int64_t, int, float*, uint32_t*, uint32_t*, uint32_t*, uint8_t*, uint64_t*,
-                      int32_t*);
 int launch_append(epk_ctx*, const epk_cache_desc*, const void*, const void*, const int32_t*, int);
 int launch_score_f32(epk_ctx*, const epk_cache_desc*, const float*, const float*, int, int, int, int64_t, float*);
 int launch_score_tc(epk_ctx*, const epk_cache_desc*, const void*, const void*, int, int, int, int64_t, float*,
@@ -388,11 +384,17 @@ int epk_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* ou
 
 int epk_append(epk_ctx* ctx, const epk_cache_desc* c, const void* k_new, const void* v_new, const int32_t* positions,
                int32_t len, int32_t slack) {
-    (void)slack;
     int rc = check_ctx(ctx);
     if (rc) return rc;
     if ((rc = check_cache(c))) return rc;
     if (!k_new || !v_new || !positions) return fail(EPK_ERR_ARG, "append: null pointer");
+    if (slack < 0) return fail(EPK_ERR_ARG, "append: negative slack");
+    // slack > 0: the gap the caller left after every head (epk_compact's
+    // out_slack); a block longer than it can never fit.  The device checks
+    // every head's actual gap either way (deferred EPK_ERR_ARG).
+    if (slack > 0 && len > slack)
+        return fail(EPK_ERR_ARG, "append: block of " + std::to_string(len) + " rows exceeds the slack of " +
+                                     std::to_string(slack) + " rows per head");
     return launch_append(ctx, c, k_new, v_new, positions, len);
 }
 
@@ -405,9 +407,6 @@ int epk_ctx_set_option(epk_ctx* ctx, int32_t option, int64_t value) {
             return EPK_OK;
         case EPK_OPT_OVERLAP:
             ctx->overlap = value != 0;
-            return EPK_OK;
-        case EPK_OPT_FUSED:
-            ctx->fused = value != 0;
             return EPK_OK;
         default:
             return fail(EPK_ERR_ARG, "unknown option");
@@ -473,17 +472,6 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     uint32_t* hist_f = reinterpret_cast<uint32_t*>(sb);
     uint32_t* hist_c = reinterpret_cast<uint32_t*>(sb + o_hc);
     uint64_t* thr = reinterpret_cast<uint64_t*>(sb + o_thr);
-
-    // The fused step (step.cu): one persistent kernel scores, selects and
-    // compacts all layers with compaction overlapping later layers' scoring.
-    if (mode == EPK_SCORE_TC_BF16 && ctx->fused && step_fused_supported(in, q_heads, prompt_len, n_pins)) {
-        if (aggregation != EPK_AGG_MAX && aggregation != EPK_AGG_AVG) return fail(EPK_ERR_ARG, "bad aggregation");
-        if (!q || !kp) return fail(EPK_ERR_ARG, "evict_step: null prompt");
-        return launch_step_fused(ctx, in, out, q, kp, q_heads, prompt_len, budgets, aggregation == EPK_AGG_MAX, n_max,
-                                 out_slack, scores, keys, reinterpret_cast<uint32_t*>(sb),
-                                 reinterpret_cast<uint32_t*>(sb + o_hc), keep, reinterpret_cast<uint64_t*>(sb + o_thr),
-                                 kept);
-    }
 
     // Layer groups (EPK_OPT_LAYER_GROUP): 0 = auto = all layers in one group.
     // Smaller groups let a group's select+compact (side stream) overlap the

@@ -32,7 +32,6 @@ struct epk_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int layer_group = 0;  // layers per group in epk_evict_step (0 = auto: group K fits in L2)
     int overlap = 1;      // run each group's compaction on `side`
-    int fused = 0;        // EPK_OPT_FUSED: single-kernel step (step.cu) where supported
     void* step_buf = nullptr;  // epk_evict_step scores + keep mask
     int64_t step_bytes = 0;
     int* err_flag = nullptr;  // deferred device-side error code (device int)
@@ -115,6 +114,9 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+
+// Per-device host state (function attributes) is kept for ordinals < kMaxDevices.
+constexpr int kMaxDevices = 64;
 
 // Layer table passed by value to kernels (host layer_base copied in).
 constexpr int kMaxLayers = 128;

@@ -62,6 +62,7 @@ struct F32Params {
     float* scores;       // global
     int agg_max;
     float scale;
+    int* err_flag;  // a head longer than n_max: EPK_ERR_ARG, the head is not scored
 };
 
 constexpr int kT = 64;    // tile rows/cols
@@ -74,6 +75,10 @@ __global__ void __launch_bounds__(256) f32_logits_kernel(const __grid_constant__
     const int t0 = blockIdx.y * kT;
     const int64_t j0 = int64_t(blockIdx.x) * kT;
     const int n_h = P.len[h];
+    if (n_h > P.n_max) {  // the scratch stride is n_max + p: refuse rather than overrun
+        if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) atomicCAS(P.err_flag, 0, EPK_ERR_ARG);
+        return;
+    }
     const int64_t cols = int64_t(n_h) + P.p;
     if (j0 >= cols || t0 >= P.p) return;
     __shared__ float sq[kT][kDc + 1];
@@ -132,6 +137,7 @@ __global__ void __launch_bounds__(256) f32_rowstat_kernel(const __grid_constant_
     const int row = blockIdx.x;
     const int qh = row / P.p, t = row % P.p;
     const int h = qh / P.G;
+    if (P.len[h] > P.n_max) return;  // flagged by the logits kernel
     const int64_t visible = int64_t(P.len[h]) + t + 1;
     const int64_t stride = P.n_max + P.p;
     float* lg = P.logits + int64_t(row) * stride;
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(256) f32_colscore_kernel(const __grid_constant
     const int h = blockIdx.y;
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int n_h = P.len[h];
-    if (j >= n_h) return;
+    if (j >= n_h || n_h > P.n_max) return;
     const int64_t stride = P.n_max + P.p;
     float best = -__int_as_float(0x7f800000);
     for (int g = 0; g < P.G; ++g) {
@@ -218,6 +224,7 @@ int launch_score_f32(epk_ctx* ctx, const epk_cache_desc* c, const float* q, cons
     P.scores = scores;
     P.agg_max = agg_max;
     P.scale = float(1.0 / std::sqrt(double(d)));
+    P.err_flag = ctx->err_flag;
     const int64_t nchunks = (stride + 63) / 64;
     const size_t rs_smem = size_t(2 * nchunks) * 4;
     if (rs_smem > 200 * 1024) return fail(EPK_ERR_UNSUPPORTED, "score(exact f32): context too long for one CTA row");

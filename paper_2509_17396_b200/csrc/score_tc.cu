@@ -50,6 +50,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "tc_common.cuh"
@@ -759,25 +760,35 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     int poly = 0;
     if (const char* e = std::getenv("EPK_TC_POLY")) poly = std::max(0, std::min(3, std::atoi(e)));
     // Dynamic shared memory limit: the per-block opt-in maximum minus the
-    // kernels' static shared memory.
-    static int limit = 0;
-    if (!limit) {
-        int optin = 0;
-        EPK_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-        size_t stat = 0;
-        for (KernelFn f : stats_fns) {
-            cudaFuncAttributes fa;
-            EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f)));
-            stat = std::max(stat, fa.sharedSizeBytes);
+    // kernels' static shared memory.  Function attributes are per device, so
+    // the opt-in is made once per device (contexts of several GPUs may share
+    // a process and call from several threads).
+    static std::mutex attr_mu;
+    static int dev_limit[kMaxDevices] = {};
+    if (ctx->device < 0 || ctx->device >= kMaxDevices) return fail(EPK_ERR_UNSUPPORTED, "device ordinal too large");
+    int limit = 0;
+    {
+        std::lock_guard<std::mutex> attr_lock(attr_mu);
+        if (!dev_limit[ctx->device]) {
+            int optin = 0;
+            EPK_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+            size_t stat = 0;
+            for (KernelFn f : stats_fns) {
+                cudaFuncAttributes fa;
+                EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f)));
+                stat = std::max(stat, fa.sharedSizeBytes);
+            }
+            cudaFuncAttributes fa1;
+            EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa1, reinterpret_cast<const void*>(score_fn)));
+            const int lim = optin - int(std::max(stat, fa1.sharedSizeBytes));
+            for (KernelFn f : stats_fns)
+                EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+            EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(score_fn),
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+            dev_limit[ctx->device] = lim;  // only once every attribute is set
         }
-        cudaFuncAttributes fa1;
-        EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa1, reinterpret_cast<const void*>(score_fn)));
-        limit = optin - int(std::max(stat, fa1.sharedSizeBytes));
-        for (KernelFn f : stats_fns)
-            EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
-        EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(score_fn),
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+        limit = dev_limit[ctx->device];
     }
     // Shared-memory budget: leave ~30 KB of the SM for co-resident side-stream
     // kernels (EPK_TC_SMEM_KB overrides, for experiments).

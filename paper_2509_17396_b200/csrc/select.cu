@@ -641,7 +641,10 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
     };
     uint32_t kb = 0;
     int64_t k_rem = limit, eq = 0;
-    const bool select = n_live > limit;
+    // budget 0 keeps nothing (evict_to_budget with no pins, kvcache.hpp:180-190):
+    // no threshold bin exists, the resolve below emits the "none" flag
+    const bool none = n_live > limit && limit == 0;
+    const bool select = n_live > limit && !none;
     if (select) {
         // threshold bin: coarse then fine histogram, bins in key order
         for (int i = tid; i < 256; i += kTSThreads) S.tot[i] = __ldcg(P.hist_coarse + l * 256 + 255 - i);
@@ -695,7 +698,10 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
     __syncthreads();
     if (!S.last) return;
     __threadfence();
+    // thr[2l] bit 32: keep every live row; bit 33: keep none; else the exact
+    // threshold key T in the low word and the (position << 8 | head) tiebreak U
     uint64_t t0 = uint64_t(1) << 32, t1 = ~uint64_t(0);  // keep every live row
+    if (none) t0 = uint64_t(2) << 32;
     if (select) {
         const unsigned n = __ldcg(P.cand_n + l);
         const bool listed = int64_t(n) == eq && n <= unsigned(kTSCand);

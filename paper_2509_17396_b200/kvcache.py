@@ -174,14 +174,16 @@ def compact(cache: EpisodeCache, keep: torch.Tensor, out: EpisodeCache, slack: i
 
 
 def append_to_cache(cache: EpisodeCache, k_new: torch.Tensor, v_new: torch.Tensor, positions: torch.Tensor,
-                    ctx: Context | None = None) -> None:
-    """append_to_cache (toymodel.hpp:428-443): k_new/v_new [layers, H, len, d]."""
+                    slack: int = 0, ctx: Context | None = None) -> None:
+    """append_to_cache (toymodel.hpp:428-443): k_new/v_new [layers, H, len, d].
+    `slack` (> 0) is the gap the caller left after every head; a longer block
+    is refused at once."""
     ctx = ctx or default_context(cache.device.index)
     if k_new.shape[:2] != (cache.layers, cache.kv_heads) or k_new.shape[3] != cache.head_dim:
         raise DimensionError("append_to_cache: block shape mismatch")
     d = cache.desc()
     _lib.call("epk_append", ctx.handle, C.byref(d), ptr(k_new.contiguous()), ptr(v_new.contiguous()),
-              ptr(positions.to(torch.int32).contiguous()), int(k_new.shape[2]), 0)
+              ptr(positions.to(torch.int32).contiguous()), int(k_new.shape[2]), int(slack))
 
 
 def evict_device(cache: EpisodeCache, scores: torch.Tensor, layer_budgets, pinned=None,

@@ -68,3 +68,26 @@ def test_expf_contract(orc):
     assert np.max(np.abs(y.view(np.int32).astype(np.int64) - cr.view(np.int32))) <= 1
     assert orc.expf(np.array([0.0], np.float32))[0] == 1.0
     assert orc.expf(np.array([-104.0], np.float32))[0] == 0.0
+
+
+def test_threaded_scorers_equal_single_threaded(orc, g):
+    """The multi-threaded restatements (used by the benchmark-scale GPU parity
+    tests) give the single-threaded bits: golden fp64 fixtures, ragged heads,
+    p not a multiple of 4, both aggregations, fp64 and EPK-F32."""
+    for i in range(int(g["sc_count"])):
+        for agg in (1, 0):
+            s = orc.score_layer_f64_mt(g[f"sc{i}_q"], g[f"sc{i}_k"], g[f"sc{i}_kp"], g[f"sc{i}_head_off"], bool(agg),
+                                       threads=3)
+            assert np.array_equal(s, g[f"sc{i}_{agg}_scores"]), (i, agg)
+    rng = np.random.default_rng(5)
+    for hq, hkv, p, counts in ((6, 2, 7, [33, 0]), (8, 4, 5, [10, 70, 1, 64]), (3, 3, 1, [5, 6, 7])):
+        ho = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        q = rng.standard_normal((hq, p, 16))
+        k = rng.standard_normal((int(ho[-1]), 16))
+        kp = rng.standard_normal((hkv, p, 16))
+        for agg in (True, False):
+            assert np.array_equal(orc.score_layer_f64_mt(q, k, kp, ho, agg, threads=4),
+                                  orc.score_layer_f64(q, k, kp, ho, agg))
+            q32, k32, kp32 = q.astype(np.float32), k.astype(np.float32), kp.astype(np.float32)
+            assert np.array_equal(orc.score_layer_f32_mt(q32, k32, kp32, ho, agg, threads=2).view(np.uint32),
+                                  orc.score_layer_f32(q32, k32, kp32, ho, agg).view(np.uint32))

@@ -1,0 +1,284 @@
+"""Parity at the benchmarked configurations (BASELINE.json configs), against
+the CPU oracle -- not GPU against GPU.
+
+* cfg2 layer (8 x 10,240 live, G = 3, p = 128, M = 8,192):
+    - bf16 tensor-core scores within 1e-4 relative of the fp64 restatement
+      (oracle.score_layer_f64_mt, pinned to the compiled reference by
+      tests/test_oracle_vs_ref.py and tests/test_golden.py); retained-set
+      recall and Jaccard (harness.hpp:266-291) >= 0.999 on identical state;
+    - fp32 parity scorer bit-exact with the EPK-F32 restatement and within
+      1e-5 relative of fp64 (north_star).
+* the DEFAULT block step (epk_evict_step: tensor-core scores with fused
+  histograms -> threshold select -> count/plan/gather) at the full cfg2 size
+  (28 layers) with tie stress -- 1 % of K rows duplicated within heads and
+  across heads (same position, identical query groups), plus a layer whose
+  keys come from a 7-row pool so the threshold falls inside a tie -- must be
+  bit-exact with the reference's own evict_to_budget (kvcache.hpp:142-201,
+  oracle/_ref) on the step's own scores: retained positions per head, per-head
+  counts and the compacted K/V rows.
+* cfg4 layer (G = 4) and cfg5 layer (Qwen2.5-7B: H = 4, G = 7, n_h = 178,858,
+  the 1M-token / 6x-compression steady state) vs fp64.
+* cfg1 full episode (16K context, block 512, M = 2,048, p = 64, 32 blocks):
+  the fp32 path bit-exact with the oracle chain at every block; the bf16 path
+  >= 99.9 % recall per block on teacher-forced (identical) state, and its
+  free-running chained Jaccard / recall reported.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import bf16_round
+
+pytestmark = pytest.mark.gpu
+
+SCORE_RTOL_TC = 1e-4   # bf16 products are exact in fp32; fp32 accumulation + ex2/lg2.approx
+SCORE_RTOL_F32 = 1e-5  # north_star
+OVERLAP_MIN = 0.999    # north_star
+
+
+def _layer(rng, Hq, H, p, n_h, d=128):
+    ho = (np.arange(H + 1) * n_h).astype(np.int64)
+    pos = np.tile(np.sort(rng.choice(8 * n_h, n_h, replace=False)), H).astype(np.int64)
+    k = bf16_round(rng.standard_normal((H * n_h, d)).astype(np.float32))
+    v = bf16_round(rng.standard_normal((H * n_h, d)).astype(np.float32))
+    q = bf16_round(rng.standard_normal((Hq, p, d)).astype(np.float32))
+    kp = bf16_round(rng.standard_normal((H, p, d)).astype(np.float32))
+    return ho, pos, k, v, q, kp
+
+
+def _score_gpu(gpu, ho, pos, k, v, q, kp, mode, agg="max"):
+    dt = torch.bfloat16 if mode == "tc_bf16" else torch.float32
+    H = len(ho) - 1
+    c = gpu.EpisodeCache(1, H, k.shape[1], [int(ho[-1])], dt, "cuda")
+    c.load_layers([(np.diff(ho), pos, k, v)])
+    sc = gpu.score_with_prompt(c, torch.as_tensor(q[None], device="cuda").to(dt),
+                               torch.as_tensor(kp[None], device="cuda").to(dt), agg, mode=mode)
+    torch.cuda.synchronize()
+    return sc[: int(ho[-1])].cpu().numpy()
+
+
+def _overlap(orc, ho, pos, ref_scores, got_scores, M):
+    _, a = orc.evict_layer(ho, pos, ref_scores.astype(np.float64), M)
+    _, b = orc.evict_layer(ho, pos, got_scores.astype(np.float64), M)
+    inter = np.logical_and(a, b).sum()
+    return inter / a.sum(), inter / np.logical_or(a, b).sum()
+
+
+@pytest.mark.timeout(600)
+def test_cfg2_layer_vs_cpu_fp64(gpu, orc):
+    rng = np.random.default_rng(2)
+    ho, pos, k, v, q, kp = _layer(rng, 24, 8, 128, 10240)
+    ref64 = orc.score_layer_f64_mt(q.astype(np.float64), k.astype(np.float64), kp.astype(np.float64), ho, True)
+    tc = _score_gpu(gpu, ho, pos, k, v, q, kp, "tc_bf16")
+    rel = np.abs(tc.astype(np.float64) - ref64) / ref64
+    recall, jac = _overlap(orc, ho, pos, ref64, tc, 8192)
+    print(f"cfg2 layer bf16 tc vs fp64: max rel {rel.max():.3e}, recall {recall:.6f}, Jaccard {jac:.6f}")
+    assert rel.max() < SCORE_RTOL_TC
+    assert recall >= OVERLAP_MIN and jac >= OVERLAP_MIN
+    # the fp32 parity path on the same layer: bitwise vs EPK-F32, 1e-5 vs fp64
+    f32 = _score_gpu(gpu, ho, pos, k, v, q, kp, "exact_f32")
+    mirror = orc.score_layer_f32_mt(q, k, kp, ho, True)
+    assert np.array_equal(f32.view(np.uint32), mirror.view(np.uint32))
+    rel32 = np.abs(f32.astype(np.float64) - ref64) / ref64
+    print(f"cfg2 layer fp32 vs fp64: max rel {rel32.max():.3e}")
+    assert rel32.max() < SCORE_RTOL_F32
+
+
+@pytest.mark.timeout(600)
+def test_cfg4_layer_vs_cpu_fp64(gpu, orc):
+    """Llama-3.1-8B grouping: 32 query heads on 8 kv heads (G = 4, four
+    query chunks per head in P1/P2)."""
+    rng = np.random.default_rng(4)
+    ho, pos, k, v, q, kp = _layer(rng, 32, 8, 128, 10240)
+    ref64 = orc.score_layer_f64_mt(q.astype(np.float64), k.astype(np.float64), kp.astype(np.float64), ho, True)
+    for agg in ("max", "avg"):
+        if agg == "avg":
+            ref64 = orc.score_layer_f64_mt(q.astype(np.float64), k.astype(np.float64), kp.astype(np.float64), ho,
+                                           False)
+        tc = _score_gpu(gpu, ho, pos, k, v, q, kp, "tc_bf16", agg)
+        rel = np.abs(tc.astype(np.float64) - ref64) / ref64
+        recall, jac = _overlap(orc, ho, pos, ref64, tc, 8192)
+        print(f"cfg4 layer ({agg}) bf16 tc vs fp64: max rel {rel.max():.3e}, recall {recall:.6f}, Jaccard {jac:.6f}")
+        assert rel.max() < SCORE_RTOL_TC
+        assert recall >= OVERLAP_MIN
+
+
+@pytest.mark.timeout(900)
+def test_cfg5_layer_vs_cpu_fp64(gpu, orc):
+    """Qwen2.5-7B, 1M tokens, block 4,096, M = N/6 = 174,762 per head: one
+    steady-state layer of 4 heads x 178,858 live entries, G = 7.  P1
+    accumulates each row's denominator over ~179K columns (SURVEY 7 hard
+    part 3: a sequential fp32 sum drifts to 1.5e-5 here)."""
+    rng = np.random.default_rng(5)
+    n_h = 174762 + 4096
+    ho, pos, k, v, q, kp = _layer(rng, 28, 4, 128, n_h)
+    ref64 = orc.score_layer_f64_mt(q.astype(np.float64), k.astype(np.float64), kp.astype(np.float64), ho, True)
+    tc = _score_gpu(gpu, ho, pos, k, v, q, kp, "tc_bf16")
+    rel = np.abs(tc.astype(np.float64) - ref64) / ref64
+    recall, jac = _overlap(orc, ho, pos, ref64, tc, 174762)
+    print(f"cfg5 layer bf16 tc vs fp64: max rel {rel.max():.3e}, recall {recall:.6f}, Jaccard {jac:.6f}")
+    assert rel.max() < SCORE_RTOL_TC
+    assert recall >= OVERLAP_MIN and jac >= OVERLAP_MIN
+
+
+def _tie_stressed_cfg2(seed):
+    """28 steady-state cfg2 layers on the device with tie stress."""
+    L, Hq, H, d, p, n_h = 28, 24, 8, 128, 128, 10240
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    rows = H * n_h
+    k = torch.randn(L, rows, d, device="cuda", generator=g).bfloat16()
+    v = torch.randn(L, rows, d, device="cuda", generator=g).bfloat16()
+    q = torch.randn(L, Hq, p, d, device="cuda", generator=g).bfloat16()
+    kp = torch.randn(L, H, p, d, device="cuda", generator=g).bfloat16()
+    ndup = rows // 100
+    G = Hq // H
+    for l in range(L):
+        # within a head: row dst takes row src's key (same head -> same query group)
+        src = torch.randint(0, rows, (ndup,), device="cuda", generator=g)
+        dst = (src // n_h) * n_h + torch.randint(0, n_h, (ndup,), device="cuda", generator=g)
+        k[l, dst] = k[l, src]
+        if l % 2 == 0:
+            # across heads: heads 0 and 1 see the same query group, and 1 % of
+            # head 1's rows copy head 0's key at the SAME position -> equal
+            # (score, position), resolved by the head
+            q[l, G:2 * G] = q[l, 0:G]
+            r = torch.randint(0, n_h, (ndup,), device="cuda", generator=g)
+            k[l, n_h + r] = k[l, r]
+    # a layer whose keys come from a 7-row pool per head: the threshold lands
+    # inside a tie whatever the scores are
+    pool = torch.randint(0, 7, (rows,), device="cuda", generator=g)
+    k[5] = k[5].view(H, n_h, d)[torch.arange(H, device="cuda")[:, None], pool.view(H, n_h)].reshape(rows, d)
+    return L, Hq, H, d, p, n_h, k, v, q, kp
+
+
+@pytest.mark.timeout(600)
+def test_default_step_cfg2_tie_stress_bitexact_vs_reference(gpu, orc):
+    from paper_2509_17396_b200.step import evict_step
+    L, Hq, H, d, p, n_h, k, v, q, kp = _tie_stressed_cfg2(17)
+    M, slack = 8192, 2048
+    cin = gpu.EpisodeCache(L, H, d, [H * n_h] * L, torch.bfloat16, "cuda")
+    cin.k.copy_(k.view(-1, d))
+    cin.v.copy_(v.view(-1, d))
+    pos_h = torch.sort(torch.randperm(131072, device="cuda")[:n_h])[0].to(torch.int32)
+    cin.pos.copy_(pos_h.repeat(L * H))
+    cin.head_off.copy_((torch.arange(H + 1, device="cuda", dtype=torch.int32) * n_h).repeat(L, 1))
+    cin.head_len.fill_(n_h)
+    cout = gpu.EpisodeCache(L, H, d, [H * (M + slack)] * L, torch.bfloat16, "cuda")
+    scores = torch.zeros(cin.rows, dtype=torch.float32, device="cuda")
+    kept = torch.zeros(L, dtype=torch.int32, device="cuda")
+    evict_step(cin, cout, q, kp, [M] * L, mode="tc_bf16", slack=slack, n_max_per_head=n_h, scores=scores,
+               kept_per_layer=kept)
+    torch.cuda.synchronize()
+    gpu.default_context(0).poll_error()
+    assert kept.cpu().tolist() == [H * M] * L
+    use_ref = orc.ref_available()
+    ties_at_threshold = 0
+    out_off, out_len = cout.head_off.cpu().numpy(), cout.head_len.cpu().numpy()
+    out_pos = cout.pos.cpu().numpy()
+    ho = (np.arange(H + 1) * n_h).astype(np.int64)
+    for l in range(L):
+        b = int(cin.layer_base[l])
+        s = scores[b:b + H * n_h].double().cpu().numpy()
+        pos = cin.pos[b:b + H * n_h].cpu().numpy().astype(np.int64)
+        if use_ref:
+            keep, counts, _ = orc.ref_evict_layer(ho, pos, s, M)
+        else:
+            _, keep = orc.evict_layer(ho, pos, s, M)
+            counts = np.array([keep[ho[h]:ho[h + 1]].sum() for h in range(H)])
+        kth = np.sort(s)[::-1][H * M - 1]
+        ties_at_threshold += int((s == kth).sum() > 1)
+        exp_pos = [pos[ho[h]:ho[h + 1]][keep[ho[h]:ho[h + 1]]].tolist() for h in range(H)]
+        assert out_len[l].tolist() == [int(c) for c in counts], l
+        ob = int(cout.layer_base[l])
+        assert [out_pos[ob + out_off[l, h]:ob + out_off[l, h] + out_len[l, h]].tolist() for h in range(H)] == exp_pos, l
+        src = torch.as_tensor(np.nonzero(keep)[0] + b, device="cuda")
+        dst = cout.live_rows(l)
+        assert torch.equal(cout.k[dst].view(torch.int16), cin.k[src].view(torch.int16)), l
+        assert torch.equal(cout.v[dst].view(torch.int16), cin.v[src].view(torch.int16)), l
+    print(f"tie-stressed cfg2 step: {ties_at_threshold} of {L} layers had a tie at the threshold score "
+          f"(checked against {'oracle/_ref evict_to_budget' if use_ref else 'the oracle restatement'})")
+    assert ties_at_threshold >= 1
+
+
+class _Cfg1Provider:
+    def __init__(self, dtype, seed=1):
+        g = torch.Generator().manual_seed(seed)
+        self.L, self.Hq, self.H, self.d, self.n, self.p = 1, 24, 8, 128, 16384, 64
+        self.k = torch.randn(1, 8, self.n, 128, generator=g).to(dtype)
+        self.v = torch.randn(1, 8, self.n, 128, generator=g).to(dtype)
+        self.q = torch.randn(1, 24, 64, 128, generator=g).to(dtype)
+        self.kp = torch.randn(1, 8, 64, 128, generator=g).to(dtype)
+
+    def block_kv(self, start, length):
+        sl = slice(start, start + length)
+        return (self.k[:, :, sl].cuda(), self.v[:, :, sl].cuda(),
+                torch.arange(start, start + length, dtype=torch.int32).cuda())
+
+    def prompt(self, episode_id, block_index):
+        return self.q.cuda(), self.kp.cuda()
+
+
+def _oracle_chain(orc, prov, M, B, score_fn, per_step=None):
+    """The oracle's block loop on its own decisions (append -> score -> evict)."""
+    H = prov.H
+    k = prov.k[0].double().numpy() if score_fn is orc.score_layer_f64_mt else prov.k[0].numpy()
+    q, kp = (prov.q[0].double().numpy(), prov.kp[0].double().numpy()) if score_fn is orc.score_layer_f64_mt else \
+        (prov.q[0].numpy(), prov.kp[0].numpy())
+    state = [np.zeros(0, np.int64) for _ in range(H)]
+    for step, start in enumerate(range(0, prov.n, B)):
+        state = [np.concatenate([s, np.arange(start, min(prov.n, start + B))]) for s in state]
+        ho = np.concatenate([[0], np.cumsum([len(s) for s in state])]).astype(np.int64)
+        pos = np.concatenate(state)
+        kk = np.concatenate([k[h, state[h]] for h in range(H)])
+        sc = score_fn(q, kk, kp, ho, True)
+        st, keep = orc.evict_layer(ho, pos, sc.astype(np.float64), M)
+        assert st >= 0
+        if per_step is not None:
+            per_step(step, state, ho, pos, sc, keep)
+        state = [pos[ho[h]:ho[h + 1]][keep[ho[h]:ho[h + 1]]] for h in range(H)]
+    return state
+
+
+@pytest.mark.timeout(900)
+def test_cfg1_full_episode_fp32_bitexact(gpu, orc):
+    M, B = 2048, 512
+    prov = _Cfg1Provider(torch.float32)
+    rep = gpu.block_prefill(prov, 1, 24, 8, 128, prov.n, gpu.BlockPrefillConfig(M, B, mode="exact_f32"),
+                            dtype=torch.float32)
+    assert rep.blocks_processed == 32
+    state = _oracle_chain(orc, prov, M, B, orc.score_layer_f32_mt)
+    assert rep.cache.retained_positions()[0] == [s.tolist() for s in state]
+    # compacted keys are the provider's rows at the retained positions
+    rows = rep.cache.live_rows(0)
+    exp_k = torch.cat([prov.k[0, h, torch.as_tensor(state[h])] for h in range(8)])
+    assert torch.equal(rep.cache.k[rows].cpu().view(torch.int32), exp_k.view(torch.int32))
+
+
+@pytest.mark.timeout(900)
+def test_cfg1_full_episode_bf16_teacher_forced_and_chained(gpu, orc):
+    M, B = 2048, 512
+    prov = _Cfg1Provider(torch.bfloat16)
+    k32 = prov.k[0].float().numpy()
+    q32, kp32 = prov.q[0].float().numpy(), prov.kp[0].float().numpy()
+    worst = [1.0]
+
+    def teacher_forced(step, state, ho, pos, sc64, keep64):
+        if ho[-1] <= 8 * M:
+            return  # under budget: everything kept by both
+        kk = np.concatenate([k32[h, state[h]] for h in range(8)])
+        tc = _score_gpu(gpu, ho, pos, kk, kk, q32, kp32, "tc_bf16")
+        _, keep_tc = orc.evict_layer(ho, pos, tc.astype(np.float64), M)
+        worst[0] = min(worst[0], np.logical_and(keep64, keep_tc).sum() / keep64.sum())
+
+    state = _oracle_chain(orc, prov, M, B, orc.score_layer_f64_mt, teacher_forced)
+    print(f"cfg1 bf16 per-block recall on identical state: min {worst[0]:.6f} over 32 blocks")
+    assert worst[0] >= OVERLAP_MIN
+    rep = gpu.block_prefill(prov, 1, 24, 8, 128, prov.n, gpu.BlockPrefillConfig(M, B, mode="tc_bf16"),
+                            dtype=torch.bfloat16)
+    got = rep.cache.retained_positions()[0]
+    a = {(h, x) for h in range(8) for x in got[h]}
+    b = {(h, int(x)) for h in range(8) for x in state[h]}
+    jac, rec = len(a & b) / len(a | b), len(a & b) / len(b)
+    print(f"cfg1 bf16 chained over 32 blocks vs the fp64 oracle chain: Jaccard {jac:.4f}, recall {rec:.4f}")
+    assert len(a) == len(b) == 8 * M
+    assert rec >= 0.98
