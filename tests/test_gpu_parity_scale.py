@@ -10,8 +10,9 @@ the CPU oracle -- not GPU against GPU.
       1e-5 relative of fp64 (north_star).
 * the DEFAULT block step (epk_evict_step: tensor-core scores with fused
   histograms -> threshold select -> count/plan/gather) at the full cfg2 size
-  (28 layers) with tie stress -- 1 % of K rows duplicated within heads and
-  across heads (same position, identical query groups), plus a layer whose
+  (28 layers) with tie stress -- 1 % of K rows duplicated within heads, whole
+  heads duplicated across heads (same positions, identical query groups, so
+  equal (score, position) pairs resolved by the head), plus a layer whose
   keys come from a 7-row pool so the threshold falls inside a tie -- must be
   bit-exact with the reference's own evict_to_budget (kvcache.hpp:142-201,
   oracle/_ref) on the step's own scores: retained positions per head, per-head
@@ -137,13 +138,14 @@ def _tie_stressed_cfg2(seed):
         src = torch.randint(0, rows, (ndup,), device="cuda", generator=g)
         dst = (src // n_h) * n_h + torch.randint(0, n_h, (ndup,), device="cuda", generator=g)
         k[l, dst] = k[l, src]
-        if l % 2 == 0:
-            # across heads: heads 0 and 1 see the same query group, and 1 % of
-            # head 1's rows copy head 0's key at the SAME position -> equal
-            # (score, position), resolved by the head
+        if l % 4 == 0:
+            # across heads: head 1 is a copy of head 0 (keys, prompt keys and
+            # query group; positions are shared), so every head-1 row ties
+            # with the head-0 row at the SAME position on (score, position)
+            # and only the head breaks the tie
             q[l, G:2 * G] = q[l, 0:G]
-            r = torch.randint(0, n_h, (ndup,), device="cuda", generator=g)
-            k[l, n_h + r] = k[l, r]
+            kp[l, 1] = kp[l, 0]
+            k[l, n_h:2 * n_h] = k[l, 0:n_h]
     # a layer whose keys come from a 7-row pool per head: the threshold lands
     # inside a tie whatever the scores are
     pool = torch.randint(0, 7, (rows,), device="cuda", generator=g)
