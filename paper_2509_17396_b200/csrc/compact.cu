@@ -306,6 +306,16 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     P.chunk_prefix = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
     P.layer_bad = carve.take<int32_t>(in->layers);
     dim3 grid((P.max_chunks + kWarpsPerCta - 1) / kWarpsPerCta, in->layers);
+#ifdef EPK_COMPACT_CARVEOUT
+    // experiment: a shared-memory carveout matching the scorer's, so the
+    // compaction CTAs may share an SM with a resident scorer CTA
+    EPK_CUDA_CHECK(cudaFuncSetAttribute(compact_count_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        EPK_COMPACT_CARVEOUT));
+    EPK_CUDA_CHECK(cudaFuncSetAttribute(compact_plan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        EPK_COMPACT_CARVEOUT));
+    EPK_CUDA_CHECK(cudaFuncSetAttribute(compact_gather_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        EPK_COMPACT_CARVEOUT));
+#endif
     EPK_PROF(ctx, "compact_count");
     EPK_CUDA_CHECK(launch_pdl(compact_count_kernel, grid, dim3(32 * kWarpsPerCta), 0, ctx->stream, P));
     EPK_LAUNCH_CHECK(ctx);

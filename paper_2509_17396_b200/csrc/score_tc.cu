@@ -60,7 +60,10 @@ namespace epk {
 using namespace sm100;
 
 constexpr int kEpiWarps = 8;      // SCORE epilogue warps (two column halves)
-constexpr int kEpiWarpsStats = 12;  // STATS epilogue warps: three job groups of four
+#ifndef EPK_STATS_EPI_WARPS
+#define EPK_STATS_EPI_WARPS 12
+#endif
+constexpr int kEpiWarpsStats = EPK_STATS_EPI_WARPS;  // STATS epilogue warps: job groups of four
 constexpr int kStatGroups = kEpiWarpsStats / 4;
 // STATS TMEM slots (128 columns each): a multiple of the group count so every
 // slot belongs to ONE epilogue group, and STATS jobs go to the MMA warp of
