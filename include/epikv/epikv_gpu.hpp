@@ -25,6 +25,11 @@
 //   block_prefill        blockprefill.hpp:92  (the block loop: the toy-model
 //                                              forward stays on the host, scoring
 //                                              and eviction run on the GPU)
+//   build                episodic.hpp:108     (Phase A over several GPUs: one host
+//                                              thread + one epk_ctx per GPU, episodes
+//                                              round-robin; k-means optionally over
+//                                              embeddings sharded across the GPUs,
+//                                              NCCL ordered chain -- epk_kmeans_sharded)
 // allocate (allocation.hpp:120) is L host scalars and stays the reference's.
 //
 // Link: -L<repo>/paper_2509_17396_b200 -lepk -lcudart.  Needs the reference
@@ -35,13 +40,17 @@
 
 #include <cstdint>
 #include <cstring>
+#include <exception>
+#include <memory>
 #include <string>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
 #include "epikv/allocation.hpp"
 #include "epikv/blockprefill.hpp"
 #include "epikv/clustering.hpp"
+#include "epikv/episodic.hpp"
 #include "epikv/kvcache.hpp"
 #include "epikv/scoring.hpp"
 #include "epikv/toymodel.hpp"
@@ -440,6 +449,175 @@ inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> 
         ++report.blocks_processed;
     }
     return report;
+}
+
+/// kmeans (clustering.hpp:148) with the points split in index order over
+/// `devices` (one shard per entry; a device may repeat): the centroid sums run
+/// as an ordered chain over NCCL (epk_kmeans_sharded), so the result is
+/// bit-identical to the reference's single-threaded kmeans.
+inline KMeansResult kmeans_sharded(const std::vector<Vec>& points, std::size_t k, std::uint64_t seed,
+                                   const std::vector<int>& devices, std::size_t max_iters = 64) {
+    if (k < 1) throw Error("kmeans: cluster count must be >= 1");
+    if (points.size() < k)
+        throw Error("kmeans: fewer points (" + std::to_string(points.size()) + ") than clusters (" +
+                    std::to_string(k) + ")");
+    if (devices.empty()) throw Error("kmeans_sharded: no devices");
+    const std::size_t n = points.size(), dim = points[0].size(), S = devices.size();
+    struct Ctx {
+        epk_ctx* c = nullptr;
+        ~Ctx() {
+            if (c) epk_ctx_destroy(c);
+        }
+    };
+    std::vector<Ctx> ctxs(S);
+    std::vector<std::unique_ptr<detail::DBuf<double>>> bufs;
+    std::vector<epk_ctx*> handles(S);
+    std::vector<const double*> shard_ptrs(S);
+    std::vector<int64_t> ns(S);
+    int cur = 0;
+    detail::cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+    for (std::size_t s = 0; s < S; ++s) {
+        const std::size_t a = n * s / S, b = n * (s + 1) / S;
+        std::vector<double> flat;
+        flat.reserve((b - a) * dim);
+        for (std::size_t i = a; i < b; ++i) {
+            if (points[i].size() != dim) throw DimensionError("kmeans: points differ in dimension");
+            flat.insert(flat.end(), points[i].begin(), points[i].end());
+        }
+        detail::cuda_check(cudaSetDevice(devices[s]), "cudaSetDevice");
+        detail::check(epk_ctx_create(devices[s], nullptr, &ctxs[s].c));
+        bufs.push_back(std::make_unique<detail::DBuf<double>>(std::max<std::size_t>(flat.size(), 1)));
+        if (!flat.empty()) bufs.back()->upload(flat.data(), flat.size());
+        handles[s] = ctxs[s].c;
+        shard_ptrs[s] = bufs.back()->p;
+        ns[s] = int64_t(b - a);
+    }
+    detail::cuda_check(cudaSetDevice(cur), "cudaSetDevice");
+    std::vector<int64_t> assign(n);
+    std::vector<double> cent(k * dim), sse(std::max<std::size_t>(max_iters, 1));
+    int64_t iters = 0;
+    detail::check(epk_kmeans_sharded(handles.data(), int32_t(S), shard_ptrs.data(), ns.data(), int64_t(dim),
+                                     int64_t(k), seed, int64_t(max_iters), assign.data(), cent.data(), &iters,
+                                     sse.data()));
+    KMeansResult r;
+    r.assignments.assign(assign.begin(), assign.end());
+    r.centroids.resize(k);
+    for (std::size_t c = 0; c < k; ++c) r.centroids[c].assign(cent.begin() + c * dim, cent.begin() + (c + 1) * dim);
+    r.iterations = std::size_t(iters);
+    r.sse_per_iteration.assign(sse.begin(), sse.begin() + iters);
+    return r;
+}
+
+/// Where gpu::build runs: the GPUs the episodes are sharded over (one host
+/// thread and one epk_ctx each; a device listed twice gets two threads), and
+/// whether the A1 k-means also shards the segment embeddings over them.
+struct BuildDevices {
+    std::vector<int> devices;        // empty: every visible device
+    bool shard_embeddings = false;   // k-means via epk_kmeans_sharded (NCCL ordered chain)
+};
+
+/// build (episodic.hpp:108-199), Phase A on several GPUs.  A1 clusters the
+/// segment embeddings (gpu::kmeans or gpu::kmeans_sharded), A2 measures the
+/// sensitivity (gpu::measure_sensitivity) and allocates (the reference's
+/// allocate), A3 runs gpu::block_prefill once per episode with episodes
+/// assigned round-robin to the devices (episodes are independent,
+/// episodic.hpp:159-171; zero inter-GPU traffic) and persists each cache as it
+/// finishes, then writes the manifest.  Every file is byte-identical to the
+/// reference build's, whatever the device count (the multi-GPU analogue of
+/// test_episodic.cpp:289-302); config.parallel_episodes is implied by
+/// more than one device.
+inline BuildResult build(const Model& model, const ConversationHistory& history, std::size_t episode_count,
+                         std::size_t budget_per_head, double alpha, const Embedder& embedder,
+                         const std::string& store_dir, const EpisodicBuildConfig& config = {},
+                         const BuildDevices& where = {}) {
+    std::vector<int> devices = where.devices;
+    if (devices.empty()) {
+        int nd = 0;
+        detail::cuda_check(cudaGetDeviceCount(&nd), "cudaGetDeviceCount");
+        for (int d = 0; d < nd; ++d) devices.push_back(d);
+    }
+    if (devices.empty()) throw Error("build: no CUDA device");
+    const std::vector<Segment> segments = segment_history(history, config.w_embed);
+    if (episode_count > segments.size()) {
+        throw Error("build: more episodes (" + std::to_string(episode_count) + ") than segments (" +
+                    std::to_string(segments.size()) + ")");
+    }
+    // A1: segment, embed, cluster, pick medoids and prompts.
+    std::vector<Vec> embeddings;
+    embeddings.reserve(segments.size());
+    for (const Segment& s : segments) embeddings.push_back(embedder.embed(s.text));
+    const KMeansResult clusters =
+        where.shard_embeddings
+            ? gpu::kmeans_sharded(embeddings, episode_count, config.cluster_seed, devices, config.kmeans_max_iters)
+            : gpu::kmeans(embeddings, episode_count, config.cluster_seed, config.kmeans_max_iters);
+    EpisodeModel episodes = finalize_episodes(history, segments, embeddings, clusters.assignments,
+                                              config.prompt_window, model.config.vocab);
+    // A2: sensitivity and per-layer budgets.
+    BudgetAllocation allocation;
+    SensitivityProfile profile;
+    if (config.use_allocation) {
+        const std::size_t cal_budget = config.calibration_budget > 0 ? config.calibration_budget : budget_per_head;
+        const std::size_t cal_sink =
+            config.calibration_sink > 0 ? config.calibration_sink : std::min<std::size_t>(128, cal_budget / 2);
+        const std::size_t cal_len =
+            config.calibration_tokens > 0 ? config.calibration_tokens : std::max<std::size_t>(4 * cal_budget, 256);
+        const std::vector<TokenId> cal_tokens =
+            synthetic_calibration_tokens(cal_len, config.calibration_seed, model.config.vocab);
+        profile = gpu::measure_sensitivity(model, cal_tokens, cal_budget, cal_sink,
+                                           "synthetic:seed=" + std::to_string(config.calibration_seed) +
+                                               ",len=" + std::to_string(cal_len));
+        allocation = allocate(profile, budget_per_head, alpha);
+    } else {
+        allocation = uniform_allocation(model.config.layers, budget_per_head);
+        profile.sigma.assign(model.config.layers, 1.0);
+        profile.sensitivity.assign(model.config.layers, 0.0);
+        profile.input_id = "uniform";
+        profile.model_seed = model.config.seed;
+    }
+    // A3: episodes round-robin over the devices, one host thread (and, through
+    // detail::ctx(), one epk_ctx) per device entry.
+    const RenderedHistory rendered = render_history_tokens(history, model.config.vocab);
+    CacheStore store(store_dir);
+    BuildResult result;
+    result.reports.resize(episode_count);
+    const std::size_t G = std::min(devices.size(), std::max<std::size_t>(episode_count, 1));
+    std::vector<std::exception_ptr> errors(G);
+    auto worker = [&](std::size_t g) {
+        try {
+            detail::cuda_check(cudaSetDevice(devices[g]), "cudaSetDevice");
+            for (std::size_t e = g; e < episode_count; e += G) {
+                BlockPrefillConfig prefill;
+                prefill.budget_per_head = budget_per_head;
+                prefill.block_size = config.block_size;
+                prefill.scorer = ScorerKind::patched;
+                prefill.aggregation = config.aggregation;
+                prefill.allocation = allocation;
+                const PatchedPrompt prompt = episodes.prompts[e];
+                prefill.prompt_provider = [prompt](std::size_t, std::size_t) { return prompt; };
+                result.reports[e] = gpu::block_prefill(model, rendered.tokens, prefill, e);
+                store.save(result.reports[e].cache);
+            }
+        } catch (...) {
+            errors[g] = std::current_exception();
+        }
+    };
+    if (G == 1) {
+        worker(0);
+    } else {
+        std::vector<std::thread> threads;
+        for (std::size_t g = 0; g < G; ++g) threads.emplace_back(worker, g);
+        for (std::thread& t : threads) t.join();
+    }
+    for (const std::exception_ptr& e : errors)
+        if (e) std::rethrow_exception(e);
+    store.write_manifest(
+        epikv::detail::manifest_json(episodes, allocation, store, ScorerKind::patched, budget_per_head, embedder.dim()));
+    result.set.episodes = std::move(episodes);
+    result.set.allocation = std::move(allocation);
+    result.set.profile = std::move(profile);
+    result.set.store_dir = store_dir;
+    result.set.budget_per_head = budget_per_head;
+    return result;
 }
 
 }  // namespace gpu

@@ -25,7 +25,8 @@
  *   epk_append           append_to_cache (toymodel.hpp:428-443)
  *   epk_evict_step       one block step of block_prefill (blockprefill.hpp:157-226):
  *                        score -> per-layer evict, all layers
- *   epk_kmeans*          kmeans (clustering.hpp:148-260)
+ *   epk_kmeans*          kmeans (clustering.hpp:148-260); epk_kmeans_sharded: the same
+ *                        over embeddings sharded across GPUs (NCCL ordered chain)
  *   epk_key_cosine_sigma measure_sensitivity reduction (allocation.hpp:80-100)
  *   epk_score_keydiff    keydiff_scores (scoring.hpp:186-221), the KeyDiff baseline
  *   epk_serialize_epkv   persist (kvcache.hpp:281-317), the episodic cache store's writer
@@ -218,6 +219,21 @@ int epk_kmeans_sq_dist(epk_ctx* ctx, const double* points, int64_t n, int64_t di
 int epk_kmeans(epk_ctx* ctx, const double* points, int64_t n, int64_t dim, int64_t k,
                uint64_t seed, int64_t max_iters, int64_t* assign_out, double* centroids_out,
                int64_t* iterations_out, double* sse_out);
+
+/* The same k-means with the points sharded in index order over `nshards`
+ * contexts (one per GPU; a device may appear more than once): shard s holds
+ * points [sum of n_per_shard[<s], + n_per_shard[s]) as points[s] [dev of
+ * ctxs[s]] fp64 [n][dim].  The centroid sums run as an ordered chain (shard s
+ * adds its points in index order on top of shard s-1's sums) and the last
+ * shard broadcasts the centroids, so every result is bit-identical to
+ * epk_kmeans on the concatenated points.  Transport: NCCL ncclSend/ncclRecv +
+ * ncclBroadcast over ncclCommInitAll of the devices when they are distinct
+ * (libnccl.so.2 loaded at first use; EPK_ERR_UNSUPPORTED if absent), device
+ * copies when shards share a device.  Synchronous; replaces kmeans
+ * (clustering.hpp:148-260) for embeddings sharded across GPUs. */
+int epk_kmeans_sharded(epk_ctx* const* ctxs, int32_t nshards, const double* const* points,
+                       const int64_t* n_per_shard, int64_t dim, int64_t k, uint64_t seed, int64_t max_iters,
+                       int64_t* assign_out, double* centroids_out, int64_t* iterations_out, double* sse_out);
 
 /* ---- K6: KeyDiff baseline scorer ------------------------------------------ *
  * scores[layer_base[l] + r] = -cosine(key_r, mean key of r's (layer, head)),

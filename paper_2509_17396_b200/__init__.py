@@ -9,7 +9,7 @@ from .kvcache import (EpisodeCache, KVEntry, LayerCache, append_to_cache, compac
                       evict_to_budget, select_per_head, select_pooled)
 from .scoring import keydiff_scores, score_grids, score_with_prompt  # noqa: F401
 from .blockprefill import BlockPrefillConfig, PrefillReport, block_prefill  # noqa: F401
-from .clustering import KMeansResult, kmeans, kmeans_sharded  # noqa: F401
+from .clustering import KMeansResult, kmeans, kmeans_multi_device, kmeans_sharded  # noqa: F401
 from .allocation import (BudgetAllocation, SensitivityProfile, allocate, sensitivity_from_keys,  # noqa: F401
                          uniform_allocation)
 from .context import Context, default_context  # noqa: F401

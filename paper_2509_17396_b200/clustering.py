@@ -55,6 +55,33 @@ def kmeans(points, k: int, seed: int, max_iters: int = 64, ctx: Context | None =
     return KMeansResult(assign.tolist(), cent, it, sse[:it].tolist())
 
 
+def kmeans_multi_device(points, k: int, seed: int, max_iters: int = 64, contexts=None) -> KMeansResult:
+    """kmeans with the points split in index order over `contexts` (one per
+    GPU of this process; a device may repeat): epk_kmeans_sharded, the ordered
+    chain over NCCL between distinct devices.  Bit-identical to `kmeans`."""
+    contexts = contexts or [default_context()]
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    if pts.ndim != 2:
+        raise Error("kmeans: points must be a 2-D array")
+    n, dim = pts.shape
+    S = len(contexts)
+    bounds = [n * s // S for s in range(S + 1)]
+    shards = [torch.as_tensor(pts[bounds[s]:bounds[s + 1]], device=torch.device("cuda", c.device))
+              for s, c in enumerate(contexts)]
+    ctxs = (C.c_void_p * S)(*[c.handle.value for c in contexts])
+    ptrs = (C.c_void_p * S)(*[s.data_ptr() if s.numel() else 0 for s in shards])
+    ns = (C.c_int64 * S)(*[bounds[s + 1] - bounds[s] for s in range(S)])
+    assign = np.zeros(n, np.int64)
+    cent = np.zeros((k, dim), np.float64)
+    iters = np.zeros(1, np.int64)
+    sse = np.zeros(max(max_iters, 1), np.float64)
+    _lib.call("epk_kmeans_sharded", C.cast(ctxs, C.c_void_p), S, C.cast(ptrs, C.c_void_p), C.cast(ns, C.c_void_p),
+              dim, k, C.c_uint64(seed), max_iters, assign.ctypes.data_as(C.c_void_p),
+              cent.ctypes.data_as(C.c_void_p), iters.ctypes.data_as(C.c_void_p), sse.ctypes.data_as(C.c_void_p))
+    it = int(iters[0])
+    return KMeansResult(assign.tolist(), cent, it, sse[:it].tolist())
+
+
 # ---------------------------------------------------------------------------
 # Sharded k-means (points split across ranks)
 # ---------------------------------------------------------------------------

@@ -31,6 +31,7 @@ struct CompactParams {
     LayerTable out_lt;
     int H;
     int max_chunks;
+    int layers;
     int slack;
     int row_vec;  // row bytes / 16
     const int32_t* in_off;
@@ -195,65 +196,71 @@ __global__ void __launch_bounds__(256) compact_plan_kernel(const __grid_constant
     }
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerCta) compact_gather_kernel(const __grid_constant__ CompactParams P) {
+// Warps walk the flattened (layer, chunk) items; the default launch gives
+// every warp one item, a persistent launch (ctx->gather_ctas) strides.
+__global__ void __launch_bounds__(512) compact_gather_kernel(const __grid_constant__ CompactParams P) {
     pdl_wait();
-    const int layer = blockIdx.y;
-    const int chunk = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+    const int wpb = blockDim.x >> 5;
     const int lane = threadIdx.x & 31;
-    if (chunk >= P.max_chunks || P.layer_bad[layer]) return;
-    const int32_t* off = P.in_off + layer * (P.H + 1);
-    const int64_t rows = off[P.H];
-    const int64_t r0 = int64_t(chunk) * kChunkRows;
-    if (r0 >= rows) return;
-    const int64_t in_base = P.in_lt.base[layer];
-    const int64_t out_base = P.out_lt.base[layer];
-    const uint8_t* kp = P.keep + in_base;
-    int32_t run = P.chunk_prefix[layer * P.max_chunks + chunk];
-    const int rv = P.row_vec;
-    const int hl = lane >> 4, cl = lane & 15;
-    // the chunk's first head and where the next one starts (a chunk rarely
-    // crosses a head boundary: rows past it take the binary search)
-    const int h0 = P.slack ? head_of_row(off, P.H, r0) : 0;
-    const int64_t h0_end = P.slack ? int64_t(off[h0 + 1]) : 0;
-    for (int sc = 0; sc < kChunkRows / 32; ++sc) {
-        const int64_t rs = r0 + sc * 32;
-        if (rs >= rows) break;
-        const int64_t r = rs + lane;
-        const bool k = r < rows && kp[r];
-        const unsigned bal = __ballot_sync(0xffffffffu, k);
-        if (bal == 0) continue;
-        int64_t dst = 0;
-        if (k) {
-            dst = out_base + run + __popc(bal & ((1u << lane) - 1u));
-            if (P.slack) dst += int64_t(P.slack) * (r < h0_end ? h0 : head_of_row(off, P.H, r));
-            P.out_pos[dst] = P.in_pos[in_base + r];
-        }
-        run += __popc(bal);
-        // copy the kept rows: a half-warp per row, 4 rows per half-warp in flight
-        for (int k0 = 0; k0 < 32; k0 += 8) {
-            uint4 kv[4], vv[4];
-            int64_t dsts[4];
-            bool ok[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int idx = k0 + 2 * u + hl;
-                ok[u] = (bal >> idx) & 1u;
-                dsts[u] = __shfl_sync(0xffffffffu, dst, idx);
+    const int64_t items = int64_t(P.layers) * P.max_chunks;
+    for (int64_t it = int64_t(blockIdx.x) * wpb + (threadIdx.x >> 5); it < items; it += int64_t(gridDim.x) * wpb) {
+        const int layer = int(it / P.max_chunks);
+        const int chunk = int(it % P.max_chunks);
+        if (P.layer_bad[layer]) continue;
+        const int32_t* off = P.in_off + layer * (P.H + 1);
+        const int64_t rows = off[P.H];
+        const int64_t r0 = int64_t(chunk) * kChunkRows;
+        if (r0 >= rows) continue;
+        const int64_t in_base = P.in_lt.base[layer];
+        const int64_t out_base = P.out_lt.base[layer];
+        const uint8_t* kp = P.keep + in_base;
+        int32_t run = P.chunk_prefix[layer * P.max_chunks + chunk];
+        const int rv = P.row_vec;
+        const int hl = lane >> 4, cl = lane & 15;
+        // the chunk's first head and where the next one starts (a chunk rarely
+        // crosses a head boundary: rows past it take the binary search)
+        const int h0 = P.slack ? head_of_row(off, P.H, r0) : 0;
+        const int64_t h0_end = P.slack ? int64_t(off[h0 + 1]) : 0;
+        for (int sc = 0; sc < kChunkRows / 32; ++sc) {
+            const int64_t rs = r0 + sc * 32;
+            if (rs >= rows) break;
+            const int64_t r = rs + lane;
+            const bool k = r < rows && kp[r];
+            const unsigned bal = __ballot_sync(0xffffffffu, k);
+            if (bal == 0) continue;
+            int64_t dst = 0;
+            if (k) {
+                dst = out_base + run + __popc(bal & ((1u << lane) - 1u));
+                if (P.slack) dst += int64_t(P.slack) * (r < h0_end ? h0 : head_of_row(off, P.H, r));
+                P.out_pos[dst] = P.in_pos[in_base + r];
             }
-            for (int c = cl; c < rv; c += 16) {
+            run += __popc(bal);
+            // copy the kept rows: a half-warp per row, 4 rows per half-warp in flight
+            for (int k0 = 0; k0 < 32; k0 += 8) {
+                uint4 kv[4], vv[4];
+                int64_t dsts[4];
+                bool ok[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    if (ok[u]) {
-                        const int64_t src = (in_base + rs + k0 + 2 * u + hl) * rv + c;
-                        kv[u] = __ldg(P.in_k + src);
-                        vv[u] = __ldg(P.in_v + src);
-                    }
+                    const int idx = k0 + 2 * u + hl;
+                    ok[u] = (bal >> idx) & 1u;
+                    dsts[u] = __shfl_sync(0xffffffffu, dst, idx);
                 }
+                for (int c = cl; c < rv; c += 16) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (ok[u]) {
-                        P.out_k[dsts[u] * rv + c] = kv[u];
-                        P.out_v[dsts[u] * rv + c] = vv[u];
+                    for (int u = 0; u < 4; ++u) {
+                        if (ok[u]) {
+                            const int64_t src = (in_base + rs + k0 + 2 * u + hl) * rv + c;
+                            kv[u] = __ldg(P.in_k + src);
+                            vv[u] = __ldg(P.in_v + src);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (ok[u]) {
+                            P.out_k[dsts[u] * rv + c] = kv[u];
+                            P.out_v[dsts[u] * rv + c] = vv[u];
+                        }
                     }
                 }
             }
@@ -279,6 +286,7 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     for (int l = 0; l < in->layers; ++l) max_rows = std::max<int64_t>(max_rows, P.in_lt.base[l + 1] - P.in_lt.base[l]);
     P.H = in->kv_heads;
     P.max_chunks = int(std::max<int64_t>(1, (max_rows + kChunkRows - 1) / kChunkRows));
+    P.layers = in->layers;
     P.slack = slack;
     P.row_vec = int(row_bytes / 16);
     P.in_off = in->head_off;
@@ -323,7 +331,17 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     EPK_CUDA_CHECK(launch_pdl(compact_plan_kernel, dim3(in->layers), dim3(256), 0, ctx->stream, P));
     EPK_LAUNCH_CHECK(ctx);
     EPK_PROF(ctx, "compact_gather");
-    EPK_CUDA_CHECK(launch_pdl(compact_gather_kernel, grid, dim3(32 * kWarpsPerCta), 0, ctx->stream, P));
+    if (ctx->gather_ctas > 0) {  // persistent (experiments: an SM-partitioned overlapped gather)
+        if (ctx->gather_smem > 0)
+            EPK_CUDA_CHECK(cudaFuncSetAttribute(compact_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                ctx->gather_smem));
+        EPK_CUDA_CHECK(launch_pdl(compact_gather_kernel, dim3(ctx->gather_ctas), dim3(ctx->gather_threads),
+                                  size_t(ctx->gather_smem), ctx->stream, P));
+    } else {
+        const int64_t items = int64_t(in->layers) * P.max_chunks;
+        EPK_CUDA_CHECK(launch_pdl(compact_gather_kernel, dim3(unsigned((items + kWarpsPerCta - 1) / kWarpsPerCta)),
+                                  dim3(32 * kWarpsPerCta), 0, ctx->stream, P));
+    }
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }

@@ -48,6 +48,19 @@ int ws_require(epk_ctx* ctx, int64_t bytes) {
     return EPK_OK;
 }
 
+int ensure_aux_stream(epk_ctx* ctx) {
+    if (ctx->aux) return EPK_OK;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (ctx->stream) cudaStreamIsCapturing(ctx->stream, &st);
+    if (st != cudaStreamCaptureStatusNone) return fail(EPK_ERR_ARG, "run the call once before graph capture");
+    int least = 0, greatest = 0;
+    EPK_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    EPK_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, greatest));
+    EPK_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_aux_fork, cudaEventDisableTiming));
+    EPK_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_aux_join, cudaEventDisableTiming));
+    return EPK_OK;
+}
+
 void prof_begin(epk_ctx* ctx, const char* name) {
     if (!ctx->profiling) return;
     epk_prof_rec r;
@@ -125,6 +138,8 @@ int launch_step_tc_grouped(epk_ctx*, const epk_cache_desc*, const epk_cache_desc
                                    const uint32_t*, const uint64_t*, uint32_t*, uint32_t*),
                            epk_cache_desc (*)(const epk_cache_desc*, int, int));
 int launch_append(epk_ctx*, const epk_cache_desc*, const void*, const void*, const int32_t*, int);
+int kmeans_shards(epk_ctx* const*, int, const double* const*, const int64_t*, int64_t, int64_t, uint64_t, int64_t,
+                  int64_t*, double*, int64_t*, double*);
 int launch_score_f32(epk_ctx*, const epk_cache_desc*, const float*, const float*, int, int, int, int64_t, float*);
 int launch_score_tc(epk_ctx*, const epk_cache_desc*, const void*, const void*, int, int, int, int64_t, float*,
                     const FusedSelect*);
@@ -161,16 +176,6 @@ static int check_cache(const epk_cache_desc* c) {
     if (c->layers < 1 || c->layers > kMaxLayers) return fail(EPK_ERR_UNSUPPORTED, "layers must be in [1, 128]");
     return EPK_OK;
 }
-
-// ---- host mirror of epikv::Rng (numerics.hpp:146-183) used by the seeding ----
-struct HostRng {
-    std::mt19937_64 gen;
-    explicit HostRng(uint64_t s) : gen(s) {}
-    double uniform() { return double(gen() >> 11) * 0x1.0p-53; }
-    int64_t uniform_index(int64_t n) {
-        return int64_t((static_cast<unsigned __int128>(gen()) * uint64_t(n)) >> 64);
-    }
-};
 
 }  // namespace epk
 
@@ -209,6 +214,11 @@ int epk_ctx_create(int device, void* stream, epk_ctx** out) {
     ctx->device = device;
     ctx->stream = static_cast<cudaStream_t>(stream);
     ctx->num_sms = prop.multiProcessorCount;
+    // experiments: SM split between the scorer and an overlapped gather
+    if (const char* e = std::getenv("EPK_GATHER_SMS")) ctx->gather_sms = std::max(0, std::min(ctx->num_sms - 8, std::atoi(e)));
+    if (const char* e = std::getenv("EPK_GATHER_CTAS")) ctx->gather_ctas = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("EPK_GATHER_THREADS")) ctx->gather_threads = std::max(32, std::min(512, std::atoi(e)));
+    if (const char* e = std::getenv("EPK_GATHER_SMEM_KB")) ctx->gather_smem = std::max(0, std::atoi(e)) * 1024;
     cudaError_t e = cudaMalloc(&ctx->err_flag, sizeof(int));
     if (e != cudaSuccess) {
         delete ctx;
@@ -238,6 +248,12 @@ int epk_ctx_destroy(epk_ctx* ctx) {
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
+    }
+    if (ctx->aux) {
+        cudaStreamSynchronize(ctx->aux);
+        cudaStreamDestroy(ctx->aux);
+        cudaEventDestroy(ctx->ev_aux_fork);
+        cudaEventDestroy(ctx->ev_aux_join);
     }
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -611,137 +627,11 @@ int epk_kmeans(epk_ctx* ctx, const double* pts, int64_t n, int64_t dim, int64_t 
                int64_t* assign_out, double* cent_out, int64_t* iters_out, double* sse_out) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
-    if (k < 1) return fail(EPK_ERR_ARG, "kmeans: cluster count must be >= 1");
-    if (n < k)
-        return fail(EPK_ERR_ARG, "kmeans: fewer points (" + std::to_string(n) + ") than clusters (" +
-                                     std::to_string(k) + ")");
-    cudaStream_t s = ctx->stream;
-    double *d_cent = nullptr, *d_sums = nullptr, *d_d2 = nullptr;
-    int64_t *d_assign = nullptr, *d_counts = nullptr;
-    auto cleanup = [&]() {
-        cudaFree(d_cent);
-        cudaFree(d_sums);
-        cudaFree(d_d2);
-        cudaFree(d_assign);
-        cudaFree(d_counts);
-    };
-#define KM_CUDA(x)                                  \
-    do {                                            \
-        cudaError_t _e = (x);                       \
-        if (_e != cudaSuccess) {                    \
-            cleanup();                              \
-            return cuda_fail(_e, #x);               \
-        }                                           \
-    } while (0)
-#define KM_RC(x)           \
-    do {                   \
-        int _r = (x);      \
-        if (_r) {          \
-            cleanup();     \
-            return _r;     \
-        }                  \
-    } while (0)
-    KM_CUDA(cudaMalloc(&d_cent, size_t(k * dim) * 8));
-    KM_CUDA(cudaMalloc(&d_sums, size_t(k * dim) * 8));
-    KM_CUDA(cudaMalloc(&d_d2, size_t(n) * 8));
-    KM_CUDA(cudaMalloc(&d_assign, size_t(n) * 8));
-    KM_CUDA(cudaMalloc(&d_counts, size_t(k) * 8));
-
-    // k-means++ seeding (clustering.hpp:160-191): distances on the device,
-    // the running min, the sequential total and the draw on the host.
-    HostRng rng(seed);
-    std::vector<int64_t> chosen_idx;
-    chosen_idx.push_back(rng.uniform_index(n));
-    KM_CUDA(cudaMemcpyAsync(d_cent, pts + chosen_idx[0] * dim, size_t(dim) * 8, cudaMemcpyDeviceToDevice, s));
-    std::vector<double> best(static_cast<size_t>(n), std::numeric_limits<double>::infinity());
-    std::vector<double> dd(static_cast<size_t>(n));
-    int64_t have = 1;
-    while (have < k) {
-        KM_RC(launch_km_dist(ctx, pts, n, dim, d_cent + (have - 1) * dim, 1, d_d2));
-        KM_CUDA(cudaMemcpyAsync(dd.data(), d_d2, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
-        KM_CUDA(cudaStreamSynchronize(s));
-        double total = 0.0;
-        for (int64_t i = 0; i < n; ++i) {
-            best[size_t(i)] = std::min(best[size_t(i)], dd[size_t(i)]);
-            total += best[size_t(i)];
-        }
-        int64_t chosen = 0;
-        if (total > 0.0) {
-            const double target = rng.uniform() * total;
-            double acc = 0.0;
-            chosen = n - 1;
-            for (int64_t i = 0; i < n; ++i) {
-                acc += best[size_t(i)];
-                if (acc > target) {
-                    chosen = i;
-                    break;
-                }
-            }
-        } else {
-            chosen = rng.uniform_index(n);
-        }
-        KM_CUDA(cudaMemcpyAsync(d_cent + have * dim, pts + chosen * dim, size_t(dim) * 8, cudaMemcpyDeviceToDevice, s));
-        ++have;
-    }
-
-    // Lloyd iterations (clustering.hpp:195-255).
-    std::vector<int64_t> assign(static_cast<size_t>(n), 0);
-    std::vector<int64_t> prev(static_cast<size_t>(n), 0);
-    std::vector<int64_t> counts(static_cast<size_t>(k));
-    int64_t iters = 0;
-    for (int64_t iter = 0; iter < max_iters; ++iter) {
-        KM_RC(launch_km_assign(ctx, pts, n, dim, d_cent, k, d_assign, nullptr));
-        KM_CUDA(cudaMemcpyAsync(assign.data(), d_assign, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
-        KM_CUDA(cudaStreamSynchronize(s));
-        bool changed = false;
-        for (int64_t i = 0; i < n; ++i)
-            if (assign[size_t(i)] != prev[size_t(i)]) changed = true;
-        std::fill(counts.begin(), counts.end(), 0);
-        for (int64_t a : assign) ++counts[size_t(a)];
-        bool repaired = false;
-        for (int64_t c = 0; c < k; ++c) {
-            if (counts[size_t(c)] > 0) continue;
-            // distances to the current centroids under the current assignment
-            KM_CUDA(cudaMemcpyAsync(d_assign, assign.data(), size_t(n) * 8, cudaMemcpyHostToDevice, s));
-            KM_RC(launch_km_sqdist(ctx, pts, n, dim, d_cent, d_assign, d_d2));
-            KM_CUDA(cudaMemcpyAsync(dd.data(), d_d2, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
-            KM_CUDA(cudaStreamSynchronize(s));
-            int64_t victim = 0;
-            double worst = -1.0;
-            for (int64_t i = 0; i < n; ++i) {
-                if (counts[size_t(assign[size_t(i)])] <= 1) continue;
-                if (dd[size_t(i)] > worst) {
-                    worst = dd[size_t(i)];
-                    victim = i;
-                }
-            }
-            --counts[size_t(assign[size_t(victim)])];
-            assign[size_t(victim)] = c;
-            ++counts[size_t(c)];
-            changed = true;
-            repaired = true;
-        }
-        if (repaired) KM_CUDA(cudaMemcpyAsync(d_assign, assign.data(), size_t(n) * 8, cudaMemcpyHostToDevice, s));
-        KM_RC(launch_km_sums(ctx, pts, n, dim, d_assign, k, d_sums, d_counts, 0));
-        KM_RC(launch_km_finalize(ctx, d_sums, d_counts, k, dim, d_cent));
-        iters = iter + 1;
-        KM_RC(launch_km_sqdist(ctx, pts, n, dim, d_cent, d_assign, d_d2));
-        KM_CUDA(cudaMemcpyAsync(dd.data(), d_d2, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
-        KM_CUDA(cudaStreamSynchronize(s));
-        double sse = 0.0;
-        for (int64_t i = 0; i < n; ++i) sse += dd[size_t(i)];
-        if (sse_out) sse_out[iter] = sse;
-        prev = assign;
-        if (!changed) break;
-    }
-    std::memcpy(assign_out, assign.data(), size_t(n) * 8);
-    KM_CUDA(cudaMemcpyAsync(cent_out, d_cent, size_t(k * dim) * 8, cudaMemcpyDeviceToHost, s));
-    KM_CUDA(cudaStreamSynchronize(s));
-    *iters_out = iters;
-    cleanup();
-#undef KM_CUDA
-#undef KM_RC
-    return EPK_OK;
+    // one shard of the multi-GPU orchestration (multigpu.cu): one code path
+    epk_ctx* ctxs[1] = {ctx};
+    const double* shards[1] = {pts};
+    const int64_t ns[1] = {n};
+    return kmeans_shards(ctxs, 1, shards, ns, dim, k, seed, max_iters, assign_out, cent_out, iters_out, sse_out);
 }
 
 // ---- K5 ---------------------------------------------------------------------

@@ -30,6 +30,8 @@ struct epk_ctx {
     cudaStream_t hi = nullptr;    // overlap mode: scoring + select at the highest stream priority
     cudaEvent_t ev_hi = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t aux = nullptr;  // highest priority: concurrent consumer kernels (K5 chain)
+    cudaEvent_t ev_aux_fork = nullptr, ev_aux_join = nullptr;
     int layer_group = 0;  // layers per group in epk_evict_step (0 = auto: group K fits in L2)
     int overlap = 1;      // run each group's compaction on `side`
     void* step_buf = nullptr;  // epk_evict_step scores + keep mask
@@ -37,11 +39,18 @@ struct epk_ctx {
     int* err_flag = nullptr;  // deferred device-side error code (device int)
     int64_t launches = 0;
     int num_sms = 148;
+    int gather_sms = 0;     // SMs left to the compaction gather while the scorer runs (0: scorer takes all)
+    int gather_ctas = 0;    // gather launch: persistent CTAs (0: one warp per 128-row chunk)
+    int gather_threads = 128;
+    int gather_smem = 0;    // dynamic shared memory reserved per gather CTA (keeps it off scorer SMs)
     bool profiling = false;  // record CUDA events around every kernel launch
     std::vector<epk_prof_rec> prof;
 };
 
 namespace epk {
+
+// Persistent CTAs of the tensor-core scorer passes.
+inline int score_grid(const epk_ctx* c) { return c->num_sms - c->gather_sms; }
 
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
@@ -50,6 +59,8 @@ int cuda_fail(cudaError_t e, const char* what);
 // Workspace carve-up: returns a pointer into ctx->ws (grows the workspace when
 // needed; growing is not allowed while the stream is being captured).
 int ws_require(epk_ctx* ctx, int64_t bytes);
+// Creates the context's aux stream and its fork/join events on first use.
+int ensure_aux_stream(epk_ctx* ctx);
 int ws2_require(epk_ctx* ctx, int64_t bytes);
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }

@@ -16,6 +16,7 @@
 #include <algorithm>
 
 #include "epk_internal.cuh"
+#include "sm100.cuh"
 
 namespace epk {
 
@@ -159,95 +160,222 @@ template <>
 __device__ __forceinline__ double to_d<__nv_bfloat16>(__nv_bfloat16 x) { return double(__bfloat162float(x)); }
 
 // K5, bit-exact with the reference's loop order (allocation.hpp:80-100 with
-// cosine / l2_norm / dot of numerics.hpp:52-87, -ffp-contract=off):
-//   pair  one thread per (layer, h, t): |a|^2, |b|^2 and a.b as sequential
-//         chains over the dimensions (explicit __dmul_rn / __dadd_rn, no FMA),
-//         correctly rounded sqrt and division, clamp to [-1, 1]; a zero-norm
-//         pair is stored as NaN (skipped).
-//   mean  one thread per layer: the (h, t)-ordered running sum of the pair
-//         cosines -- the reference's sequential accumulation -- with a
-//         64-deep rotating register prefetch so the dependent fp64 adds, not
-//         the loads, set the pace; sigma = sum / counted (1 when none count).
+// cosine / l2_norm / dot of numerics.hpp:52-87, -ffp-contract=off), as two
+// kernels that run CONCURRENTLY (the chain kernel on the context's aux stream):
+//   pair   a CTA of TR threads per tile of TR (h, t) pairs of one layer; the
+//          tile's K_full / K_block rows are staged in shared memory with
+//          coalesced cp.async copies (rows padded by 16 bytes, so the
+//          per-thread 16-byte row reads are bank-conflict free), then each
+//          thread runs |a|^2, |b|^2 and a.b as sequential chains over the
+//          dimensions (explicit __dmul_rn / __dadd_rn, no FMA), correctly
+//          rounded sqrt and division, clamp to [-1, 1]; a zero-norm pair is
+//          stored as NaN (skipped).  Tiles go chunk-major over the layers and
+//          each publishes a ready flag.
+//   chain  one CTA per layer: warp 1 follows the ready flags, loads the
+//          cosines in (h, t) order and compacts away the NaNs into a
+//          shared-memory ring; lane 0 of warp 0 runs the reference's
+//          sequential fp64 running sum from the ring (nothing but the
+//          dependent adds on its critical path).  sigma = sum / counted
+//          (1 when none count).
+// pairs per tile (= threads per pair CTA): ~64 KB of staged rows at d = 128
 template <typename T>
-__device__ __forceinline__ void cos_vec(const T* p, int j, double (&x)[16 / sizeof(T)]) {
-    const uint4 w = __ldg(reinterpret_cast<const uint4*>(p) + j);
-    const T* e = reinterpret_cast<const T*>(&w);
-#pragma unroll
-    for (int u = 0; u < int(16 / sizeof(T)); ++u) x[u] = to_d(e[u]);
-}
+struct K5Shape;
+template <>
+struct K5Shape<double> {
+    static constexpr int TR = 32;
+};
+template <>
+struct K5Shape<float> {
+    static constexpr int TR = 64;
+};
+template <>
+struct K5Shape<__nv_bfloat16> {
+    static constexpr int TR = 128;
+};
+
+struct K5Params {
+    const void* kf;
+    const void* kb;
+    int64_t rows;        // (h, t) pairs per layer
+    int64_t cos_stride;  // cosv layer stride (16-byte aligned)
+    int dim, layers;
+    int64_t tiles;       // tiles per layer
+    double* cosv;
+    unsigned* ready;     // [layers][tiles]
+    double* sigma;
+    int64_t* skipped_per_layer;
+    int* err_flag;
+};
 
 template <typename T>
-__global__ void __launch_bounds__(256) cosine_pair_kernel(const T* __restrict__ kf, const T* __restrict__ kb,
-                                                          int64_t rows_per_layer, int dim, double* cosv) {
-    const int layer = blockIdx.y;
-    const int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (row >= rows_per_layer) return;
-    const int64_t g = int64_t(layer) * rows_per_layer + row;
-    const T* a = kf + g * dim;
-    const T* b = kb + g * dim;
-    double na = 0.0, nb = 0.0, dot = 0.0;
-    constexpr int V = 16 / sizeof(T);
-    if ((dim * int(sizeof(T))) % 16 == 0) {
-        for (int j = 0; j < dim / V; ++j) {
-            double x[V], y[V];
-            cos_vec<T>(a, j, x);
-            cos_vec<T>(b, j, y);
+__device__ __forceinline__ void cos_accum(const uint4 w1, const uint4 w2, double& na, double& nb, double& dot) {
+    const T* e1 = reinterpret_cast<const T*>(&w1);
+    const T* e2 = reinterpret_cast<const T*>(&w2);
 #pragma unroll
-            for (int u = 0; u < V; ++u) {
-                na = __dadd_rn(na, __dmul_rn(x[u], x[u]));
-                nb = __dadd_rn(nb, __dmul_rn(y[u], y[u]));
-                dot = __dadd_rn(dot, __dmul_rn(x[u], y[u]));
-            }
+    for (int u = 0; u < int(16 / sizeof(T)); ++u) {
+        const double x = to_d(e1[u]), y = to_d(e2[u]);
+        na = __dadd_rn(na, __dmul_rn(x, x));
+        nb = __dadd_rn(nb, __dmul_rn(y, y));
+        dot = __dadd_rn(dot, __dmul_rn(x, y));
+    }
+}
+
+__device__ __forceinline__ double finish_cosine(double na, double nb, double dot) {
+    na = __dsqrt_rn(na);
+    nb = __dsqrt_rn(nb);
+    if (na == 0.0 || nb == 0.0) return __longlong_as_double(0x7ff8000000000000ll);  // skipped (zero norm)
+    const double c = __ddiv_rn(dot, __dmul_rn(na, nb));
+    return c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
+}
+
+// STAGED: rows staged through shared memory (row bytes a multiple of 16);
+// else each thread reads its own row directly (any dim).
+template <typename T, bool STAGED>
+__global__ void __launch_bounds__(K5Shape<T>::TR) cosine_pair_kernel(const __grid_constant__ K5Params P) {
+    constexpr int TR = K5Shape<T>::TR;
+    extern __shared__ __align__(16) uint8_t k5_smem[];
+    const int layer = int(blockIdx.x % P.layers);
+    const int64_t tile = blockIdx.x / P.layers;  // chunk-major: every layer advances together
+    const int64_t r0 = tile * TR;
+    const int nrows = int(min(int64_t(TR), P.rows - r0));
+    const int64_t g0 = int64_t(layer) * P.rows + r0;
+    const T* kf = static_cast<const T*>(P.kf);
+    const T* kb = static_cast<const T*>(P.kb);
+    double na = 0.0, nb = 0.0, dot = 0.0;
+    if (STAGED) {
+        const int rowb = P.dim * int(sizeof(T));
+        const int stride = rowb + 16;
+        const int cpr = rowb / 16;
+        uint8_t* sa = k5_smem;
+        uint8_t* sb = k5_smem + TR * stride;
+        const uint8_t* ga = reinterpret_cast<const uint8_t*>(kf + g0 * P.dim);
+        const uint8_t* gb = reinterpret_cast<const uint8_t*>(kb + g0 * P.dim);
+        const int nchunk = nrows * cpr;
+        for (int q = threadIdx.x; q < nchunk; q += TR) {
+            const int r = q / cpr, c = q % cpr;
+            const uint32_t da = sm100::smem_u32(sa + r * stride + c * 16);
+            const uint32_t db = sm100::smem_u32(sb + r * stride + c * 16);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(da), "l"(ga + int64_t(q) * 16) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(db), "l"(gb + int64_t(q) * 16) : "memory");
         }
-    } else {
-        for (int i = 0; i < dim; ++i) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        if (int(threadIdx.x) < nrows) {
+            const uint4* ra = reinterpret_cast<const uint4*>(sa + threadIdx.x * stride);
+            const uint4* rb = reinterpret_cast<const uint4*>(sb + threadIdx.x * stride);
+            for (int j = 0; j < cpr; ++j) cos_accum<T>(ra[j], rb[j], na, nb, dot);
+        }
+    } else if (int(threadIdx.x) < nrows) {
+        const T* a = kf + (g0 + threadIdx.x) * P.dim;
+        const T* b = kb + (g0 + threadIdx.x) * P.dim;
+        for (int i = 0; i < P.dim; ++i) {
             const double x = to_d(a[i]), y = to_d(b[i]);
             na = __dadd_rn(na, __dmul_rn(x, x));
             nb = __dadd_rn(nb, __dmul_rn(y, y));
             dot = __dadd_rn(dot, __dmul_rn(x, y));
         }
     }
-    na = __dsqrt_rn(na);
-    nb = __dsqrt_rn(nb);
-    double c;
-    if (na == 0.0 || nb == 0.0) {
-        c = __longlong_as_double(0x7ff8000000000000ll);  // skipped (zero norm)
-    } else {
-        c = __ddiv_rn(dot, __dmul_rn(na, nb));
-        c = c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
+    if (int(threadIdx.x) < nrows) P.cosv[int64_t(layer) * P.cos_stride + r0 + threadIdx.x] = finish_cosine(na, nb, dot);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.ready + int64_t(layer) * P.tiles + tile), "r"(1u)
+                     : "memory");
     }
-    cosv[g] = c;
 }
 
-__global__ void __launch_bounds__(32) cosine_mean_kernel(const double* __restrict__ cosv, int64_t rows,
-                                                         double* sigma, int64_t* skipped_per_layer) {
-    if (threadIdx.x != 0) return;
+constexpr int kChainChunk = 1024;  // cosines per ring stage (8 KB)
+constexpr int kChainStages = 4;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(64) cosine_chain_kernel(const __grid_constant__ K5Params P, int tr) {
+    __shared__ __align__(128) double ring[kChainStages][kChainChunk];
+    __shared__ int nvalid[kChainStages], nskip[kChainStages];
+    __shared__ __align__(8) uint64_t full[kChainStages], empty[kChainStages];
     const int l = blockIdx.x;
-    const double* v = cosv + int64_t(l) * rows;
-    constexpr int D = 64;
-    double buf[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) buf[j] = j < rows ? __ldcg(v + j) : 0.0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double* v = P.cosv + int64_t(l) * P.cos_stride;
+    const unsigned* ready = P.ready + int64_t(l) * P.tiles;
+    const int64_t nchunks = (P.rows + kChainChunk - 1) / kChainChunk;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kChainStages; ++s) {
+            sm100::mbar_init(&full[s], 1);
+            sm100::mbar_init(&empty[s], 1);
+        }
+        sm100::fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == 1) {  // loader: flags -> cosines -> NaN-free ring slot
+        bool timed_out = false;
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const int s = int(c % kChainStages);
+            sm100::mbar_wait(&empty[s], (uint32_t(c / kChainStages) & 1u) ^ 1u);
+            const int64_t i0 = c * kChainChunk;
+            const int n = int(min(int64_t(kChainChunk), P.rows - i0));
+            if (lane == 0 && !timed_out) {  // wait until every tile of this chunk is published (bounded)
+                const int64_t t1 = (i0 + n - 1) / tr;
+                for (int64_t t = i0 / tr; t <= t1; ++t) {
+                    long spins = 0;
+                    while (ld_acquire_u32(ready + t) == 0u) {
+                        if (++spins > (1l << 25)) {
+                            atomicCAS(P.err_flag, 0, EPK_ERR_CUDA);
+                            timed_out = true;
+                            break;
+                        }
+                        __nanosleep(64);
+                    }
+                    if (timed_out) break;
+                }
+                __threadfence();
+            }
+            __syncwarp();
+            int base = 0, sk = 0;
+            for (int j = 0; j < n; j += 32) {
+                const int i = j + lane;
+                const double x = i < n ? __ldcg(v + i0 + i) : 0.0;
+                const bool ok = i < n && x == x;
+                const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                if (ok) ring[s][base + __popc(bal & ((1u << lane) - 1u))] = x;
+                base += __popc(bal);
+                sk += __popc(__ballot_sync(0xffffffffu, i < n && !ok));
+            }
+            if (lane == 0) {
+                nvalid[s] = base;
+                nskip[s] = sk;
+            }
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&full[s]);  // release: the ring stores above precede it
+        }
+        return;
+    }
+    if (lane != 0) return;
     double acc = 0.0;
     long long cnt = 0, sk = 0;
-    for (int64_t b0 = 0; b0 < rows; b0 += D) {
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int s = int(c % kChainStages);
+        sm100::mbar_wait(&full[s], uint32_t(c / kChainStages) & 1u);
+        const int n = nvalid[s];
+        const double* x = ring[s];
+        int i = 0;
+        for (; i + 8 <= n; i += 8) {
+            double b[8];
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            const int64_t i = b0 + j;
-            if (i < rows) {
-                const double x = buf[j];
-                if (x == x) {
-                    acc = __dadd_rn(acc, x);
-                    ++cnt;
-                } else {
-                    ++sk;
-                }
-            }
-            buf[j] = i + D < rows ? __ldcg(v + i + D) : 0.0;
+            for (int u = 0; u < 8; ++u) b[u] = x[i + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, b[u]);
         }
+        for (; i < n; ++i) acc = __dadd_rn(acc, x[i]);
+        cnt += n;
+        sk += nskip[s];
+        sm100::mbar_arrive(&empty[s]);
     }
-    sigma[l] = cnt > 0 ? __ddiv_rn(acc, double(cnt)) : 1.0;
-    skipped_per_layer[l] = sk;
+    P.sigma[l] = cnt > 0 ? __ddiv_rn(acc, double(cnt)) : 1.0;
+    P.skipped_per_layer[l] = sk;
 }
 
 __global__ void cosine_skip_total_kernel(const int64_t* per_layer, int layers, int64_t* skipped) {
@@ -258,31 +386,74 @@ __global__ void cosine_skip_total_kernel(const int64_t* per_layer, int layers, i
     }
 }
 
+template <typename T>
+static int k5_launch_pair(epk_ctx* ctx, const K5Params& P) {
+    constexpr int TR = K5Shape<T>::TR;
+    const int rowb = P.dim * int(sizeof(T));
+    const size_t smem = size_t(2) * TR * (rowb + 16);
+    const bool staged = rowb % 16 == 0 && smem <= 200 * 1024 && (reinterpret_cast<uintptr_t>(P.kf) & 15) == 0 &&
+                        (reinterpret_cast<uintptr_t>(P.kb) & 15) == 0;
+    const dim3 grid(unsigned(P.tiles * P.layers));
+    EPK_PROF(ctx, "cosine_pair");
+    if (staged) {
+        EPK_CUDA_CHECK(cudaFuncSetAttribute(cosine_pair_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            int(smem)));
+        cosine_pair_kernel<T, true><<<grid, TR, smem, ctx->stream>>>(P);
+    } else {
+        cosine_pair_kernel<T, false><<<grid, TR, 0, ctx->stream>>>(P);
+    }
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
 int launch_key_cosine(epk_ctx* ctx, const void* kf, const void* kb, int dtype, int layers, int H, int64_t ntok,
                       int dim, double* sigma, int64_t* skipped) {
     const int64_t rows = int64_t(H) * ntok;
-    int rc = ws_require(ctx, int64_t(layers) * rows * 8 + int64_t(layers) * 8 + 1024);
+    const int tr = dtype == EPK_F64 ? K5Shape<double>::TR : dtype == EPK_F32 ? K5Shape<float>::TR
+                                                                             : K5Shape<__nv_bfloat16>::TR;
+    const int64_t tiles = (rows + tr - 1) / tr;
+    if (tiles * layers > int64_t(0x7fffffff)) return fail(EPK_ERR_UNSUPPORTED, "key_cosine: too many pairs");
+    const int64_t stride = (rows + 1) & ~int64_t(1);  // 16-byte aligned layer rows
+    int rc = ws_require(ctx, int64_t(layers) * stride * 8 + 16 + int64_t(layers) * 8 + tiles * layers * 4 + 2048);
     if (rc) return rc;
     WsCarver carve(ctx->ws);
-    double* cosv = carve.take<double>(int64_t(layers) * rows);
-    int64_t* skl = carve.take<int64_t>(layers);
-    const dim3 g(unsigned((rows + 255) / 256), layers);
-    EPK_PROF(ctx, "cosine_pair");
-    if (dtype == EPK_F64)
-        cosine_pair_kernel<double><<<g, 256, 0, ctx->stream>>>(static_cast<const double*>(kf),
-                                                               static_cast<const double*>(kb), rows, dim, cosv);
-    else if (dtype == EPK_F32)
-        cosine_pair_kernel<float><<<g, 256, 0, ctx->stream>>>(static_cast<const float*>(kf),
-                                                              static_cast<const float*>(kb), rows, dim, cosv);
-    else
-        cosine_pair_kernel<__nv_bfloat16><<<g, 256, 0, ctx->stream>>>(
-            static_cast<const __nv_bfloat16*>(kf), static_cast<const __nv_bfloat16*>(kb), rows, dim, cosv);
-    EPK_LAUNCH_CHECK(ctx);
-    EPK_PROF(ctx, "cosine_mean");
-    cosine_mean_kernel<<<layers, 32, 0, ctx->stream>>>(cosv, rows, sigma, skl);
-    EPK_LAUNCH_CHECK(ctx);
+    K5Params P;
+    P.kf = kf;
+    P.kb = kb;
+    P.rows = rows;
+    P.cos_stride = stride;
+    P.dim = dim;
+    P.layers = layers;
+    P.tiles = tiles;
+    P.cosv = carve.take<double>(int64_t(layers) * stride + 2);
+    P.skipped_per_layer = carve.take<int64_t>(layers);
+    P.ready = carve.take<unsigned>(tiles * layers);
+    P.sigma = sigma;
+    P.err_flag = ctx->err_flag;
+    if ((rc = ensure_aux_stream(ctx))) return rc;
+    cudaStream_t main = ctx->stream;
+    EPK_CUDA_CHECK(cudaMemsetAsync(P.ready, 0, size_t(tiles * layers) * 4, main));
+    // the chain CTAs follow the pair tiles' ready flags from the aux stream
+    EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_aux_fork, main));
+    EPK_CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->ev_aux_fork, 0));
+    ctx->stream = ctx->aux;
+    EPK_PROF(ctx, "cosine_chain");
+    cosine_chain_kernel<<<layers, 64, 0, ctx->aux>>>(P, tr);
+    ctx->stream = main;
+    {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "cosine_chain launch");
+        ctx->launches++;
+        if (ctx->profiling && !ctx->prof.empty()) cudaEventRecord(ctx->prof.back().stop, ctx->aux);
+    }
+    if (dtype == EPK_F64) rc = k5_launch_pair<double>(ctx, P);
+    else if (dtype == EPK_F32) rc = k5_launch_pair<float>(ctx, P);
+    else rc = k5_launch_pair<__nv_bfloat16>(ctx, P);
+    if (rc) return rc;
+    EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_aux_join, ctx->aux));
+    EPK_CUDA_CHECK(cudaStreamWaitEvent(main, ctx->ev_aux_join, 0));
     EPK_PROF(ctx, "cosine_total");
-    cosine_skip_total_kernel<<<1, 32, 0, ctx->stream>>>(skl, layers, skipped);
+    cosine_skip_total_kernel<<<1, 32, 0, ctx->stream>>>(P.skipped_per_layer, layers, skipped);
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
 }

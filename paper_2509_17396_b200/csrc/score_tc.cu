@@ -104,10 +104,10 @@ struct TcParams {
     int p1_grid;    // STATS grid (SCORE reads it to locate the partials)
     int p1_runs;    // STATS runs
     int slots;      // partial slots per query row (kStatGroups per STATS CTA)
-    int hk_base;    // SCORE: global (layer, head) index of this launch's first head (P1 ran on all layers)
+    int hk_base;    // global (layer, head) index of this launch's first head (rows of part_m / part_z)
     const int32_t* head_off;
     const int32_t* head_len;
-    int32_t* p1_pre;  // [p1_runs + 1] STATS run prefix (written by STATS CTA 0)
+    int32_t* p1_pre;  // [p1_runs + 1] run prefix of the STATS launch over this layer range (its CTA 0 writes it)
     float c2;         // d^-1/2 * log2(e)
     float* part_m;    // [L*H*NQ*128][slots]
     float* part_z;
@@ -253,15 +253,15 @@ __device__ __forceinline__ float merge_slots(const float* pm, const float* pz, c
     return M + log2f(Z);
 }
 
-// lse2 of STATS query row rq of head hk from the partials of every P1 CTA
-// that covered the row's run (general path: any number of P1 CTAs).
+// lse2 of STATS query row rq of head hk (launch-local) from the partials of
+// every P1 CTA that covered the row's run (general path: any number of P1 CTAs).
 __device__ float merge_lse2(const TcParams& P, int hk, int rq, int64_t T1) {
     const int cg = (rq / kChunk) / P.cg_chunks;
     const int run = hk * P.cgroups + cg;
     const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
     if (R1 <= R0) return INFINITY;
     const int b0 = part_cnt(T1, P.p1_grid, R0) - 1, b1 = part_cnt(T1, P.p1_grid, R1 - 1) - 1;
-    const int64_t row = int64_t(hk) * (P.NQ * kChunk) + rq;
+    const int64_t row = int64_t(hk + P.hk_base) * (P.NQ * kChunk) + rq;
     const float* pm = P.part_m + row * P.slots;
     const float* pz = P.part_z + row * P.slots;
     float M = -INFINITY;
@@ -581,7 +581,7 @@ __global__ void __maxnreg__(128)
                 for (int cc = 0; cc < kMaxQRes; ++cc) {
                     if (cc < x.nq) {
                         const int rq = (x.c0 + cc) * kChunk + r_local;
-                        const int64_t o = (int64_t(x.hk) * (P.NQ * kChunk) + rq) * P.slots + x.slot + half;  // slot = 3 per CTA
+                        const int64_t o = (int64_t(x.hk + P.hk_base) * (P.NQ * kChunk) + rq) * P.slots + x.slot + half;
                         P.part_m[o] = m[cc];
                         P.part_z[o] = z[cc];
                     }
@@ -591,7 +591,7 @@ __global__ void __maxnreg__(128)
                     named_bar_sync(1, 32 * kEpiWarps);
                     if (P.keys && lkey >= 0 && lkey / P.H != x.l) flush_coarse(P, lkey / P.H, s_coarse, etid);
                     if (etid < P.cgroups) {  // slot list of each P1 run (head, chunk group)
-                        const int run = (x.hk + P.hk_base) * P.cgroups + etid;
+                        const int run = x.hk * P.cgroups + etid;  // the P1 launch of this layer range
                         const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
                         int n = 0;
                         if (R1 > R0) {
@@ -615,7 +615,7 @@ __global__ void __maxnreg__(128)
                             const int64_t row = int64_t(x.hk + P.hk_base) * (P.NQ * kChunk) + r;
                             v = n >= 0 ? merge_slots(P.part_m + row * P.slots, P.part_z + row * P.slots,
                                                      s_slot + cg * kMaxSlots, n)
-                                       : merge_lse2(P, x.hk + P.hk_base, r, T1);
+                                       : merge_lse2(P, x.hk, r, T1);
                         }
                         s_lse[r] = -v;  // negated: the epilogue adds it with FFMA2
                     }
@@ -707,18 +707,22 @@ static int smem_bytes(const TcParams& P, int mode) {
            (2 * P.kstages + 2 * kMaxQRes + 8) * 8 + 16 + (P.runs + 1) * 4;
 }
 
-// A tensor-core scoring launch plan: P1 over every layer of `c`, then P2 over
-// any layer range [l0, l1) (several ranges may follow one P1, so a step can
-// interleave the selection/compaction of finished layer groups with the
-// scoring of the next).
+// A tensor-core scoring launch plan.  P1 and P2 run per layer range [l0, l1)
+// (a step's layer group): P1 of a range, then P2 of the same range, so the
+// range's K tiles are re-read from L2 and a finished group's selection /
+// compaction can overlap the next group's scoring.
 struct TcPlan {
     TcParams P1, P2;
     CUtensorMap tm_k, tm_q, tm_kp;
     int smem1, smem2;
+    int grid;  // persistent CTAs of both passes
     void (*stats_fn)(TcParams, CUtensorMap, CUtensorMap, CUtensorMap);
     void (*score_fn)(TcParams, CUtensorMap, CUtensorMap, CUtensorMap);
     const void* q;
-    int64_t qlayer;  // bytes of one layer's query rows
+    const void* kp;
+    int64_t qlayer;   // bytes of one layer's query rows
+    int64_t kplayer;  // bytes of one layer's prompt-key rows
+    int32_t* p1_pre_all;  // run prefixes: range [l0, l1) at p1_pre_all + l0 * (H * cgroups + 1)
     epk_cache_desc c;
 };
 
@@ -751,7 +755,7 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.hist_coarse = fs ? fs->hist_coarse : nullptr;
     P.ptiles = (p + 127) / 128;
     P.hk_base = 0;
-    const int grid = ctx->num_sms;  // persistent: one CTA per SM, tile-balanced ranges
+    const int grid = score_grid(ctx);  // persistent: one CTA per SM, tile-balanced ranges
 
     // STATS kernels by exp2 split (POLY of every 4 column pairs on the FMA
     // pipe); EPK_TC_POLY picks one (default 0: measured on B200 the FFMA2
@@ -828,12 +832,15 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.p1_runs = P.runs;
     P.slots = kStatGroups * grid;
     const int64_t rows = int64_t(P.L) * H * P.NQ * kChunk;
-    rc = ws_require(ctx, 2 * rows * P.slots * 4 + int64_t(P.runs + 1) * 4 + 4096);
+    const int64_t pre_n = int64_t(P.L) * (int64_t(H) * P.cgroups + 1) + 1;
+    rc = ws_require(ctx, 2 * rows * P.slots * 4 + pre_n * 4 + 4096);
     if (rc) return rc;
     WsCarver carve(ctx->ws);
     P.part_m = carve.take<float>(rows * P.slots);
     P.part_z = carve.take<float>(rows * P.slots);
-    P.p1_pre = carve.take<int32_t>(P.runs + 1);
+    P.p1_pre = carve.take<int32_t>(pre_n);
+    out->p1_pre_all = P.p1_pre;
+    out->grid = grid;
     T.P1 = P;
     T.smem1 = smem_bytes(P, MODE_STATS);
     T.stats_fn = stats_fns[poly];
@@ -862,7 +869,9 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     T.smem2 = smem_bytes(P, MODE_SCORE);
     T.score_fn = score_fn;
     T.q = q;
+    T.kp = kp;
     T.qlayer = int64_t(hq) * p * kD * 2;
+    T.kplayer = int64_t(H) * p * kD * 2;
     T.c = *c;
     if (std::getenv("EPK_TC_VERBOSE"))
         fprintf(stderr, "P2: NQ=%d resident=%d kstages=%d smem=%d runs=%d\n", P.NQ, P.resident, P.kstages, T.smem2,
@@ -870,18 +879,15 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     return EPK_OK;
 }
 
-static int tc_launch_p1(epk_ctx* ctx, const TcPlan& T) {
-    EPK_PROF(ctx, "p1_rowstats");
-    EPK_CUDA_CHECK(launch_pdl(T.stats_fn, dim3(ctx->num_sms), dim3(kThreadsStats), T.smem1, ctx->stream, T.P1, T.tm_k,
-                              T.tm_q, T.tm_kp));
-    EPK_LAUNCH_CHECK(ctx);
-    return EPK_OK;
-}
-
-// P2 over layers [l0, l1) of the plan's cache (after tc_launch_p1).
-static int tc_launch_p2(epk_ctx* ctx, const TcPlan& T, int l0, int l1) {
-    TcParams P = T.P2;
-    CUtensorMap tm_q = T.tm_q;
+// The plan's parameters of one pass restricted to layers [l0, l1), with its
+// query (and, for P1, prompt-key) tensor maps re-based to layer l0.
+static int tc_view(const TcPlan& T, int mode, int l0, int l1, TcParams* out, CUtensorMap* tm_q, CUtensorMap* tm_kp) {
+    TcParams P = mode == MODE_STATS ? T.P1 : T.P2;
+    *tm_q = T.tm_q;
+    *tm_kp = T.tm_kp;
+    P.hk_base = l0 * P.H;
+    P.p1_pre = T.p1_pre_all + int64_t(l0) * (int64_t(P.H) * P.cgroups + 1);
+    P.p1_runs = (l1 - l0) * P.H * P.cgroups;
     if (l0 > 0 || l1 < P.L) {
         epk_cache_desc v = T.c;
         v.layers = l1 - l0;
@@ -889,19 +895,44 @@ static int tc_launch_p2(epk_ctx* ctx, const TcPlan& T, int l0, int l1) {
         int rc = make_layer_table(&v, &P.lt);
         if (rc) return rc;
         P.L = l1 - l0;
-        P.runs = P.L * P.H;
+        P.runs = mode == MODE_STATS ? P.p1_runs : P.L * P.H;
         P.head_off = T.c.head_off + int64_t(l0) * (P.H + 1);
         P.head_len = T.c.head_len + int64_t(l0) * P.H;
         if (P.hist_fine) {
             P.hist_fine += int64_t(l0) * 65536;
             P.hist_coarse += int64_t(l0) * 256;
         }
-        P.hk_base = l0 * P.H;
-        if ((rc = make_map(&tm_q, static_cast<const char*>(T.q) + l0 * T.qlayer, int64_t(P.L) * P.Hq * P.p, kChunk)))
+        if ((rc = make_map(tm_q, static_cast<const char*>(T.q) + l0 * T.qlayer, int64_t(P.L) * P.Hq * P.p, kChunk)))
+            return rc;
+        if (mode == MODE_STATS &&
+            (rc = make_map(tm_kp, static_cast<const char*>(T.kp) + l0 * T.kplayer, int64_t(P.L) * P.H * P.p, 128)))
             return rc;
     }
+    *out = P;
+    return EPK_OK;
+}
+
+// P1 over layers [l0, l1) of the plan's cache.
+static int tc_launch_p1(epk_ctx* ctx, const TcPlan& T, int l0, int l1) {
+    TcParams P;
+    CUtensorMap tm_q, tm_kp;
+    int rc = tc_view(T, MODE_STATS, l0, l1, &P, &tm_q, &tm_kp);
+    if (rc) return rc;
+    EPK_PROF(ctx, "p1_rowstats");
+    EPK_CUDA_CHECK(launch_pdl(T.stats_fn, dim3(T.grid), dim3(kThreadsStats), T.smem1, ctx->stream, P, T.tm_k, tm_q,
+                              tm_kp));
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
+// P2 over layers [l0, l1) (after tc_launch_p1 of the same range).
+static int tc_launch_p2(epk_ctx* ctx, const TcPlan& T, int l0, int l1) {
+    TcParams P;
+    CUtensorMap tm_q, tm_kp;
+    int rc = tc_view(T, MODE_SCORE, l0, l1, &P, &tm_q, &tm_kp);
+    if (rc) return rc;
     EPK_PROF(ctx, "p2_colscore");
-    EPK_CUDA_CHECK(launch_pdl(T.score_fn, dim3(ctx->num_sms), dim3(kThreads), T.smem2, ctx->stream, P, T.tm_k, tm_q,
+    EPK_CUDA_CHECK(launch_pdl(T.score_fn, dim3(T.grid), dim3(kThreads), T.smem2, ctx->stream, P, T.tm_k, tm_q,
                               T.tm_kp));
     EPK_LAUNCH_CHECK(ctx);
     return EPK_OK;
@@ -913,14 +944,14 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     TcPlan T;
     int rc = tc_plan(ctx, c, q, kp, hq, p, agg_max, scores, fs, &T);
     if (rc) return rc;
-    if ((rc = tc_launch_p1(ctx, T))) return rc;
+    if ((rc = tc_launch_p1(ctx, T, 0, c->layers))) return rc;
     return tc_launch_p2(ctx, T, 0, c->layers);
 }
 
-// One tensor-core block step with the fused selection: P1 over every layer,
-// then per layer group P2 -> threshold select on the context stream and
-// count/plan/gather on `side` (when given) so a group's compaction overlaps
-// the next group's P2 and select.
+// One tensor-core block step with the fused selection: per layer group
+// P1 -> P2 -> threshold select on the context stream and count/plan/gather on
+// `side` (when given) so a group's compaction overlaps the next group's
+// scoring.
 int launch_step_tc_grouped(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const void* q,
                            const void* kp, int hq, int p, int agg_max, const int64_t* budgets, int group,
                            cudaStream_t side, cudaEvent_t ev_fork, int out_slack, float* scores, uint8_t* keep,
@@ -933,11 +964,11 @@ int launch_step_tc_grouped(epk_ctx* ctx, const epk_cache_desc* in, const epk_cac
     TcPlan T;
     int rc = tc_plan(ctx, in, q, kp, hq, p, agg_max, scores, &fs_all, &T);
     if (rc) return rc;
-    if ((rc = tc_launch_p1(ctx, T))) return rc;
     const int L = in->layers;
     cudaStream_t main = ctx->stream;
     for (int l0 = 0; l0 < L; l0 += group) {
         const int l1 = std::min(L, l0 + group);
+        if ((rc = tc_launch_p1(ctx, T, l0, l1))) return rc;
         if ((rc = tc_launch_p2(ctx, T, l0, l1))) return rc;
         const epk_cache_desc vin = view_fn(in, l0, l1), vout = view_fn(out, l0, l1);
         const FusedSelect fs{fs_all.keys,
@@ -952,7 +983,11 @@ int launch_step_tc_grouped(epk_ctx* ctx, const epk_cache_desc* in, const epk_cac
             EPK_CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork, 0));
             ctx->stream = side;
         }
+        // the last group's compaction has no scoring left to overlap: all SMs
+        const int saved_ctas = ctx->gather_ctas;
+        if (l1 == L) ctx->gather_ctas = 0;
         rc = compact_fn(ctx, &vin, &vout, keep, out_slack, fs.keys, thr + 2 * l0, fs.hist_fine, fs.hist_coarse);
+        ctx->gather_ctas = saved_ctas;
         ctx->stream = main;
         if (rc) return rc;
     }

@@ -30,3 +30,21 @@ def test_plain_c_abi_step(gpu):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "abi_c_step ok" in r.stdout
+
+
+B_BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_build", "test_build")
+
+
+@pytest.mark.parametrize("nccl", [False, True])
+def test_cpp_multi_gpu_build_matches_reference(gpu, nccl):
+    """epikv::gpu::build (one thread + epk_ctx per device entry, episodes
+    round-robin, optional sharded k-means) writes the reference build's bytes;
+    with EPK_FORCE_NCCL=1 the one-device k-means chain goes through NCCL
+    (ncclCommInitAll + ncclBroadcast, libnccl.so.2 loaded at run time)."""
+    if not os.path.exists(B_BIN):
+        pytest.skip("C++ build driver not built (needs /root/reference at build time)")
+    env = dict(os.environ, EPK_FORCE_NCCL="1") if nccl else None
+    r = subprocess.run([B_BIN], capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "0 failed" in r.stdout

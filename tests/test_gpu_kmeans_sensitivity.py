@@ -98,3 +98,42 @@ def test_kmeans_sharded_device_ops_nccl_world1(gpu, orc):
         assert np.array_equal(np.array(r.sse_per_iteration), sse)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype,L,H,N,d", [(torch.bfloat16, 3, 2, 1000, 128), (torch.float32, 2, 3, 333, 128),
+                                           (torch.float64, 2, 1, 77, 128), (torch.float32, 2, 2, 150, 7),
+                                           (torch.bfloat16, 1, 1, 1, 8)])
+def test_sensitivity_ragged_tiles_and_skips(gpu, orc, dtype, L, H, N, d):
+    """The pair tiles (128 / 64 / 32 pairs by dtype, chunk-major over layers)
+    and the chain's 1,024-cosine ring slots with partial last tiles, rows not
+    16-byte multiples (the direct-read pair kernel), zero-norm pairs skipped
+    across tile and slot boundaries: bit-exact vs the oracle."""
+    torch.manual_seed(L * 100 + N)
+    kf = torch.randn(L, H, N, d, dtype=torch.float64, device="cuda").to(dtype)
+    kb = (kf.double() + 0.5 * torch.randn_like(kf.double())).to(dtype)
+    kb.view(L, -1, d)[:, ::97] = 0
+    kf.view(L, -1, d)[-1, -1] = 0
+    prof = gpu.sensitivity_from_keys(kf, kb)
+    sig, sk = orc.sensitivity(kf.double().cpu().numpy(), kb.double().cpu().numpy())
+    assert np.array_equal(np.asarray(prof.sigma), sig) and prof.skipped_zero_norm == sk
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3, 5])
+def test_kmeans_multi_device_chain(gpu, orc, shards):
+    """epk_kmeans_sharded: the ordered chain over `shards` contexts (one GPU,
+    device copies between shards) equals kmeans / the oracle bit for bit,
+    including an empty shard and the empty-cluster repair."""
+    from paper_2509_17396_b200.context import Context
+    rng = np.random.default_rng(shards)
+    pts = rng.standard_normal((700, 48)) + rng.integers(0, 4, (700, 1))
+    ctxs = [Context(0) for _ in range(shards)]
+    for k, p in ((5, pts), (6, np.repeat(pts[:4], 3, axis=0))):
+        r = gpu.kmeans_multi_device(p, k, 11, contexts=ctxs)
+        a, c, it, sse = orc.kmeans(p, k, 11)
+        assert r.assignments == a.tolist() and np.array_equal(r.centroids, c) and r.iterations == it
+        assert np.array_equal(np.array(r.sse_per_iteration), sse)
+    r = gpu.kmeans_multi_device(pts[:3], 3, 2, contexts=ctxs)  # fewer points than shards: empty shards
+    a, c, it, sse = orc.kmeans(pts[:3], 3, 2)
+    assert r.assignments == a.tolist() and np.array_equal(r.centroids, c)
+    for c_ in ctxs:
+        c_.close()
