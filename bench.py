@@ -49,6 +49,9 @@ CONFIGS = {
     "cfg2": dict(L=28, Hq=24, H=8, d=128, N=131072, block=2048, M=8192, p=128,
                  desc="cfg2 Llama-3.2-3B shape (28 layers, 24 Q / 8 KV heads, hd 128), 128K context, block 2048, "
                       "budget 8192/head, uniform layer budgets, p=128 patched-prompt rows, steady-state block step"),
+    "cfg3": dict(L=28, Hq=24, H=8, d=128, N=131072, block=2048, M=8192, p=128, E=4, adaptive=True,
+                 desc="cfg3 Llama-3.2-3B shape, E=4 episodes (K-means on 2,048 segment embeddings of dim 1,024), "
+                      "adaptive layer budgets allocate(sigma, 8192, alpha=1.1), block 2048, 128K context"),
     "cfg4": dict(L=32, Hq=32, H=8, d=128, N=262144, block=2048, M=8192, p=128,
                  desc="cfg4 Llama-3.1-8B shape (32 layers, 32 Q / 8 KV heads), 256K context, block 2048, budget 8192"),
     "cfg5": dict(L=28, Hq=28, H=4, d=128, N=1048576, block=4096, M=174762, p=128,
@@ -134,15 +137,36 @@ class ClockSampler:
 # workload
 # ---------------------------------------------------------------------------
 
+def synthetic_sigma(L, seed=11):
+    """A seeded per-layer key-similarity profile sigma_l (cfg3's adaptive
+    budgets): the same numbers for both arms, so the reference's allocate and
+    ours see identical inputs (SURVEY 7 hard part 10)."""
+    rng = np.random.default_rng(seed)
+    return (1.0 - rng.uniform(0.05, 0.6, L)).tolist()
+
+
+def layer_budgets(c):
+    """Per-layer per-head budgets: uniform M, or cfg3's allocate(sigma, M, 1.1)
+    (allocation.hpp:120-198, restated bit-for-bit in paper_2509_17396_b200.allocation)."""
+    if not c.get("adaptive"):
+        return [c["M"]] * c["L"]
+    from paper_2509_17396_b200.allocation import SensitivityProfile, allocate
+    sig = synthetic_sigma(c["L"])
+    prof = SensitivityProfile(sigma=sig, sensitivity=[1.0 - x for x in sig])
+    return list(allocate(prof, c["M"], 1.1).layer_budgets)
+
+
 def step_sizes(c):
-    n_h = c["M"] + c["block"]
-    live = c["L"] * c["H"] * n_h
-    keep = c["L"] * c["H"] * c["M"]
+    """(max live per head, live entries, kept entries) of ONE episode's steady-state step."""
+    bud = layer_budgets(c)
+    n_h = max(bud) + c["block"]
+    live = sum(c["H"] * (b + c["block"]) for b in bud)
+    keep = sum(c["H"] * b for b in bud)
     return n_h, live, keep
 
 
 def algorithmic(c):
-    """bytes / flops / exps per step (bf16)."""
+    """bytes / flops / exps per episode step (bf16)."""
     n_h, live, keep = step_sizes(c)
     d, G, p = c["d"], c["Hq"] // c["H"], c["p"]
     B = live * d * 2 + c["L"] * (c["Hq"] + c["H"]) * p * d * 2 + 4 * keep * d * 2 + 4 * live + 4 * keep
@@ -151,28 +175,58 @@ def algorithmic(c):
     return B, F, X
 
 
-def make_inputs(epk, torch, c, R, device, seed):
-    """R steady-state input caches (n_h = M + block live rows per head, dense)
-    and R prompt sets, bf16, resident in HBM."""
-    n_h, live, keep = step_sizes(c)
+def config_dict(c, c_total, world, shard):
+    """The workload description both arms print (identical dicts)."""
+    n_h, live, keep = step_sizes(c_total)
+    E = c_total.get("E", 1)
+    return {"workload": c_total["desc"], "layers": c_total["L"], "q_heads": c_total["Hq"], "kv_heads": c_total["H"],
+            "head_dim": c_total["d"], "context": c_total["N"], "block": c_total["block"],
+            "budget_per_head": c_total["M"], "layer_budgets": "adaptive" if c_total.get("adaptive") else "uniform",
+            "prompt_len": c_total["p"], "episodes": E, "live_entries_per_episode_step": live,
+            "kept_per_episode_step": keep, "aggregation": "max",
+            "parallelism": f"layers x{world} (one episode)" if shard else f"episodes over {world} GPU(s)",
+            "l2": "inputs larger than L2: >= 3 rotating steady-state caches of "
+                  f"{2 * live * c_total['d'] * 2 / 1e9:.2f} GB K+V per GPU"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def make_inputs(epk, torch, c, R, device, seed, dtype=None):
+    """R steady-state input caches (n_l = M_l + block live rows per head of
+    layer l, dense) and R prompt sets, resident in HBM (bf16 by default)."""
+    dtype = dtype or torch.bfloat16
+    bud = layer_budgets(c)
     L, H, d, p, Hq = c["L"], c["H"], c["d"], c["p"], c["Hq"]
-    cap = H * n_h
+    nl = [b + c["block"] for b in bud]
+    cap = [H * n for n in nl]
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     caches, qs, kps = [], [], []
-    pos_head = torch.sort(torch.randperm(c["N"], device=device, generator=g)[:n_h])[0].to(torch.int32)
+    pos_all = torch.sort(torch.randperm(c["N"], device=device, generator=g)[:max(nl)])[0].to(torch.int32)
     for r in range(R):
-        cc = epk.EpisodeCache(L, H, d, [cap] * L, torch.bfloat16, device)
-        cc.k.copy_(torch.randn(cc.rows, d, device=device, generator=g, dtype=torch.float32).to(torch.bfloat16))
-        cc.v.copy_(torch.randn(cc.rows, d, device=device, generator=g, dtype=torch.float32).to(torch.bfloat16))
-        cc.pos.copy_(pos_head.repeat(L * H))
-        off = (torch.arange(H + 1, device=device, dtype=torch.int32) * n_h).repeat(L, 1)
+        cc = epk.EpisodeCache(L, H, d, cap, dtype, device)
+        cc.k.copy_(torch.randn(cc.rows, d, device=device, generator=g, dtype=torch.float32).to(dtype))
+        cc.v.copy_(torch.randn(cc.rows, d, device=device, generator=g, dtype=torch.float32).to(dtype))
+        for l in range(L):
+            b = int(cc.layer_base[l])
+            cc.pos[b:b + H * nl[l]].copy_(torch.sort(pos_all[:nl[l]])[0].repeat(H))
+        off = torch.stack([torch.arange(H + 1, device=device, dtype=torch.int32) * n for n in nl])
         cc.head_off.copy_(off)
-        cc.head_len.fill_(n_h)
+        cc.head_len.copy_(torch.tensor(nl, device=device, dtype=torch.int32)[:, None].expand(L, H))
         caches.append(cc)
-        qs.append(torch.randn(L, Hq, p, d, device=device, generator=g).to(torch.bfloat16))
-        kps.append(torch.randn(L, H, p, d, device=device, generator=g).to(torch.bfloat16))
-    out = epk.EpisodeCache(L, H, d, [cap] * L, torch.bfloat16, device)
+        qs.append(torch.randn(L, Hq, p, d, device=device, generator=g).to(dtype))
+        kps.append(torch.randn(L, H, p, d, device=device, generator=g).to(dtype))
+    out = epk.EpisodeCache(L, H, d, cap, dtype, device)
     return caches, qs, kps, out
 
 
@@ -183,44 +237,59 @@ def run_ours(args, c, rank, world, device, torch, dist):
     ctx = epk.default_context(device.index)
     ctx.set_option(layer_group=args.layer_group, overlap=not args.no_overlap)
     n_h, live, keep = step_sizes(c)
-    R = 3
-    caches, qs, kps, out = make_inputs(epk, torch, c, R, device, 1234 + rank)
-    budgets = [c["M"]] * c["L"]
-    plans = [StepPlan(caches[r], out, budgets) for r in range(R)]
+    # this rank's episodes (episodes round-robin over the GPUs)
+    n_ep = len(range(rank, c.get("E", 1), world)) if not args.total_live else 1
+    R = max(1, -(-3 // max(1, n_ep)))  # >= 3 distinct input caches per GPU: every step reads cold K/V
+    eps = []
+    for e in range(n_ep):
+        caches, qs, kps, out = make_inputs(epk, torch, c, R, device, 1234 + 97 * rank + e)
+        eps.append((caches, qs, kps, out))
+    budgets = layer_budgets(c)
+    plans = [[StepPlan(cs[r], out, budgets) for r in range(R)] for cs, _, _, out in eps]
 
     def step(i):
         r = i % R
-        evict_step(caches[r], out, qs[r], kps[r], budgets, mode="tc_bf16", slack=c["block"], n_max_per_head=n_h,
-                   plan=plans[r], ctx=ctx)
+        for e, (caches, qs, kps, out) in enumerate(eps):
+            evict_step(caches[r], out, qs[r], kps[r], budgets, mode="tc_bf16", slack=c["block"], n_max_per_head=n_h,
+                       plan=plans[e][r], ctx=ctx)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
     ctx.poll_error()
     stream = torch.cuda.current_stream(device)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(device.index)
-    clocks.start()
-    time.sleep(0.3)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = ctx.launches
-    ev0.record(stream)
-    for i in range(args.steps):
-        step(i)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    launches = ctx.launches - launches0
-    clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], device=device, dtype=torch.float64)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    ctx.poll_error()
+
+    def timed(steps):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks = ClockSampler(device.index)
+        clocks.start()
+        time.sleep(0.3)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = ctx.launches
+        ev0.record(stream)
+        for i in range(steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        launches = ctx.launches - launches0
+        clk = clocks.stop()
+        t = torch.tensor([ev0.elapsed_time(ev1)], device=device, dtype=torch.float64)
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ctx.poll_error()
+        return float(t.item()), launches, clk
+
+    ms_max, launches, clk = timed(args.steps)
+    # the same step over a long power-capped run (clocks settle under the 1 kW cap)
+    sustained = None
+    if args.sustained_steps > 0:
+        s_ms, _, s_clk = timed(args.sustained_steps)
+        sustained = {"steps": args.sustained_steps, "ms_per_step": s_ms / args.sustained_steps,
+                     "value": None, "clocks": s_clk}
 
     # per-kernel live timing: a separate pass with events around every launch
     prof_steps = min(args.steps, 30)
@@ -248,8 +317,87 @@ def run_ours(args, c, rank, world, device, torch, dist):
             f.write("# kernel  start_ms  dur_ms  stream(0 main, 1 side)\n")
             for name, t0, d, side in tl:
                 f.write(f"{name:16s} {t0:9.4f} {d:8.4f} {side}\n")
+    del eps, plans
+    torch.cuda.empty_cache()
+    exact = run_exact_f32(args, c, epk, torch, device, ctx, dist) if not args.no_exact else None
     e2e = run_e2e(args, c, epk, torch, device, ctx, dist) if not args.no_e2e else None
-    return dict(ms=ms_max, launches=launches, clocks=clk, kernels=kernels, e2e=e2e, live=live, keep=keep)
+    phase_a = run_phase_a(c, epk, torch, device) if c.get("E", 1) > 1 and rank == 0 else None
+    return dict(ms=ms_max, launches=launches, clocks=clk, kernels=kernels, e2e=e2e, live=live * n_ep, keep=keep,
+                sustained=sustained, exact=exact, phase_a=phase_a, episodes=n_ep)
+
+
+def run_exact_f32(args, c, epk, torch, device, ctx, dist):
+    """The precision-matched path: the same step with fp32 K/V/Q through the
+    EPK-F32 parity scorer (bit-exact with the CPU restatement) and the generic
+    pooled select -- the throughput a user gets with bit-exact retained sets."""
+    from paper_2509_17396_b200.step import StepPlan, evict_step
+    n_h, live, keep = step_sizes(c)
+    caches, qs, kps, out = make_inputs(epk, torch, c, 2, device, 4321, dtype=torch.float32)
+    budgets = layer_budgets(c)
+    plans = [StepPlan(caches[r], out, budgets) for r in range(2)]
+    steps = max(2, min(args.steps, 6))
+
+    def step(i):
+        evict_step(caches[i % 2], out, qs[i % 2], kps[i % 2], budgets, mode="exact_f32", slack=c["block"],
+                   n_max_per_head=n_h, plan=plans[i % 2], ctx=ctx)
+
+    step(0)
+    torch.cuda.synchronize()
+    ctx.poll_error()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    e0.record()
+    for i in range(steps):
+        step(i)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device=device, dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    world = dist.get_world_size() if dist is not None else 1
+    units = getattr(args, "total_live", None) or world * live
+    ms = float(t.item()) / steps
+    del caches, qs, kps, out, plans
+    torch.cuda.empty_cache()
+    return {"value": units / (ms / 1000.0), "unit": UNIT, "ms_per_step": ms, "steps": steps, "dtype": "f32",
+            "path": "epk_evict_step mode EPK_SCORE_EXACT_F32 (score_f32.cu) -> generic pooled select -> compaction; "
+                    "retained sets bit-exact vs the CPU restatement"}
+
+
+def run_phase_a(c, epk, torch, device):
+    """cfg3's one-time Phase A on this GPU (episodic.hpp:117-146): K-means of
+    2,048 segment embeddings (dim 1,024, k = E) and the layer-sensitivity
+    reduction at the calibration size N_cal = max(4M, 256) (episodic.hpp:138-140),
+    then allocate(sigma, M, 1.1)."""
+    rng = np.random.default_rng(3)
+    E = c["E"]
+    pts = rng.standard_normal((E, 1024))[rng.integers(0, E, 2048)] + 0.7 * rng.standard_normal((2048, 1024))
+    epk.kmeans(pts, E, 1)
+    t0 = time.perf_counter()
+    km = epk.kmeans(pts, E, 1)
+    km_ms = (time.perf_counter() - t0) * 1e3
+    ncal = max(4 * c["M"], 256)
+    g = torch.Generator(device=device).manual_seed(5)
+    kf = torch.randn(c["L"], c["H"], ncal, c["d"], device=device, generator=g).bfloat16()
+    noise = torch.linspace(0.1, 0.8, c["L"], device=device).view(-1, 1, 1, 1)
+    kb = (kf.float() + noise * torch.randn(kf.shape, device=device, generator=g)).bfloat16()
+    epk.sensitivity_from_keys(kf, kb)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    prof = epk.sensitivity_from_keys(kf, kb)
+    e1.record()
+    torch.cuda.synchronize()
+    alloc = epk.allocate(prof, c["M"], 1.1)
+    del kf, kb
+    torch.cuda.empty_cache()
+    return {"kmeans_2048x1024": {"k": E, "ms": km_ms, "iterations": km.iterations,
+                                 "us_per_lloyd_iteration": 1e3 * km_ms / max(1, km.iterations)},
+            "sensitivity": {"tokens": ncal, "ms": e0.elapsed_time(e1),
+                            "key_bytes": 2 * c["L"] * c["H"] * ncal * c["d"] * 2},
+            "allocate_from_measured_sigma": alloc.layer_budgets,
+            "bench_layer_budgets": layer_budgets(c)}
 
 
 def run_e2e(args, c, epk, torch, device, ctx, dist):
@@ -356,11 +504,12 @@ def run_e2e(args, c, epk, torch, device, ctx, dist):
 # reference CPU path (oracle/_ref = the reference headers compiled in place)
 # ---------------------------------------------------------------------------
 
-def ref_layer_inputs(c, layer_seed):
+def ref_layer_inputs(c, layer, layer_seed):
     """One steady-state layer of the same synthetic distribution, fp64
     (bf16-rounded values, as the GPU sees them)."""
     from tests.helpers import bf16_round
-    n_h, _, _ = step_sizes(c)
+    M_l = layer_budgets(c)[layer]
+    n_h = M_l + c["block"]
     H, d, p, Hq = c["H"], c["d"], c["p"], c["Hq"]
     rng = np.random.default_rng(layer_seed)
     ho = (np.arange(H + 1) * n_h).astype(np.int64)
@@ -368,13 +517,14 @@ def ref_layer_inputs(c, layer_seed):
     k = bf16_round(rng.standard_normal((H * n_h, d)).astype(np.float32)).astype(np.float64)
     q = bf16_round(rng.standard_normal((Hq, p, d)).astype(np.float32)).astype(np.float64)
     kp = bf16_round(rng.standard_normal((H, p, d)).astype(np.float32)).astype(np.float64)
-    return ho, pos, q, k, kp
+    return ho, pos, q, k, kp, M_l
 
 
-def ref_sample(c, units, threads):
-    """Runs `units` layer-steps of the reference CPU path (restated attention
-    grid -> epikv::score_with_prompt -> epikv::evict_to_budget) on `threads`
-    host threads; returns (tokens, seconds, kind)."""
+def ref_units(c, units, threads, seed0=1000):
+    """Runs the reference CPU path (restated fp64 attention grid ->
+    epikv::score_with_prompt -> epikv::evict_to_budget, oracle/_ref = the
+    reference headers compiled in place) over `units` = [(layer, seed)] on
+    `threads` host threads; returns (tokens, seconds, kind)."""
     from oracle import oracle as O
     kind = "reference"
     try:
@@ -383,25 +533,20 @@ def ref_sample(c, units, threads):
     except Exception:
         kind = "port"
         fn = None
-    inputs = [ref_layer_inputs(c, 1000 + u) for u in range(units)]
-    n_h, _, _ = step_sizes(c)
-    tokens = units * c["H"] * n_h
-    results = [None] * units
+    inputs = [ref_layer_inputs(c, l, seed0 + sd) for l, sd in units]
+    tokens = sum(int(x[0][-1]) for x in inputs)
 
     def work(u):
-        ho, pos, q, k, kp = inputs[u]
+        ho, pos, q, k, kp, M_l = inputs[u]
         keep = np.zeros(len(pos), np.uint8)
         if fn is not None:
-            rc = fn(c["Hq"], c["H"], c["d"], c["p"], c["M"], ho, pos, q, k.ctypes.data_as(O.C.c_void_p),
-                    k.ctypes.data_as(O.C.c_void_p), kp, 1, keep)
-            results[u] = int(rc)
+            fn(c["Hq"], c["H"], c["d"], c["p"], M_l, ho, pos, q, k.ctypes.data_as(O.C.c_void_p),
+               k.ctypes.data_as(O.C.c_void_p), kp, 1, keep)
         else:
-            s = O.score_layer_f64(q, k, kp, ho, True)
-            results[u] = O.evict_layer(ho, pos, s, c["M"])[0]
+            sc = O.score_layer_f64(q, k, kp, ho, True)
+            O.evict_layer(ho, pos, sc, M_l)
 
-    t0 = time.perf_counter()
-    ths = []
-    it = iter(range(units))
+    it = iter(range(len(units)))
     lock = threading.Lock()
 
     def worker():
@@ -412,10 +557,10 @@ def ref_sample(c, units, threads):
                 return
             work(u)
 
-    for _ in range(threads):
-        th = threading.Thread(target=worker)
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=worker) for _ in range(max(1, threads))]
+    for th in ths:
         th.start()
-        ths.append(th)
     for th in ths:
         th.join()
     return tokens, time.perf_counter() - t0, kind
@@ -428,29 +573,54 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def run_reference(args, c, rank):
+def cpu_baseline(c):
+    """The reference CPU path on this box's host cores, bounded: one whole
+    steady-state step (every layer) on all host threads, and a 2-layer sample
+    on one thread."""
+    cores = cpu_cores()
+    L = c["L"]
+    tok_n, sec_n, kind = ref_units(c, [(l, l) for l in range(L)], cores)
+    tok_1, sec_1, _ = ref_units(c, [(0, 0), (1 % L, 1)], 1)
+    return {"value": tok_n / sec_n, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+            "value_1_thread": tok_1 / sec_1,
+            "sample": f"{cores} threads: one whole steady-state step ({L} layers x {c['H']} heads, "
+                      f"p={c['p']}) in {sec_n:.1f} s; 1 thread: 2 of {L} layer-steps in {sec_1:.1f} s "
+                      "(per-step throughput, the metric's unit; whole runs not timed): restated fp64 attention -> "
+                      "epikv::score_with_prompt -> epikv::evict_to_budget (oracle/_ref)"}
+
+
+def run_reference(args, c, rank, config):
+    """--impl reference: the reference's own CPU path on all host threads, K
+    timed steps after W warm-up steps.  A step is one steady-state block step
+    over every layer when K such steps fit ~3 minutes of host time, else a
+    per-step sample of layers (stated in `sample`)."""
     if rank != 0:
         return None
     cores = cpu_cores()
-    units = min(c["L"], cores)
-    for _ in range(min(args.warmup, 1)):
-        ref_sample(c, min(units, 2), min(units, 2))
-    steps = max(1, min(args.steps, 3))
-    rates = []
-    kind = "reference"
-    for _ in range(steps):
-        tok, sec, kind = ref_sample(c, units, units)
-        rates.append(tok / sec)
-    v = float(np.median(rates))
-    sample = (f"{units} of {c['L']} layers of one steady-state cfg block step ({c['H']} heads x "
-              f"{c['M'] + c['block']} live entries each, p={c['p']}), one layer per host thread, "
-              f"{steps} step(s); attention restated in fp64 -> epikv::score_with_prompt -> epikv::evict_to_budget")
-    return dict(metric=METRIC, value=v, unit=UNIT, impl="reference", n_gpus=args.gpus, steps=steps,
-                warmup=min(args.warmup, 1), ms_per_step=1000.0 * c["L"] * c["H"] * (c["M"] + c["block"]) / v,
+    L, E = c["L"], c.get("E", 1)
+    t_unit = None
+    for w in range(args.warmup):  # warm-up: one layer-step each (the first one sizes the steps)
+        tok, sec, _ = ref_units(c, [(w % L, 500 + w)], 1)
+        t_unit = sec if t_unit is None else min(t_unit, sec)
+    if t_unit is None:
+        tok, t_unit, _ = ref_units(c, [(0, 500)], 1)
+    budget_s = 180.0
+    whole = L * E
+    per_step = whole if args.steps * whole * t_unit / cores <= budget_s else \
+        max(1, min(whole, int(budget_s * cores / (args.steps * t_unit))))
+    units = [((u % whole) % L, s * whole + u) for s in range(args.steps) for u in range(per_step)]
+    tok, sec, kind = ref_units(c, units, cores)
+    v = tok / sec
+    sample = (f"each of {args.steps} steps: " + (f"one whole block step ({L} layers" + (f" x {E} episodes" if E > 1 else "")
+                                                + ")" if per_step == whole else f"{per_step} of {whole} layer-steps")
+              + f" ({c['H']} heads x M_l + {c['block']} live entries, p={c['p']}) on {cores} host threads "
+              f"({cpu_model()}); restated fp64 attention -> epikv::score_with_prompt -> epikv::evict_to_budget")
+    return dict(metric=METRIC, value=v, unit=UNIT, impl="reference", n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1000.0 * step_sizes(c)[1] * E / v,
                 higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
-                config={"workload": c["desc"], "layers": c["L"], "q_heads": c["Hq"], "kv_heads": c["H"],
-                        "head_dim": c["d"], "block": c["block"], "budget_per_head": c["M"], "prompt_len": c["p"]},
-                cpu_baseline={"value": v, "unit": UNIT, "cores": units, "kind": kind, "sample": sample},
+                config=config,
+                cpu_baseline={"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                              "cpu_model": cpu_model()},
                 e2e={"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
 
 
@@ -473,7 +643,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--sustained-steps", type=int, default=1000,
+                    help="a second, long timed run of the same step (power-capped clocks); 0 = skip")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-exact", action="store_true", help="skip the precision-matched fp32 step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layer-group", type=int, default=0, help="layers per P2/select/compaction group (0 = all layers)")
     ap.add_argument("--no-overlap", action="store_true", help="compaction on the main stream")
@@ -490,9 +663,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    shard = args.shard_layers and world > 1
+    if "E" not in c:
+        c["E"] = world if not shard else 1  # weak scaling: one episode per GPU
+    config = config_dict(c, c, world, shard)
 
     if args.impl == "reference":
-        res = run_reference(args, c, rank)
+        res = run_reference(args, dict(c, E=1), rank, config)  # per-step throughput of one episode's step
         if res is not None:
             print(json.dumps(res), flush=True)
         return
@@ -511,9 +688,8 @@ def main():
         else:
             td.init_process_group("nccl", device_id=device)
         dist = td
-    # episodes are the natural shard (one per rank, weak scaling);
-    # --shard-layers splits one episode's layers instead (strong scaling)
-    shard = args.shard_layers and world > 1
+    # episodes are the natural shard (round-robin over the ranks,
+    # weak scaling); --shard-layers splits one episode's layers instead (strong)
     c_total = c
     if shard:
         l0, l1 = c["L"] * rank // world, c["L"] * (rank + 1) // world
@@ -521,19 +697,22 @@ def main():
     args.total_live = step_sizes(c_total)[1] if shard else None
     r = run_ours(args, c, rank, world, device, torch, dist)
     hbm, tc_sus, tc_burst, peak_src = load_peaks()
-    B, F, X = algorithmic(c)  # per GPU
+    n_ep = r["episodes"]
+    B1, F1, X1 = algorithmic(c)
+    B, F, X = B1 * n_ep, F1 * n_ep, X1 * n_ep  # this GPU's work per step
     ms = r["ms"]
     step_ms = ms / args.steps
-    value = (args.total_live or world * r["live"]) * args.steps / (ms / 1000.0)
-    # dominant kernel (largest share of the step) and its roofline
+    units_all = args.total_live or c_total["E"] * step_sizes(c_total)[1]  # every rank's episodes
+    value = units_all * args.steps / (ms / 1000.0)
     kernels = r["kernels"]
     G, p, d, L, H = c["Hq"] // c["H"], c["p"], c["d"], c["L"], c["H"]
     n_h, live, keep = step_sizes(c)
+    live, keep = live * n_ep, keep * n_ep
     # per-kernel algorithmic work per step: bound, amount, unit, peak
     sfu_peak = 4.63e12  # measured MUFU.EX2 rate (profiles/mufu_rate_r01.txt)
     work = {
-        "p1_rowstats": ("sfu", G * p * (live + L * H * p) / 1e12, "Tex2/s", sfu_peak / 1e12),
-        "p2_colscore": ("tensor", 2.0 * G * p * d * live / 1e12, "TFLOP/s", tc_sus),
+        "p1_rowstats": ("sfu", G * p * (live + L * H * p * n_ep) / 1e12, "Tex2/s", sfu_peak / 1e12),
+        "p2_colscore": ("tensor", 2.0 * G * p * d * live / 1e12, "TFLOP/s", tc_burst),
         "compact_gather": ("hbm", (4.0 * keep * d * 2 + 8.0 * keep + live) / 1e9, "GB/s", hbm),
         "select": ("hbm", (4.0 * live) / 1e9, "GB/s", hbm),
         "compact_count": ("hbm", (4.0 * live + live) / 1e9, "GB/s", hbm),
@@ -542,8 +721,8 @@ def main():
         if k in kernels and kernels[k]["ms_per_step"] > 0:
             ach = amount / (kernels[k]["ms_per_step"] / 1000.0)
             kernels[k].update({"bound": bound, "achieved": ach, "unit": unit, "peak": peak, "frac": ach / peak})
-    dom = max((k for k in kernels if k in work and work[k][0] in ("hbm", "tensor")),
-              key=lambda k: kernels[k]["ms_per_step"], default=None)
+    # dominant kernel: the largest share of the step, whatever unit bounds it
+    dom = max((k for k in kernels if k in work), key=lambda k: kernels[k]["ms_per_step"], default=None)
     roof = None
     if dom is not None:
         bound, amount, unit, peak = work[dom]
@@ -552,37 +731,33 @@ def main():
         amount = amount / nl  # the work of ONE launch (a layer group)
         ach = amount / (kms / 1000.0)
         roof = {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                "traffic": traffic_from_profiles(dom), "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"
-                if peak_src == "measured" else "fallback (B200_PROFILING.md)",
+                "traffic": traffic_from_profiles(dom) if bound == "hbm" else None,
+                "peak_source": (f"{peak_src} (MEASURED_PEAKS.json)" if peak_src == "measured"
+                                else "fallback (B200_PROFILING.md)") if bound != "sfu"
+                else "measured MUFU.EX2 microbenchmark (profiles/mufu_rate_r01.txt)",
                 "algorithmic_per_launch": amount * (1e9 if unit == "GB/s" else 1e12), "ms_per_launch": kms}
     step_roof = {"bound": "hbm", "algorithmic_bytes": B, "achieved": B / (step_ms / 1000.0) / 1e9, "peak": hbm,
                  "unit": "GB/s", "frac": B / (step_ms / 1000.0) / 1e9 / hbm,
                  "tensor_flops_single_pass": F, "exps": X,
-                 "bound_times_ms": {"hbm": B / hbm / 1e6, "tensor": F / tc_sus / 1e9}}
+                 "bound_times_ms": {"hbm": B / hbm / 1e6, "tensor_burst": F / tc_burst / 1e9,
+                                    "sfu": X / sfu_peak * 1e3}}
+    sus = r["sustained"]
+    if sus is not None:
+        sus["value"] = units_all / (sus["ms_per_step"] / 1000.0)
+        sus["step_roofline_frac"] = B / (sus["ms_per_step"] / 1000.0) / 1e9 / hbm
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        units = min(4, L)
-        tok, sec, kind = ref_sample(c, units, units)
-        cpu = {"value": tok / sec, "unit": UNIT, "cores": units, "kind": kind,
-               "sample": f"{units} layer-steps of the cfg shape ({H} heads x {n_h} live entries, p={p}), "
-                         f"one per host thread: fp64 attention restatement -> epikv::score_with_prompt -> "
-                         f"epikv::evict_to_budget (oracle/_ref)"}
+        cpu = cpu_baseline(dict(c, E=1))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": c["desc"], "layers": c_total["L"], "q_heads": c["Hq"], "kv_heads": H, "head_dim": d,
-                       "context": c["N"], "block": c["block"], "budget_per_head": c["M"], "prompt_len": p,
-                       "live_entries_per_step": step_sizes(c_total)[1], "kept_per_step": step_sizes(c_total)[2],
-                       "score_mode": "tc_bf16", "aggregation": "max",
-                       "episodes_per_gpu": 1 if not shard else 1.0 / world,
-                       "parallelism": f"layers x{world} (one episode)" if shard else f"episodes x{world}",
-                       "l2": "inputs larger than L2: 3 rotating steady-state caches of "
-                             f"{2 * live * d * 2 / 1e9:.2f} GB K+V each"},
+            "config": config, "score_mode": "tc_bf16", "episodes_per_gpu": n_ep,
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels, "cpu_baseline": cpu,
             "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
+            "sustained": sus, "exact_f32": r["exact"], "phase_a": r["phase_a"],
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -14,6 +14,10 @@
 // skipped: per-pair cosines in the reference's operation order, then each
 // layer's (h, t)-ordered running sum (see cosine_pair_kernel / cosine_mean_kernel).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "epk_internal.cuh"
 #include "sm100.cuh"
@@ -276,6 +280,7 @@ __global__ void __launch_bounds__(K5Shape<T>::TR) cosine_pair_kernel(const __gri
         }
     }
     if (int(threadIdx.x) < nrows) P.cosv[int64_t(layer) * P.cos_stride + r0 + threadIdx.x] = finish_cosine(na, nb, dot);
+    __threadfence();  // every writer's cosine is visible device-wide before the tile's flag
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -290,6 +295,13 @@ constexpr int kChainStages = 4;
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// An L2 load the compiler may not hoist above the flag wait (__ldcg is not
+// volatile and can move across it).
+__device__ __forceinline__ double ld_cg_ordered(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -317,30 +329,41 @@ __global__ void __launch_bounds__(64) cosine_chain_kernel(const __grid_constant_
             sm100::mbar_wait(&empty[s], (uint32_t(c / kChainStages) & 1u) ^ 1u);
             const int64_t i0 = c * kChainChunk;
             const int n = int(min(int64_t(kChainChunk), P.rows - i0));
-            if (lane == 0 && !timed_out) {  // wait until every tile of this chunk is published (bounded)
-                const int64_t t1 = (i0 + n - 1) / tr;
-                for (int64_t t = i0 / tr; t <= t1; ++t) {
-                    long spins = 0;
-                    while (ld_acquire_u32(ready + t) == 0u) {
-                        if (++spins > (1l << 25)) {
-                            atomicCAS(P.err_flag, 0, EPK_ERR_CUDA);
+            if (!timed_out) {  // every tile of this chunk published? lane j watches tile t0 + j (bounded wait)
+                const int64_t t0 = i0 / tr, nt = (i0 + n - 1) / tr - t0 + 1;
+                for (int64_t tb = 0; tb < nt; tb += 32) {
+                    const bool mine = tb + lane < nt;
+                    unsigned long long t_start = 0, t_now = 0;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+                    while (!__all_sync(0xffffffffu, !mine || ld_acquire_u32(ready + t0 + tb + lane) != 0u)) {
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+                        if (t_now - t_start > 4000000000ull) {  // 4 s without progress: give up, flag the error
+                            if (lane == 0) atomicCAS(P.err_flag, 0, EPK_ERR_CUDA);
                             timed_out = true;
                             break;
                         }
-                        __nanosleep(64);
+                        __nanosleep(32);
                     }
                     if (timed_out) break;
                 }
-                __threadfence();
             }
             __syncwarp();
+            __threadfence();  // every lane ordered after the flags its neighbours acquired
+            // all of the chunk's loads in flight at once (32 per lane), then
+            // the order-preserving NaN compaction
+            double xs[kChainChunk / 32];
+#pragma unroll
+            for (int u = 0; u < kChainChunk / 32; ++u) {
+                const int i = u * 32 + lane;
+                xs[u] = i < n ? ld_cg_ordered(v + i0 + i) : 0.0;
+            }
             int base = 0, sk = 0;
-            for (int j = 0; j < n; j += 32) {
-                const int i = j + lane;
-                const double x = i < n ? __ldcg(v + i0 + i) : 0.0;
-                const bool ok = i < n && x == x;
+#pragma unroll
+            for (int u = 0; u < kChainChunk / 32; ++u) {
+                const int i = u * 32 + lane;
+                const bool ok = i < n && xs[u] == xs[u];
                 const unsigned bal = __ballot_sync(0xffffffffu, ok);
-                if (ok) ring[s][base + __popc(bal & ((1u << lane) - 1u))] = x;
+                if (ok) ring[s][base + __popc(bal & ((1u << lane) - 1u))] = xs[u];
                 base += __popc(bal);
                 sk += __popc(__ballot_sync(0xffffffffu, i < n && !ok));
             }
@@ -384,6 +407,22 @@ __global__ void cosine_skip_total_kernel(const int64_t* per_layer, int layers, i
         for (int l = 0; l < layers; ++l) t += per_layer[l];
         if (skipped) *skipped = t;
     }
+}
+
+// With lazy module loading, the first launch of a kernel may wait for the
+// kernels already running; the pair kernels must therefore be loaded before
+// the chain kernel that spins on their flags starts.
+static int k5_preload() {
+    cudaFuncAttributes fa;
+    EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, cosine_pair_kernel<double, true>));
+    EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, cosine_pair_kernel<double, false>));
+    EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, cosine_pair_kernel<float, true>));
+    EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, cosine_pair_kernel<float, false>));
+    EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, cosine_pair_kernel<__nv_bfloat16, true>));
+    EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, cosine_pair_kernel<__nv_bfloat16, false>));
+    EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, cosine_chain_kernel));
+    EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, cosine_skip_total_kernel));
+    return EPK_OK;
 }
 
 template <typename T>
@@ -430,7 +469,7 @@ int launch_key_cosine(epk_ctx* ctx, const void* kf, const void* kb, int dtype, i
     P.ready = carve.take<unsigned>(tiles * layers);
     P.sigma = sigma;
     P.err_flag = ctx->err_flag;
-    if ((rc = ensure_aux_stream(ctx))) return rc;
+    if ((rc = ensure_aux_stream(ctx)) || (rc = k5_preload())) return rc;
     cudaStream_t main = ctx->stream;
     EPK_CUDA_CHECK(cudaMemsetAsync(P.ready, 0, size_t(tiles * layers) * 4, main));
     // the chain CTAs follow the pair tiles' ready flags from the aux stream

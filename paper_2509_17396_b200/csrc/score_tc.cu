@@ -105,6 +105,7 @@ struct TcParams {
     int p1_runs;    // STATS runs
     int slots;      // partial slots per query row (kStatGroups per STATS CTA)
     int hk_base;    // global (layer, head) index of this launch's first head (rows of part_m / part_z)
+    int run_hk_base;  // SCORE: heads of the P1 launch (its layer range) before this launch's first head
     const int32_t* head_off;
     const int32_t* head_len;
     int32_t* p1_pre;  // [p1_runs + 1] run prefix of the STATS launch over this layer range (its CTA 0 writes it)
@@ -257,7 +258,7 @@ __device__ __forceinline__ float merge_slots(const float* pm, const float* pz, c
 // every P1 CTA that covered the row's run (general path: any number of P1 CTAs).
 __device__ float merge_lse2(const TcParams& P, int hk, int rq, int64_t T1) {
     const int cg = (rq / kChunk) / P.cg_chunks;
-    const int run = hk * P.cgroups + cg;
+    const int run = (hk + P.run_hk_base) * P.cgroups + cg;
     const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
     if (R1 <= R0) return INFINITY;
     const int b0 = part_cnt(T1, P.p1_grid, R0) - 1, b1 = part_cnt(T1, P.p1_grid, R1 - 1) - 1;
@@ -591,7 +592,7 @@ __global__ void __maxnreg__(128)
                     named_bar_sync(1, 32 * kEpiWarps);
                     if (P.keys && lkey >= 0 && lkey / P.H != x.l) flush_coarse(P, lkey / P.H, s_coarse, etid);
                     if (etid < P.cgroups) {  // slot list of each P1 run (head, chunk group)
-                        const int run = x.hk * P.cgroups + etid;  // the P1 launch of this layer range
+                        const int run = (x.hk + P.run_hk_base) * P.cgroups + etid;  // in the P1 launch's run order
                         const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
                         int n = 0;
                         if (R1 > R0) {
@@ -755,6 +756,7 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.hist_coarse = fs ? fs->hist_coarse : nullptr;
     P.ptiles = (p + 127) / 128;
     P.hk_base = 0;
+    P.run_hk_base = 0;
     const int grid = score_grid(ctx);  // persistent: one CTA per SM, tile-balanced ranges
 
     // STATS kernels by exp2 split (POLY of every 4 column pairs on the FMA
@@ -880,14 +882,22 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
 }
 
 // The plan's parameters of one pass restricted to layers [l0, l1), with its
-// query (and, for P1, prompt-key) tensor maps re-based to layer l0.
-static int tc_view(const TcPlan& T, int mode, int l0, int l1, TcParams* out, CUtensorMap* tm_q, CUtensorMap* tm_kp) {
+// query (and, for P1, prompt-key) tensor maps re-based to layer l0.  A P2
+// view names the layer range [p0, p1) of the P1 launch whose partials it reads
+// (P1 may cover more layers than one P2 launch).
+static int tc_view(const TcPlan& T, int mode, int l0, int l1, int p0, int p1, TcParams* out, CUtensorMap* tm_q,
+                   CUtensorMap* tm_kp) {
     TcParams P = mode == MODE_STATS ? T.P1 : T.P2;
     *tm_q = T.tm_q;
     *tm_kp = T.tm_kp;
+    if (mode == MODE_STATS) {
+        p0 = l0;
+        p1 = l1;
+    }
     P.hk_base = l0 * P.H;
-    P.p1_pre = T.p1_pre_all + int64_t(l0) * (int64_t(P.H) * P.cgroups + 1);
-    P.p1_runs = (l1 - l0) * P.H * P.cgroups;
+    P.run_hk_base = (l0 - p0) * P.H;
+    P.p1_pre = T.p1_pre_all + int64_t(p0) * (int64_t(P.H) * P.cgroups + 1);
+    P.p1_runs = (p1 - p0) * P.H * P.cgroups;
     if (l0 > 0 || l1 < P.L) {
         epk_cache_desc v = T.c;
         v.layers = l1 - l0;
@@ -916,7 +926,7 @@ static int tc_view(const TcPlan& T, int mode, int l0, int l1, TcParams* out, CUt
 static int tc_launch_p1(epk_ctx* ctx, const TcPlan& T, int l0, int l1) {
     TcParams P;
     CUtensorMap tm_q, tm_kp;
-    int rc = tc_view(T, MODE_STATS, l0, l1, &P, &tm_q, &tm_kp);
+    int rc = tc_view(T, MODE_STATS, l0, l1, l0, l1, &P, &tm_q, &tm_kp);
     if (rc) return rc;
     EPK_PROF(ctx, "p1_rowstats");
     EPK_CUDA_CHECK(launch_pdl(T.stats_fn, dim3(T.grid), dim3(kThreadsStats), T.smem1, ctx->stream, P, T.tm_k, tm_q,
@@ -925,11 +935,11 @@ static int tc_launch_p1(epk_ctx* ctx, const TcPlan& T, int l0, int l1) {
     return EPK_OK;
 }
 
-// P2 over layers [l0, l1) (after tc_launch_p1 of the same range).
-static int tc_launch_p2(epk_ctx* ctx, const TcPlan& T, int l0, int l1) {
+// P2 over layers [l0, l1), after the P1 launch over [p0, p1) (a superset).
+static int tc_launch_p2(epk_ctx* ctx, const TcPlan& T, int l0, int l1, int p0, int p1) {
     TcParams P;
     CUtensorMap tm_q, tm_kp;
-    int rc = tc_view(T, MODE_SCORE, l0, l1, &P, &tm_q, &tm_kp);
+    int rc = tc_view(T, MODE_SCORE, l0, l1, p0, p1, &P, &tm_q, &tm_kp);
     if (rc) return rc;
     EPK_PROF(ctx, "p2_colscore");
     EPK_CUDA_CHECK(launch_pdl(T.score_fn, dim3(T.grid), dim3(kThreads), T.smem2, ctx->stream, P, T.tm_k, tm_q,
@@ -945,13 +955,15 @@ int launch_score_tc(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const 
     int rc = tc_plan(ctx, c, q, kp, hq, p, agg_max, scores, fs, &T);
     if (rc) return rc;
     if ((rc = tc_launch_p1(ctx, T, 0, c->layers))) return rc;
-    return tc_launch_p2(ctx, T, 0, c->layers);
+    return tc_launch_p2(ctx, T, 0, c->layers, 0, c->layers);
 }
 
-// One tensor-core block step with the fused selection: per layer group
-// P1 -> P2 -> threshold select on the context stream and count/plan/gather on
-// `side` (when given) so a group's compaction overlaps the next group's
-// scoring.
+// One tensor-core block step with the fused selection: P1 over every layer
+// (one tile-balanced launch: the partition, hence the bits, do not depend on
+// the grouping), then per layer group P2 -> threshold select on the context
+// stream and count/plan/gather on `side` (when given) so a group's compaction
+// overlaps the next group's scoring.  (P1 per group -- its K re-read by P2
+// from L2 -- measured slower: every launch pays the ~25 us CTA-speed tail.)
 int launch_step_tc_grouped(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const void* q,
                            const void* kp, int hq, int p, int agg_max, const int64_t* budgets, int group,
                            cudaStream_t side, cudaEvent_t ev_fork, int out_slack, float* scores, uint8_t* keep,
@@ -966,10 +978,10 @@ int launch_step_tc_grouped(epk_ctx* ctx, const epk_cache_desc* in, const epk_cac
     if (rc) return rc;
     const int L = in->layers;
     cudaStream_t main = ctx->stream;
+    if ((rc = tc_launch_p1(ctx, T, 0, L))) return rc;
     for (int l0 = 0; l0 < L; l0 += group) {
         const int l1 = std::min(L, l0 + group);
-        if ((rc = tc_launch_p1(ctx, T, l0, l1))) return rc;
-        if ((rc = tc_launch_p2(ctx, T, l0, l1))) return rc;
+        if ((rc = tc_launch_p2(ctx, T, l0, l1, 0, L))) return rc;
         const epk_cache_desc vin = view_fn(in, l0, l1), vout = view_fn(out, l0, l1);
         const FusedSelect fs{fs_all.keys,
                              fs_all.hist_fine + int64_t(l0) * 65536,

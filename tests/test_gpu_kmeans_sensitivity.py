@@ -102,7 +102,7 @@ def test_kmeans_sharded_device_ops_nccl_world1(gpu, orc):
 
 @pytest.mark.parametrize("dtype,L,H,N,d", [(torch.bfloat16, 3, 2, 1000, 128), (torch.float32, 2, 3, 333, 128),
                                            (torch.float64, 2, 1, 77, 128), (torch.float32, 2, 2, 150, 7),
-                                           (torch.bfloat16, 1, 1, 1, 8)])
+                                           (torch.bfloat16, 1, 1, 2, 8)])
 def test_sensitivity_ragged_tiles_and_skips(gpu, orc, dtype, L, H, N, d):
     """The pair tiles (128 / 64 / 32 pairs by dtype, chunk-major over layers)
     and the chain's 1,024-cosine ring slots with partial last tiles, rows not
