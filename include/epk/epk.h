@@ -108,9 +108,14 @@ int epk_version(void);
  *                        all layers in one group)
  *   EPK_OPT_OVERLAP      1 (default): with more than one group, each group's
  *                        select + compaction runs on a second stream,
- *                        overlapping the next group's scoring */
+ *                        overlapping the next group's scoring
+ *   EPK_OPT_POOL_KERNEL  1 (default, the reference's semantics) or an odd
+ *                        kernel w > 1: the step max-pools every head's scores
+ *                        over a w-row window before selecting (opt-in; see
+ *                        epk_pool_scores) */
 #define EPK_OPT_LAYER_GROUP 1
 #define EPK_OPT_OVERLAP 2
+#define EPK_OPT_POOL_KERNEL 4
 int epk_ctx_set_option(epk_ctx* ctx, int32_t option, int64_t value);
 /* Number of kernels this library launched on the context since creation. */
 int64_t epk_ctx_launch_count(epk_ctx* ctx);
@@ -150,6 +155,14 @@ int epk_score(epk_ctx* ctx, const epk_cache_desc* cache, const void* q_prompt,
 int epk_score_grids(epk_ctx* ctx, int32_t q_heads, int32_t kv_heads, int32_t prompt_len,
                     const int64_t* head_off, const double* grids, int32_t aggregation,
                     double* scores);
+
+/* ---- opt-in score smoothing (north_star's "1-D max-pool smoothing") -------- *
+ * NOT part of the reference (score_with_prompt has no pooling, scoring.hpp:
+ * 80-128): SnapKV-style max_pool1d, odd kernel w, stride 1, "same" padding,
+ * over every (layer, head)'s live rows in position order, never across heads:
+ *   pooled[r] = max scores[i], i live in r's head, |i - r| <= w / 2.
+ * scores, pooled [dev] fp32 [rows] (distinct buffers).  Asynchronous. */
+int epk_pool_scores(epk_ctx* ctx, const epk_cache_desc* cache, const float* scores, float* pooled, int32_t kernel);
 
 /* ---- K2: selection -------------------------------------------------------- *
  * Pooled selection of evict_to_budget for every layer of `cache`:

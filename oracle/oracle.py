@@ -197,6 +197,26 @@ def score_layer_f32(q, k, kp, head_off, agg_max=True):
     return out
 
 
+def maxpool_scores(head_off, scores, kernel):
+    """Opt-in max-pool smoothing restated (north_star; no reference counterpart):
+    per head, pooled[j] = max scores[i] over |i - j| <= kernel // 2 within the
+    head (SnapKV's max_pool1d, stride 1, same padding).  TEST INFRASTRUCTURE."""
+    head_off = np.asarray(head_off, np.int64)
+    s = np.asarray(scores)
+    out = np.empty_like(s)
+    half = int(kernel) // 2
+    for h in range(len(head_off) - 1):
+        a, b = int(head_off[h]), int(head_off[h + 1])
+        seg = s[a:b]
+        n = b - a
+        if n == 0:
+            continue
+        pad = np.concatenate([np.full(half, -np.inf, s.dtype), seg, np.full(half, -np.inf, s.dtype)])
+        win = np.lib.stride_tricks.sliding_window_view(pad, 2 * half + 1)
+        out[a:b] = win.max(axis=1).astype(s.dtype)
+    return out
+
+
 def expf(x):
     x = _c(x, np.float32).ravel()
     out = np.empty_like(x)

@@ -7,7 +7,7 @@ include/epk/epk.h.  There is no CPU fallback.
 from .errors import DimensionError, Error, IoError, ZeroNormError  # noqa: F401
 from .kvcache import (EpisodeCache, KVEntry, LayerCache, append_to_cache, compact, evict_device,  # noqa: F401
                       evict_to_budget, select_per_head, select_pooled)
-from .scoring import keydiff_scores, score_grids, score_with_prompt  # noqa: F401
+from .scoring import keydiff_scores, pool_scores, score_grids, score_with_prompt  # noqa: F401
 from .blockprefill import BlockPrefillConfig, PrefillReport, block_prefill  # noqa: F401
 from .clustering import KMeansResult, kmeans, kmeans_multi_device, kmeans_sharded  # noqa: F401
 from .allocation import (BudgetAllocation, SensitivityProfile, allocate, sensitivity_from_keys,  # noqa: F401

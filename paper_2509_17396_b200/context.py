@@ -41,13 +41,16 @@ class Context:
     def launches(self) -> int:
         return int(_lib.load().epk_ctx_launch_count(self.handle))
 
-    def set_option(self, layer_group: int | None = None, overlap: bool | None = None) -> None:
-        """epk_evict_step tuning: layers per group (0 = auto) and compaction
-        overlap."""
+    def set_option(self, layer_group: int | None = None, overlap: bool | None = None,
+                   pool_kernel: int | None = None) -> None:
+        """epk_evict_step tuning: layers per group (0 = auto), compaction
+        overlap, and the opt-in max-pool smoothing kernel (1 = off)."""
         if layer_group is not None:
             _lib.call("epk_ctx_set_option", self.handle, 1, int(layer_group))
         if overlap is not None:
             _lib.call("epk_ctx_set_option", self.handle, 2, int(bool(overlap)))
+        if pool_kernel is not None:
+            _lib.call("epk_ctx_set_option", self.handle, 4, int(pool_kernel))
 
     def profile(self, enable: bool) -> None:
         """Bracket every kernel launch with CUDA events (live per-kernel timing)."""

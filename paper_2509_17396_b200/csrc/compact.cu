@@ -429,3 +429,62 @@ int launch_append(epk_ctx* ctx, const epk_cache_desc* c, const void* k_new, cons
 }
 
 }  // namespace epk
+
+namespace epk {
+
+// ---------------------------------------------------------------------------
+// Opt-in 1-D max-pool smoothing of the scores (north_star's "1-D max-pool
+// smoothing"; NOT in the reference, whose score_with_prompt has no pooling,
+// scoring.hpp:80-128 -- SURVEY 0.4): SnapKV-style max_pool1d with an odd
+// kernel w, stride 1 and "same" padding over each (layer, head)'s live rows in
+// position order: pooled[j] = max of scores[i], |i - j| <= w / 2, i live in
+// j's head.  One thread per cache row; the window never crosses a head.
+// ---------------------------------------------------------------------------
+struct PoolParams {
+    LayerTable lt;
+    int H;
+    int half;
+    int64_t max_region;
+    const int32_t* off;
+    const int32_t* len;
+    const float* in;
+    float* out;
+};
+
+__global__ void __launch_bounds__(256) pool_scores_kernel(const __grid_constant__ PoolParams P) {
+    const int layer = blockIdx.y;
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int32_t* off = P.off + layer * (P.H + 1);
+    if (r >= off[P.H]) return;
+    const int h = head_of_row(off, P.H, r);
+    const int64_t lo = off[h], n = P.len[layer * P.H + h];
+    if (r - lo >= n) return;  // slack row
+    const int64_t base = P.lt.base[layer];
+    const int64_t a = max(lo, r - P.half), b = min(lo + n - 1, r + P.half);
+    float m = __ldg(P.in + base + a);
+    for (int64_t i = a + 1; i <= b; ++i) m = fmaxf(m, __ldg(P.in + base + i));
+    P.out[base + r] = m;
+}
+
+int launch_pool_scores(epk_ctx* ctx, const epk_cache_desc* c, const float* in, float* out, int kernel) {
+    if (kernel < 1 || kernel % 2 == 0) return fail(EPK_ERR_ARG, "pool_scores: kernel must be odd and >= 1");
+    if (c->kv_heads > 64) return fail(EPK_ERR_UNSUPPORTED, "pool_scores: more than 64 kv heads");
+    PoolParams P;
+    int rc = make_layer_table(c, &P.lt);
+    if (rc) return rc;
+    P.H = c->kv_heads;
+    P.half = kernel / 2;
+    P.max_region = 0;
+    for (int l = 0; l < c->layers; ++l) P.max_region = std::max<int64_t>(P.max_region, P.lt.base[l + 1] - P.lt.base[l]);
+    P.off = c->head_off;
+    P.len = c->head_len;
+    P.in = in;
+    P.out = out;
+    const dim3 grid(unsigned(std::max<int64_t>(1, (P.max_region + 255) / 256)), unsigned(c->layers));
+    EPK_PROF(ctx, "pool_scores");
+    EPK_CUDA_CHECK(launch_pdl(pool_scores_kernel, grid, dim3(256), 0, ctx->stream, P));
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
+}  // namespace epk

@@ -138,6 +138,7 @@ int launch_step_tc_grouped(epk_ctx*, const epk_cache_desc*, const epk_cache_desc
                                    const uint32_t*, const uint64_t*, uint32_t*, uint32_t*),
                            epk_cache_desc (*)(const epk_cache_desc*, int, int));
 int launch_append(epk_ctx*, const epk_cache_desc*, const void*, const void*, const int32_t*, int);
+int launch_pool_scores(epk_ctx*, const epk_cache_desc*, const float*, float*, int);
 int kmeans_shards(epk_ctx* const*, int, const double* const*, const int64_t*, int64_t, int64_t, uint64_t, int64_t,
                   int64_t*, double*, int64_t*, double*);
 int launch_score_f32(epk_ctx*, const epk_cache_desc*, const float*, const float*, int, int, int, int64_t, float*);
@@ -380,6 +381,15 @@ int epk_select_pooled(epk_ctx* ctx, const epk_cache_desc* c, const void* scores,
     return EPK_OK;
 }
 
+int epk_pool_scores(epk_ctx* ctx, const epk_cache_desc* c, const float* scores, float* pooled, int32_t kernel) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(c))) return rc;
+    if (!scores || !pooled) return fail(EPK_ERR_ARG, "pool_scores: null pointer");
+    if (scores == pooled) return fail(EPK_ERR_ARG, "pool_scores: in-place pooling is not supported");
+    return launch_pool_scores(ctx, c, scores, pooled, kernel);
+}
+
 int epk_select_per_head(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int32_t score_dtype,
                         const int64_t* k_per_layer, uint8_t* keep) {
     int rc = check_ctx(ctx);
@@ -424,6 +434,10 @@ int epk_ctx_set_option(epk_ctx* ctx, int32_t option, int64_t value) {
         case EPK_OPT_OVERLAP:
             ctx->overlap = value != 0;
             return EPK_OK;
+        case EPK_OPT_POOL_KERNEL:
+            if (value < 1 || value % 2 == 0 || value > 4095) return fail(EPK_ERR_ARG, "pool kernel must be odd, 1..4095");
+            ctx->pool_kernel = int(value);
+            return EPK_OK;
         default:
             return fail(EPK_ERR_ARG, "unknown option");
     }
@@ -451,7 +465,8 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     // Tensor-core steps without pins take the fused selection: the scorer
     // writes keys + score histograms, select_threshold_kernel finds each
     // layer's threshold from them, the compaction derives keep[] itself.
-    const bool fused = mode == EPK_SCORE_TC_BF16 && n_pins == 0 && in->kv_heads <= 64;
+    const bool pooled = ctx->pool_kernel > 1;  // opt-in smoothing: scores -> pool -> generic select
+    const bool fused = mode == EPK_SCORE_TC_BF16 && n_pins == 0 && in->kv_heads <= 64 && !pooled;
     // Step buffers live in their own allocation so the kernels' workspace
     // growth never aliases them.  Layout: histograms at fixed offsets for
     // kMaxLayers layers (zeroed once here, re-zeroed by every threshold
@@ -463,7 +478,8 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     const int64_t o_scores = o_cnt + int64_t(kMaxLayers) * 8;
     const int64_t o_keep = o_scores + align_up(rows * 4, 256);
     const int64_t o_keys = o_keep + align_up(rows, 256);
-    const int64_t need = o_keys + align_up(rows * 4, 256);
+    const int64_t o_pool = o_keys + align_up(rows * 4, 256);
+    const int64_t need = o_pool + (pooled ? align_up(rows * 4, 256) : 0);
     const bool capturing = [&] {
         cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(ctx->stream, &st);
@@ -564,6 +580,8 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
                                  &fs);
         } else {
             rc = epk_score(ctx, &vin, qg, kpg, q_heads, prompt_len, aggregation, mode, n_max, scores);
+            if (rc == EPK_OK && pooled)
+                rc = launch_pool_scores(ctx, &vin, scores, reinterpret_cast<float*>(sb + o_pool), ctx->pool_kernel);
         }
         if (rc) return rc;
         // select + compact of this group run on the side stream (when
@@ -580,7 +598,8 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
             if (rc == EPK_OK)
                 rc = launch_compact(ctx, &vin, &vout, keep, out_slack, keys, thr + 2 * l0, fs.hist_fine, fs.hist_coarse);
         } else {
-            rc = launch_select(ctx, &vin, scores, EPK_F32, budgets + l0, pins, n_pins, keep, kept ? kept + l0 : nullptr, 0);
+            rc = launch_select(ctx, &vin, pooled ? reinterpret_cast<const float*>(sb + o_pool) : scores, EPK_F32,
+                               budgets + l0, pins, n_pins, keep, kept ? kept + l0 : nullptr, 0);
             if (rc == EPK_OK) rc = launch_compact(ctx, &vin, &vout, keep, out_slack, nullptr, nullptr, nullptr, nullptr);
         }
         ctx->stream = main;

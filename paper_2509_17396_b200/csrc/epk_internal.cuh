@@ -34,6 +34,7 @@ struct epk_ctx {
     cudaEvent_t ev_aux_fork = nullptr, ev_aux_join = nullptr;
     int layer_group = 0;  // layers per group in epk_evict_step (0 = auto: group K fits in L2)
     int overlap = 1;      // run each group's compaction on `side`
+    int pool_kernel = 1;  // EPK_OPT_POOL_KERNEL: opt-in max-pool smoothing of the scores (1 = off, the reference)
     void* step_buf = nullptr;  // epk_evict_step scores + keep mask
     int64_t step_bytes = 0;
     int* err_flag = nullptr;  // deferred device-side error code (device int)

@@ -97,6 +97,21 @@ def keydiff_scores(cache: EpisodeCache, out: torch.Tensor | None = None, ctx: Co
     return out
 
 
+def pool_scores(cache: EpisodeCache, scores: torch.Tensor, kernel: int, out: torch.Tensor | None = None,
+                ctx: Context | None = None) -> torch.Tensor:
+    """Opt-in 1-D max-pool smoothing (north_star; NOT in the reference, whose
+    score_with_prompt has no pooling, scoring.hpp:80-128): max over an odd
+    `kernel`-row window of each head's live rows (position order), never
+    across heads.  epk_pool_scores."""
+    ctx = ctx or default_context(cache.device.index)
+    if scores.dtype != torch.float32 or scores.numel() < cache.rows:
+        raise DimensionError("pool_scores: fp32 scores for every cache row expected")
+    out = out if out is not None else torch.empty_like(scores)
+    d = cache.desc()
+    _lib.call("epk_pool_scores", ctx.handle, C.byref(d), ptr(scores), ptr(out), int(kernel))
+    return out
+
+
 def debug_expf(x: torch.Tensor, ctx: Context | None = None) -> torch.Tensor:
     """The device epk_expf (EPK-F32 v1), for the bitwise parity test."""
     ctx = ctx or default_context(x.device.index)

@@ -91,3 +91,17 @@ def test_threaded_scorers_equal_single_threaded(orc, g):
             q32, k32, kp32 = q.astype(np.float32), k.astype(np.float32), kp.astype(np.float32)
             assert np.array_equal(orc.score_layer_f32_mt(q32, k32, kp32, ho, agg, threads=2).view(np.uint32),
                                   orc.score_layer_f32(q32, k32, kp32, ho, agg).view(np.uint32))
+
+
+def test_maxpool_restatement_vs_loop(orc):
+    """oracle.maxpool_scores (the opt-in smoothing's checker) against a plain
+    per-element loop: windows clipped at head boundaries, empty heads."""
+    rng = np.random.default_rng(2)
+    ho = np.array([0, 7, 7, 20, 21])
+    s = rng.random(21).astype(np.float32)
+    for k in (1, 3, 5, 9, 41):
+        got = orc.maxpool_scores(ho, s, k)
+        for h in range(4):
+            for j in range(ho[h], ho[h + 1]):
+                lo, hi = max(ho[h], j - k // 2), min(ho[h + 1] - 1, j + k // 2)
+                assert got[j] == s[lo:hi + 1].max()
