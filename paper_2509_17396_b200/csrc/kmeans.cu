@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(64) cosine_chain_kernel(const __grid_constant_
     const int64_t nchunks = (P.rows + kChainChunk - 1) / kChainChunk;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kChainStages; ++s) {
-            sm100::mbar_init(&full[s], 1);
+            sm100::mbar_init(&full[s], 32);  // every loader lane releases its own ring stores
             sm100::mbar_init(&empty[s], 1);
         }
         sm100::fence_barrier_init();
@@ -371,8 +371,7 @@ __global__ void __launch_bounds__(64) cosine_chain_kernel(const __grid_constant_
                 nvalid[s] = base;
                 nskip[s] = sk;
             }
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(&full[s]);  // release: the ring stores above precede it
+            sm100::mbar_arrive(&full[s]);  // release: this lane's ring stores (and lane 0's counts) precede it
         }
         return;
     }
@@ -385,12 +384,27 @@ __global__ void __launch_bounds__(64) cosine_chain_kernel(const __grid_constant_
         const int n = nvalid[s];
         const double* x = ring[s];
         int i = 0;
-        for (; i + 8 <= n; i += 8) {
-            double b[8];
+        if (n >= 8) {  // software-pipelined: the next 8 values load while the current 8 are added
+            double2 b[4], nb[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) b[u] = x[i + u];
+            for (int u = 0; u < 4; ++u) b[u] = reinterpret_cast<const double2*>(x)[u];
+            for (; i + 16 <= n; i += 8) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, b[u]);
+                for (int u = 0; u < 4; ++u) nb[u] = reinterpret_cast<const double2*>(x + i + 8)[u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc = __dadd_rn(acc, b[u].x);
+                    acc = __dadd_rn(acc, b[u].y);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) b[u] = nb[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc = __dadd_rn(acc, b[u].x);
+                acc = __dadd_rn(acc, b[u].y);
+            }
+            i += 8;
         }
         for (; i < n; ++i) acc = __dadd_rn(acc, x[i]);
         cnt += n;
