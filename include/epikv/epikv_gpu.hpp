@@ -302,20 +302,13 @@ inline KMeansResult kmeans(const std::vector<Vec>& points, std::size_t k, std::u
     return r;
 }
 
-/// measure_sensitivity (allocation.hpp:55): the two forwards (causal and
-/// sink+recent) are the reference's model substrate on the host; the key
-/// cosine reduction sigma_l runs on the GPU (fp64, deterministic order).
-inline SensitivityProfile measure_sensitivity(const Model& model, std::span<const TokenId> calibration_tokens,
-                                              std::size_t calibration_budget, std::size_t sink,
-                                              std::string input_id = "") {
-    const std::size_t n = calibration_tokens.size();
-    if (n < 2) throw Error("measure_sensitivity: need at least 2 calibration tokens");
-    if (calibration_budget < sink + 1) throw Error("measure_sensitivity: budget must be >= sink + 1");
-    TraceOptions opts;
-    opts.store_attention = false;
-    const ForwardTrace full = forward(model, calibration_tokens, MaskSpec::causal(), nullptr, opts);
-    const ForwardTrace block =
-        forward(model, calibration_tokens, MaskSpec::sink_recent(sink, calibration_budget - sink), nullptr, opts);
+namespace detail {
+// The GPU key-cosine reduction of measure_sensitivity (allocation.hpp:80-100)
+// over the two calibration traces.
+inline SensitivityProfile sensitivity_from_traces(const Model& model, const ForwardTrace& full,
+                                                  const ForwardTrace& block, std::size_t n,
+                                                  std::size_t calibration_budget, std::size_t sink,
+                                                  std::string input_id) {
     const std::size_t L = model.config.layers, H = model.config.kv_heads, d = model.config.head_dim;
     std::vector<double> kf(L * H * n * d), kb(L * H * n * d);
     for (std::size_t l = 0; l < L; ++l)
@@ -342,6 +335,247 @@ inline SensitivityProfile measure_sensitivity(const Model& model, std::span<cons
     profile.skipped_zero_norm = std::size_t(skipped);
     return profile;
 }
+}  // namespace detail
+
+/// measure_sensitivity (allocation.hpp:55): the two forwards (causal and
+/// sink+recent) are the reference's model substrate on the host; the key
+/// cosine reduction sigma_l runs on the GPU (fp64, deterministic order).
+inline SensitivityProfile measure_sensitivity(const Model& model, std::span<const TokenId> calibration_tokens,
+                                              std::size_t calibration_budget, std::size_t sink,
+                                              std::string input_id = "") {
+    const std::size_t n = calibration_tokens.size();
+    if (n < 2) throw Error("measure_sensitivity: need at least 2 calibration tokens");
+    if (calibration_budget < sink + 1) throw Error("measure_sensitivity: budget must be >= sink + 1");
+    TraceOptions opts;
+    opts.store_attention = false;
+    const ForwardTrace full = epikv::forward(model, calibration_tokens, MaskSpec::causal(), nullptr, opts);
+    const ForwardTrace block =
+        epikv::forward(model, calibration_tokens, MaskSpec::sink_recent(sink, calibration_budget - sink), nullptr, opts);
+    return detail::sensitivity_from_traces(model, full, block, n, calibration_budget, sink, std::move(input_id));
+}
+
+// ---- the model forward on the GPU ----------------------------
+/// Where the attention rows' softmax (max, exp, denominator) runs in
+/// gpu::forward: on the host with std::exp -- the reference's own code, every
+/// output bit-identical -- or on the device (CUDA exp, <= 1 ulp from std::exp,
+/// outputs within ~1e-15 relative).
+enum class Softmax { host, device };
+
+namespace detail {
+
+/// A reference Model's weights in HBM (epk_toy_model layout), cached per
+/// thread by object identity and config (init_model is deterministic in the
+/// config; a model whose weights are edited in place needs a fresh object).
+struct DeviceModel {
+    const Model* src = nullptr;
+    ModelConfig cfg;
+    std::unique_ptr<DBuf<double>> emb, weights;
+    epk_toy_model desc{};
+};
+
+inline const DeviceModel& device_model(const Model& m) {
+    thread_local std::vector<std::unique_ptr<DeviceModel>> cache;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    for (auto& d : cache)
+        if (d->src == &m && d->cfg == m.config) return *d;
+    const ModelConfig& c = m.config;
+    auto d = std::make_unique<DeviceModel>();
+    d->src = &m;
+    d->cfg = c;
+    d->emb = std::make_unique<DBuf<double>>(m.token_embedding.values.size());
+    d->emb->upload(m.token_embedding.values.data(), m.token_embedding.values.size());
+    std::vector<double> w;
+    for (const LayerWeights& lw : m.layers)
+        for (const Matrix* x : {&lw.wq, &lw.wk, &lw.wv, &lw.wo, &lw.mlp_in, &lw.mlp_out})
+            w.insert(w.end(), x->values.begin(), x->values.end());
+    d->weights = std::make_unique<DBuf<double>>(w.size());
+    d->weights->upload(w.data(), w.size());
+    d->desc = epk_toy_model{int32_t(c.layers), int32_t(c.query_heads), int32_t(c.kv_heads), int32_t(c.head_dim),
+                            int32_t(c.model_dim), int64_t(c.vocab), d->emb->p, d->weights->p};
+    if (cache.size() >= 4) cache.erase(cache.begin());
+    cache.push_back(std::move(d));
+    return *cache.back();
+}
+
+/// An EpisodicCache as an fp64 layered CSR in HBM (the past cache of forward).
+struct DeviceCache {
+    std::unique_ptr<DBuf<double>> k, v;
+    std::unique_ptr<DBuf<int32_t>> pos, off, len;
+    std::vector<int64_t> base;
+    epk_cache_desc desc{};
+};
+
+inline std::unique_ptr<DeviceCache> upload_cache(const EpisodicCache& c, std::size_t kv_heads, std::size_t dh) {
+    auto d = std::make_unique<DeviceCache>();
+    const std::size_t L = c.layers.size();
+    std::vector<double> k, v;
+    std::vector<int32_t> pos, off, len;
+    d->base.push_back(0);
+    for (const LayerCache& layer : c.layers) {
+        int32_t o = 0;
+        for (std::size_t h = 0; h < kv_heads; ++h) {
+            off.push_back(o);
+            const auto& head = layer.heads[h];
+            len.push_back(int32_t(head.size()));
+            for (const KVEntry& e : head) {
+                if (e.key.size() != dh || e.value.size() != dh) throw DimensionError("forward: cache entry dimension mismatch");
+                if (e.position > 0x7fffffffu) throw Error("forward: position exceeds the device int32 range");
+                k.insert(k.end(), e.key.begin(), e.key.end());
+                v.insert(v.end(), e.value.begin(), e.value.end());
+                pos.push_back(int32_t(e.position));
+            }
+            o += int32_t(head.size());
+        }
+        off.push_back(o);
+        d->base.push_back(d->base.back() + o);
+    }
+    d->k = std::make_unique<DBuf<double>>(std::max<std::size_t>(k.size(), 1));
+    d->v = std::make_unique<DBuf<double>>(std::max<std::size_t>(v.size(), 1));
+    d->pos = std::make_unique<DBuf<int32_t>>(std::max<std::size_t>(pos.size(), 1));
+    d->off = std::make_unique<DBuf<int32_t>>(off.size());
+    d->len = std::make_unique<DBuf<int32_t>>(len.size());
+    if (!k.empty()) {
+        d->k->upload(k.data(), k.size());
+        d->v->upload(v.data(), v.size());
+        d->pos->upload(pos.data(), pos.size());
+    }
+    d->off->upload(off.data(), off.size());
+    d->len->upload(len.data(), len.size());
+    d->desc = epk_cache_desc{int32_t(L), int32_t(kv_heads), int32_t(dh), EPK_F64, d->k->p, d->v->p,
+                             d->pos->p, d->off->p, d->len->p, d->base.data()};
+    return d;
+}
+
+}  // namespace detail
+
+/// forward (toymodel.hpp:228-411) with the layers on the GPU (epk_toy_forward):
+/// same signature and trace (keys, values, context positions, attention
+/// grids, hidden), same validation and exceptions.  Softmax::host (default)
+/// keeps every output bit-identical to the reference.
+inline ForwardTrace forward(const Model& model, std::span<const TokenId> tokens, std::span<const std::size_t> positions,
+                            const MaskSpec& mask, const EpisodicCache* past = nullptr, TraceOptions opts = {},
+                            Softmax softmax = Softmax::host) {
+    const ModelConfig& cfg = model.config;
+    const std::size_t n = tokens.size();
+    if (n == 0) throw Error("forward: empty token sequence");
+    if (positions.size() != n) throw DimensionError("forward: positions size mismatch");
+    for (std::size_t i = 0; i < n; ++i) {
+        if (tokens[i] >= cfg.vocab) throw Error("forward: token id " + std::to_string(tokens[i]) + " out of vocab");
+        if (i > 0 && positions[i] <= positions[i - 1]) throw Error("forward: positions must be strictly increasing");
+    }
+    if (past != nullptr) {
+        if (past->layer_count() != cfg.layers) throw DimensionError("forward: cache layer count mismatch");
+        if (!past->empty() && past->max_position() >= positions[0])
+            throw Error("forward: position overlap between cache and new tokens");
+    }
+    const std::size_t L = cfg.layers, Hq = cfg.query_heads, Hkv = cfg.kv_heads, dh = cfg.head_dim, D = cfg.model_dim;
+    const detail::DeviceModel& dm = detail::device_model(model);
+    std::vector<int32_t> tok(tokens.begin(), tokens.end());
+    std::vector<int64_t> pos(positions.begin(), positions.end());
+    std::vector<double> pe;
+    pe.reserve(n * D);
+    for (std::size_t t = 0; t < n; ++t) {
+        const Vec p = model.position_embedding(positions[t]);
+        pe.insert(pe.end(), p.begin(), p.end());
+    }
+    detail::DBuf<int32_t> d_tok(n);
+    detail::DBuf<int64_t> d_pos(n);
+    detail::DBuf<double> d_pe(n * D), d_k(L * n * Hkv * dh), d_v(L * n * Hkv * dh), d_h(n * D);
+    d_tok.upload(tok.data(), n);
+    d_pos.upload(pos.data(), n);
+    d_pe.upload(pe.data(), pe.size());
+    std::unique_ptr<detail::DeviceCache> dc;
+    std::vector<std::size_t> cache_len(L * Hkv, 0);
+    if (past != nullptr) {
+        dc = detail::upload_cache(*past, Hkv, dh);
+        for (std::size_t l = 0; l < L; ++l)
+            for (std::size_t h = 0; h < Hkv; ++h) cache_len[l * Hkv + h] = past->layers[l].heads[h].size();
+    }
+    std::vector<int64_t> attn_off;
+    std::size_t attn_total = 0;
+    if (opts.store_attention) {
+        for (std::size_t l = 0; l < L; ++l)
+            for (std::size_t qh = 0; qh < Hq; ++qh) {
+                attn_off.push_back(int64_t(attn_total));
+                attn_total += n * (cache_len[l * Hkv + cfg.kv_head_of(qh)] + n);
+            }
+    }
+    std::unique_ptr<detail::DBuf<double>> d_attn;
+    if (opts.store_attention) d_attn = std::make_unique<detail::DBuf<double>>(std::max<std::size_t>(attn_total, 1));
+    const MaskSpec::Kind kind = mask.kind;
+    detail::check(epk_toy_forward(detail::ctx(), &dm.desc, d_tok.p, d_pe.p, d_pos.p, int64_t(n),
+                                  kind == MaskSpec::Kind::Causal ? 0 : 1, int64_t(mask.sink_count),
+                                  int64_t(mask.recent_count), dc ? &dc->desc : nullptr, d_k.p, d_v.p,
+                                  d_attn ? d_attn->p : nullptr, attn_off.empty() ? nullptr : attn_off.data(), d_h.p,
+                                  softmax == Softmax::host ? 1 : 0));
+    std::vector<double> hk(L * n * Hkv * dh), hv(hk.size()), hh(n * D), ha(attn_total);
+    d_k.download(hk.data(), hk.size());
+    d_v.download(hv.data(), hv.size());
+    d_h.download(hh.data(), hh.size());
+    if (d_attn && attn_total) d_attn->download(ha.data(), attn_total);
+    ForwardTrace trace;
+    trace.positions.assign(positions.begin(), positions.end());
+    trace.layers.resize(L);
+    for (std::size_t l = 0; l < L; ++l) {
+        LayerTrace& lt = trace.layers[l];
+        lt.keys.resize(Hkv);
+        lt.values.resize(Hkv);
+        lt.context_positions.resize(Hkv);
+        for (std::size_t h = 0; h < Hkv; ++h) {
+            lt.keys[h] = Matrix(n, dh);
+            lt.values[h] = Matrix(n, dh);
+            for (std::size_t t = 0; t < n; ++t)
+                for (std::size_t d = 0; d < dh; ++d) {
+                    const std::size_t src = (l * n + t) * Hkv * dh + h * dh + d;
+                    lt.keys[h].values[t * dh + d] = hk[src];
+                    lt.values[h].values[t * dh + d] = hv[src];
+                }
+            if (past != nullptr)
+                for (const KVEntry& e : past->layers[l].heads[h]) lt.context_positions[h].push_back(e.position);
+            lt.context_positions[h].insert(lt.context_positions[h].end(), positions.begin(), positions.end());
+        }
+        if (opts.store_attention) {
+            lt.attention.resize(Hq);
+            for (std::size_t qh = 0; qh < Hq; ++qh) {
+                const std::size_t cols = cache_len[l * Hkv + cfg.kv_head_of(qh)] + n;
+                lt.attention[qh] = Matrix(n, cols);
+                std::copy(ha.begin() + attn_off[l * Hq + qh], ha.begin() + attn_off[l * Hq + qh] + n * cols,
+                          lt.attention[qh].values.begin());
+            }
+        }
+    }
+    trace.hidden = Matrix(n, D);
+    trace.hidden.values = std::move(hh);
+    return trace;
+}
+
+/// measure_sensitivity (allocation.hpp:55) with its two calibration forwards
+/// (causal and sink+recent, allocation.hpp:70-72) on the GPU as well.
+inline SensitivityProfile measure_sensitivity(const Model& model, std::span<const TokenId> calibration_tokens,
+                                              std::size_t calibration_budget, std::size_t sink, std::string input_id,
+                                              Softmax softmax) {
+    const std::size_t n = calibration_tokens.size();
+    if (n < 2) throw Error("measure_sensitivity: need at least 2 calibration tokens");
+    if (calibration_budget < sink + 1) throw Error("measure_sensitivity: budget must be >= sink + 1");
+    TraceOptions opts;
+    opts.store_attention = false;
+    std::vector<std::size_t> pos(n);
+    for (std::size_t i = 0; i < n; ++i) pos[i] = i;
+    const ForwardTrace full = gpu::forward(model, calibration_tokens, pos, MaskSpec::causal(), nullptr, opts, softmax);
+    const ForwardTrace block = gpu::forward(model, calibration_tokens, pos,
+                                            MaskSpec::sink_recent(sink, calibration_budget - sink), nullptr, opts,
+                                            softmax);
+    return detail::sensitivity_from_traces(model, full, block, n, calibration_budget, sink, std::move(input_id));
+}
+
+/// Which forwards of gpu::block_prefill run on the GPU (default: none -- the
+/// reference's host forward, as in the reference-signature overload).
+struct PrefillForward {
+    bool block_on_device = false;   // the block's own forward (appended K/V)
+    bool prompt_on_device = false;  // the patched prompt's forward (attention grids for scoring)
+    Softmax softmax = Softmax::host;
+};
 
 /// block_prefill (blockprefill.hpp:92) with scoring and eviction on the GPU.
 /// The toy-model forwards (block and prompt) are the reference's own, on the
@@ -350,8 +584,8 @@ inline SensitivityProfile measure_sensitivity(const Model& model, std::span<cons
 /// the reference.  Supports every scorer: patched, snapkv, kvzip, infinipot
 /// (GPU prompt scoring), keydiff (GPU KeyDiff scores) and streaming.
 inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> context,
-                                   const BlockPrefillConfig& config, std::size_t episode_id = 0,
-                                   std::span<const std::size_t> positions = {}) {
+                                   const BlockPrefillConfig& config, std::size_t episode_id,
+                                   std::span<const std::size_t> positions, const PrefillForward& fwd) {
     const ModelConfig& cfg = model.config;
     if (context.empty()) throw Error("block_prefill: empty context");
     if (config.budget_per_head < 1 || config.block_size < 1)
@@ -403,7 +637,10 @@ inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> 
         const std::span<const TokenId> block = context.subspan(start, len);
         const std::span<const std::size_t> block_positions = positions.subspan(start, len);
         const std::size_t block_index = report.blocks_processed;
-        ForwardTrace trace = forward(model, block, block_positions, MaskSpec::causal(), &report.cache, block_opts);
+        ForwardTrace trace =
+            fwd.block_on_device
+                ? gpu::forward(model, block, block_positions, MaskSpec::causal(), &report.cache, block_opts, fwd.softmax)
+                : epikv::forward(model, block, block_positions, MaskSpec::causal(), &report.cache, block_opts);
         append_to_cache(report.cache, trace);
         report.occupancy.record(OccupancyKind::Append, entries(report.cache), zeros);
         TokenScoreMap scores;
@@ -421,7 +658,10 @@ inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> 
             for (std::size_t i = 0; i < prompt.tokens.size(); ++i) prompt_positions[i] = prompt_base + i;
             report.prompt_ranges.push_back({prompt_base, prompt.tokens.size()});
             const ForwardTrace prompt_trace =
-                forward(model, prompt.tokens, prompt_positions, MaskSpec::causal(), &report.cache);
+                fwd.prompt_on_device
+                    ? gpu::forward(model, prompt.tokens, prompt_positions, MaskSpec::causal(), &report.cache, {},
+                                   fwd.softmax)
+                    : epikv::forward(model, prompt.tokens, prompt_positions, MaskSpec::causal(), &report.cache);
             report.occupancy.record(OccupancyKind::PromptResident, entries(report.cache),
                                     std::vector<std::size_t>(cfg.layers, cfg.kv_heads * prompt.tokens.size()));
             scores = gpu::score_with_prompt(prompt_trace, config.aggregation);
@@ -449,6 +689,14 @@ inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> 
         ++report.blocks_processed;
     }
     return report;
+}
+
+/// block_prefill with the reference's signature: host forwards (the
+/// reference's), GPU scoring and eviction.
+inline PrefillReport block_prefill(const Model& model, std::span<const TokenId> context,
+                                   const BlockPrefillConfig& config, std::size_t episode_id = 0,
+                                   std::span<const std::size_t> positions = {}) {
+    return gpu::block_prefill(model, context, config, episode_id, positions, PrefillForward{});
 }
 
 /// kmeans (clustering.hpp:148) with the points split in index order over

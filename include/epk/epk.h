@@ -30,6 +30,7 @@
  *   epk_key_cosine_sigma measure_sensitivity reduction (allocation.hpp:80-100)
  *   epk_score_keydiff    keydiff_scores (scoring.hpp:186-221), the KeyDiff baseline
  *   epk_serialize_epkv   persist (kvcache.hpp:281-317), the episodic cache store's writer
+ *   epk_toy_forward      forward (toymodel.hpp:228-411), the model step before the path
  */
 #ifndef EPK_EPK_H
 #define EPK_EPK_H
@@ -279,6 +280,40 @@ int epk_serialize_epkv(epk_ctx* ctx, const epk_cache_desc* cache, uint64_t episo
 int epk_key_cosine_sigma(epk_ctx* ctx, const void* k_full, const void* k_block, int32_t dtype,
                          int32_t layers, int32_t kv_heads, int64_t ntok, int32_t dim,
                          double* sigma, int64_t* skipped);
+
+/* ---- the model step before the hot path -------------------- *
+ * The reference's toy GQA transformer forward (toymodel.hpp:228-411) on the
+ * GPU, fp64, the reference's operation order (no FMA).  Weights [dev], per
+ * layer in this order: wq [D][D], wk [D][Hkv*dh], wv [D][Hkv*dh], wo [D][D],
+ * mlp_in [D][2D], mlp_out [2D][D] (row-major, as the reference's Matrix). */
+typedef struct epk_toy_model {
+    int32_t layers;
+    int32_t query_heads;
+    int32_t kv_heads;
+    int32_t head_dim;
+    int32_t model_dim; /* = query_heads * head_dim */
+    int64_t vocab;
+    const double* token_embedding; /* [dev] [vocab][model_dim] */
+    const double* weights;         /* [dev] all layers, layout above */
+} epk_toy_model;
+
+/* forward (toymodel.hpp:228) over n new tokens at `positions` attending to
+ * the past cache (F64 layered CSR, may be NULL) and to earlier new tokens.
+ *   tokens [dev] int32 [n]; pos_emb [dev] [n][D] = Model::position_embedding
+ *   rows; positions [dev] int64 [n]; mask_kind 0 causal, 1 sink+recent
+ *   (sink, recent as MaskSpec).
+ *   k_out, v_out [dev] [layers][n][kv_heads*head_dim]: the new keys / values.
+ *   attention [dev, optional]: query head qh of layer l writes its n x
+ *   (cache_len(h) + n) weight grid at attention + attn_offsets[l*Hq + qh]
+ *   (attn_offsets [host]); hidden_out [dev, optional] [n][D].
+ * softmax_on_host != 0: each attention row's max / exp / denominator runs on
+ * the host with std::exp (the reference's code): every output is bit-identical
+ * to the reference forward.  0: on the device (CUDA exp, <= 1 ulp away).
+ * Synchronous when softmax_on_host (or a past cache is given), else async. */
+int epk_toy_forward(epk_ctx* ctx, const epk_toy_model* model, const int32_t* tokens, const double* pos_emb,
+                    const int64_t* positions, int64_t n, int32_t mask_kind, int64_t sink, int64_t recent,
+                    const epk_cache_desc* past, double* k_out, double* v_out, double* attention,
+                    const int64_t* attn_offsets, double* hidden_out, int32_t softmax_on_host);
 
 /* ---- diagnostics ---------------------------------------------------------- *
  * y[i] = epk_expf(x[i]) as the EPK-F32 v1 kernels compute it ([dev] fp32),

@@ -48,3 +48,19 @@ def test_cpp_multi_gpu_build_matches_reference(gpu, nccl):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "0 failed" in r.stdout
+
+
+F_BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_build", "test_forward")
+
+
+def test_cpp_device_forward_matches_reference(gpu):
+    """epikv::gpu::forward (epk_toy_forward, SURVEY 8f row 4) bit-identical to the
+    reference forward with the softmax rows on the host, within 1e-13 with them
+    on the device; gpu::block_prefill / measure_sensitivity with device forwards
+    equal the reference; the timing line compares the three block loops."""
+    if not os.path.exists(F_BIN):
+        pytest.skip("C++ forward driver not built (needs /root/reference at build time)")
+    r = subprocess.run([F_BIN, "--timing"], capture_output=True, text=True, timeout=1800)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "0 failed" in r.stdout
