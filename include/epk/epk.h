@@ -52,6 +52,8 @@ extern "C" {
 #define EPK_ERR_EMPTY_PROMPT (-6) /* score_with_prompt: empty prompt (scoring.hpp:82) */
 #define EPK_ERR_CUDA (-7)         /* CUDA runtime / launch failure                  */
 #define EPK_ERR_UNSUPPORTED (-8)  /* shape outside what the kernels support         */
+#define EPK_ERR_NAN (-9)          /* a score is NaN (non-finite K/Q): no selection   */
+                                  /*   order exists (kvcache.hpp:181-185); deferred  */
 
 /* ---- enums ---------------------------------------------------------------- */
 #define EPK_F32 0

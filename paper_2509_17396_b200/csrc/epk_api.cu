@@ -196,6 +196,7 @@ const char* epk_status_string(int s) {
         case EPK_ERR_EMPTY_PROMPT: return "empty prompt";
         case EPK_ERR_CUDA: return "CUDA error";
         case EPK_ERR_UNSUPPORTED: return "unsupported shape";
+        case EPK_ERR_NAN: return "NaN score";
         default: return "unknown status";
     }
 }
@@ -295,7 +296,10 @@ int epk_ctx_poll_error(epk_ctx* ctx) {
         EPK_CUDA_CHECK(cudaMemsetAsync(ctx->err_flag, 0, sizeof(int), ctx->stream));
         EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         if (v == EPK_ERR_PIN_OVERFLOW) return fail(v, "evict_to_budget: pinned entries exceed layer budget");
-        return fail(v, "device-side capacity check failed (slack or output buffer too small)");
+        if (v == EPK_ERR_NAN) return fail(v, "evict_to_budget: NaN score (non-finite keys or prompt)");
+        if (v == EPK_ERR_CUDA) return fail(v, "device-side wait timed out (a producer kernel never ran)");
+        return fail(v, "device-side check failed: a head longer than n_max_per_head, or slack / output capacity "
+                       "too small");
     }
     return EPK_OK;
 }

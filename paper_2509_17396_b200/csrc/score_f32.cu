@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(256) f32_colscore_kernel(const __grid_constant
         if (!P.agg_max) acc = __fdiv_rn(acc, float(P.p));
         best = fmaxf(best, acc);
     }
+    if (best != best) atomicCAS(P.err_flag, 0, EPK_ERR_NAN);
     P.scores[P.layer_base + P.off[h] + j] = best;
 }
 

@@ -120,6 +120,7 @@ struct TcParams {
     uint32_t* keys;         // [rows] or null
     uint32_t* hist_fine;    // [L][65536]
     uint32_t* hist_coarse;  // [L][256]
+    int* err_flag;          // EPK_ERR_NAN on a NaN score
 };
 
 // ---- tile-balanced partition ------------------------------------------------
@@ -217,6 +218,7 @@ constexpr int kMaxSlots = 16;  // P1 CTAs per run held in the P2 slot list
 // SCORE output of one live row: the score, and (fused selection) its key and
 // histogram counts.
 __device__ __forceinline__ void emit_score(const TcParams& P, int layer, int64_t row, float sc, uint32_t* s_coarse) {
+    if (sc != sc) atomicCAS(P.err_flag, 0, EPK_ERR_NAN);  // non-finite inputs: the selection has no order for NaN
     P.scores[row] = sc;
     if (P.keys) {
         P.keys[row] = desc_key(sc);
@@ -751,6 +753,7 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.c2 = float((1.0 / std::sqrt(double(kD))) * 1.4426950408889634);
     P.scores = scores;
     P.agg_max = agg_max;
+    P.err_flag = ctx->err_flag;
     P.keys = fs ? fs->keys : nullptr;
     P.hist_fine = fs ? fs->hist_fine : nullptr;
     P.hist_coarse = fs ? fs->hist_coarse : nullptr;

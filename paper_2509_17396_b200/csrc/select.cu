@@ -386,7 +386,9 @@ __global__ void __launch_bounds__(kSelThreads, 4) select_kernel(const __grid_con
                 ++pinned_mine;
                 continue;
             }
-            k[u] = desc_key(__ldcg(scores + r));
+            const ScoreT sv = __ldcg(scores + r);
+            if (sv != sv) atomicCAS(P.err_flag, 0, EPK_ERR_NAN);  // no order for NaN (kvcache.hpp:181-185)
+            k[u] = desc_key(sv);
             kmin = k[u] < kmin ? k[u] : kmin;
             kmax = k[u] > kmax ? k[u] : kmax;
         }

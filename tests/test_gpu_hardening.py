@@ -162,3 +162,24 @@ def test_two_contexts_two_threads(gpu):
     live = torch.cat([cin.live_rows(l) for l in range(3)])
     for o in outs:
         assert torch.equal(o[live].view(torch.int32), ref[live].view(torch.int32))
+
+
+def test_nan_scores_are_refused(gpu):
+    """SURVEY 7 hard part 5: a NaN score has no place in evict_to_budget's
+    order (kvcache.hpp:181-185); the scorers and the generic select flag it
+    (deferred EPK_ERR_NAN) instead of selecting on garbage."""
+    from paper_2509_17396_b200.step import evict_step
+    rng = np.random.default_rng(6)
+    cin, cap = _cache(gpu, rng, [[100, 80]], 4)
+    cin.k[3, 0] = float("nan")
+    q = torch.randn(1, 4, 8, 128, device="cuda").bfloat16()
+    kp = torch.randn(1, 2, 8, 128, device="cuda").bfloat16()
+    out = gpu.EpisodeCache(1, 2, 128, cap, torch.bfloat16, "cuda")
+    evict_step(cin, out, q, kp, [50], mode="tc_bf16", slack=4)
+    torch.cuda.synchronize()
+    with pytest.raises(gpu.Error, match="NaN"):
+        gpu.default_context(0).poll_error()
+    scores = torch.rand(cin.rows, device="cuda")
+    scores[int(cin.live_rows(0)[7])] = float("nan")
+    with pytest.raises(gpu.Error, match="NaN"):
+        gpu.select_pooled(cin, scores, [50])
