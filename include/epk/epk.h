@@ -274,6 +274,21 @@ int epk_serialize_epkv(epk_ctx* ctx, const epk_cache_desc* cache, uint64_t episo
                        uint64_t budget_per_head, const int64_t* layer_budgets, int32_t n_layer_budgets,
                        uint8_t* out, int64_t capacity, int64_t* offset_out, int64_t* total_out);
 
+/* The reader (load_cache, kvcache.hpp:321-374; Phase B "KVs Retrieve").
+ * epk_epkv_scan walks a file's structure on the host: info [4] = {layers,
+ * kv_heads, dim, header bytes}; counts [layers*kv_heads] entry counts and
+ * entry_off [layers*kv_heads] byte offsets of each head's first entry (either
+ * may be NULL).  Fails closed on bad magic / version / truncation, like the
+ * reference.  epk_load_epkv narrows every entry of the file (copied to the
+ * device at dev_file + pad, pad chosen so that pad + entry_off[0] is a
+ * multiple of 4) into `cache` (F32 / BF16 / F64; head_off / head_len already
+ * laid out for the counts): positions, keys, values.  A value that does not
+ * round-trip to the cache dtype, or a dim that differs, raises a deferred
+ * EPK_ERR_ARG.  Asynchronous. */
+int epk_epkv_scan(const uint8_t* bytes, int64_t nbytes, int64_t* info, int64_t* counts, int64_t* entry_off);
+int epk_load_epkv(epk_ctx* ctx, const uint8_t* dev_file, int64_t pad, const int64_t* entry_off,
+                  const epk_cache_desc* cache);
+
 /* ---- K5: layer sensitivity ------------------------------------------------ *
  * sigma[l] = mean over (h, t) of cosine(k_full, k_block), zero-norm pairs
  * skipped (allocation.hpp:80-100).  k_full, k_block [dev] [layers][kv_heads][ntok][dim]

@@ -13,7 +13,7 @@ from .clustering import KMeansResult, kmeans, kmeans_multi_device, kmeans_sharde
 from .allocation import (BudgetAllocation, SensitivityProfile, allocate, sensitivity_from_keys,  # noqa: F401
                          uniform_allocation)
 from .context import Context, default_context  # noqa: F401
-from .store import (CacheMeta, CacheStore, SessionState, centroid_similarity, load_cache, manifest_json,  # noqa: F401
+from .store import (CacheMeta, CacheStore, SessionState, centroid_similarity, load_cache, manifest_json, retrieve,  # noqa: F401,E501
                     persist, route, serialize)
 
 __version__ = "0.1.0"

@@ -70,6 +70,8 @@ _SIGS = {
     "epk_kmeans_sq_dist": (C.c_int, [vp, vp, i64, i64, vp, vp, vp]),
     "epk_kmeans": (C.c_int, [vp, vp, i64, i64, i64, u64, i64, vp, vp, vp, vp]),
     "epk_pool_scores": (C.c_int, [vp, C.POINTER(CacheDesc), vp, vp, i32]),
+    "epk_epkv_scan": (C.c_int, [vp, i64, vp, vp, vp]),
+    "epk_load_epkv": (C.c_int, [vp, vp, i64, vp, C.POINTER(CacheDesc)]),
     "epk_kmeans_sharded": (C.c_int, [vp, i32, vp, vp, i64, i64, u64, i64, vp, vp, vp, vp]),
     "epk_key_cosine_sigma": (C.c_int, [vp, vp, vp, i32, i32, i32, i64, i32, vp, vp]),
     "epk_score_keydiff": (C.c_int, [vp, vp, vp]),

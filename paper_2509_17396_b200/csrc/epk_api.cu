@@ -139,6 +139,8 @@ int launch_step_tc_grouped(epk_ctx*, const epk_cache_desc*, const epk_cache_desc
                            epk_cache_desc (*)(const epk_cache_desc*, int, int));
 int launch_append(epk_ctx*, const epk_cache_desc*, const void*, const void*, const int32_t*, int);
 int launch_pool_scores(epk_ctx*, const epk_cache_desc*, const float*, float*, int);
+int scan_epkv(const uint8_t*, int64_t, int64_t*, int64_t*, int64_t*);
+int launch_load_epkv(epk_ctx*, const uint8_t*, int64_t, const int64_t*, const epk_cache_desc*);
 int kmeans_shards(epk_ctx* const*, int, const double* const*, const int64_t*, int64_t, int64_t, uint64_t, int64_t,
                   int64_t*, double*, int64_t*, double*);
 int launch_score_f32(epk_ctx*, const epk_cache_desc*, const float*, const float*, int, int, int, int64_t, float*);
@@ -684,6 +686,20 @@ int epk_serialize_epkv(epk_ctx* ctx, const epk_cache_desc* cache, uint64_t episo
     if (n_layer_budgets < 0) return fail(EPK_ERR_ARG, "persist: negative layer budget count");
     return launch_serialize_epkv(ctx, cache, episode_id, scorer, budget_per_head, layer_budgets, n_layer_budgets, out,
                                  capacity, offset_out, total_out);
+}
+
+int epk_epkv_scan(const uint8_t* bytes, int64_t nbytes, int64_t* info, int64_t* counts, int64_t* entry_off) {
+    if (!info) return fail(EPK_ERR_ARG, "load: null info");
+    return scan_epkv(bytes, nbytes, info, counts, entry_off);
+}
+
+int epk_load_epkv(epk_ctx* ctx, const uint8_t* dev_file, int64_t pad, const int64_t* entry_off,
+                  const epk_cache_desc* cache) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if ((rc = check_cache(cache))) return rc;
+    if (!dev_file || !entry_off) return fail(EPK_ERR_ARG, "load: null pointer");
+    return launch_load_epkv(ctx, dev_file, pad, entry_off, cache);
 }
 
 // ---- diagnostics ---------------------------------------------------------------

@@ -191,4 +191,176 @@ int launch_serialize_epkv(epk_ctx* ctx, const epk_cache_desc* c, uint64_t episod
     return EPK_OK;
 }
 
+// ---------------------------------------------------------------------------
+// K7': the store's reader (load_cache, kvcache.hpp:321-374, Phase B "KVs
+// Retrieve") on the GPU: the host walks the header and the per-head counts
+// (epk_epkv_scan), the file bytes go to the device in one copy, and a kernel
+// narrows every entry into a device cache, checking that each value
+// round-trips (fails closed like the reference's loader).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct LoadParams {
+    LayerTable lt;
+    int H, d;
+    const int32_t* head_off;     // [L][H+1] of the output cache
+    const int32_t* head_len;     // [L][H]
+    const int64_t* head_word;    // [L][H] word offset of the head's first entry (from the file start + pad)
+    const uint32_t* words;       // the file, 4-byte aligned body
+    void* k;
+    void* v;
+    int32_t* pos;
+    int* err_flag;
+};
+
+template <typename T>
+__device__ __forceinline__ T ld_narrow(double x, bool& exact);
+template <>
+__device__ __forceinline__ float ld_narrow<float>(double x, bool& exact) {
+    const float f = __double2float_rn(x);
+    exact = double(f) == x || (x != x);
+    return f;
+}
+template <>
+__device__ __forceinline__ double ld_narrow<double>(double x, bool& exact) {
+    exact = true;
+    return x;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 ld_narrow<__nv_bfloat16>(double x, bool& exact) {
+    const __nv_bfloat16 b = __double2bfloat16(x);
+    exact = double(__bfloat162float(b)) == x || (x != x);
+    return b;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) epkv_read_kernel(const __grid_constant__ LoadParams P) {
+    const int h = blockIdx.y, l = blockIdx.z;
+    const int n = P.head_len[l * P.H + h];
+    const int e0 = blockIdx.x * kStoreEntriesPerCta;
+    if (e0 >= n) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t words = 3 + 4 * int64_t(P.d);
+    const int64_t row0 = P.lt.base[l] + P.head_off[l * (P.H + 1) + h];
+    const uint32_t* first = P.words + P.head_word[l * P.H + h];
+    bool ok = true;
+    for (int e = e0 + warp; e < min(n, e0 + kStoreEntriesPerCta); e += 8) {
+        const uint32_t* in = first + int64_t(e) * words;
+        const int64_t row = row0 + e;
+        if (lane == 0) {
+            const uint64_t ps = uint64_t(in[0]) | (uint64_t(in[1]) << 32);
+            if (in[2] != uint32_t(P.d) || ps > 0x7fffffffull) ok = false;
+            P.pos[row] = int32_t(ps);
+        }
+        for (int j = lane; j < 2 * P.d; j += 32) {
+            const uint64_t b = uint64_t(in[3 + 2 * j]) | (uint64_t(in[4 + 2 * j]) << 32);
+            bool ex;
+            const T x = ld_narrow<T>(__longlong_as_double(static_cast<long long>(b)), ex);
+            ok = ok && ex;
+            if (j < P.d) static_cast<T*>(P.k)[row * P.d + j] = x;
+            else static_cast<T*>(P.v)[row * P.d + (j - P.d)] = x;
+        }
+    }
+    if (!ok) atomicCAS(P.err_flag, 0, EPK_ERR_ARG);
+}
+
+int64_t rd_le(const uint8_t* b, int64_t at, int n) {
+    uint64_t v = 0;
+    for (int i = 0; i < n; ++i) v |= uint64_t(b[at + i]) << (8 * i);
+    return int64_t(v);
+}
+
+}  // namespace
+
+// Host walk of the file structure: info = {layers, heads, dim, header bytes};
+// counts [L*H] and entry_off [L*H] (byte offset of each head's first entry).
+int scan_epkv(const uint8_t* b, int64_t n, int64_t* info, int64_t* counts, int64_t* entry_off) {
+    auto need = [&](int64_t at, int64_t len) { return at + len <= n; };
+    if (!b || n < 34 || std::memcmp(b, "EPKV", 4) != 0) return fail(EPK_ERR_ARG, "load: bad magic");
+    if (rd_le(b, 4, 2) != 1) return fail(EPK_ERR_ARG, "load: version mismatch");
+    int64_t at = 14;
+    const int64_t L = rd_le(b, at, 4);
+    at += 8;  // layers, heads of layer 0
+    if (!need(at, 4)) return fail(EPK_ERR_ARG, "load: cache file truncated");
+    const int64_t slen = rd_le(b, at, 4);
+    at += 4 + slen + 8;
+    if (!need(at, 4)) return fail(EPK_ERR_ARG, "load: cache file truncated");
+    const int64_t nb = rd_le(b, at, 4);
+    at += 4 + 8 * nb;
+    const int64_t header = at;
+    int64_t H = -1, dim = -1;
+    std::vector<int64_t> cnt, off;
+    for (int64_t l = 0; l < L; ++l) {
+        if (!need(at, 12)) return fail(EPK_ERR_ARG, "load: cache file truncated");
+        const int64_t heads = rd_le(b, at + 8, 4);
+        at += 12;
+        if (H < 0) H = heads;
+        if (heads != H) return fail(EPK_ERR_UNSUPPORTED, "load: layers with different head counts");
+        for (int64_t h = 0; h < heads; ++h) {
+            if (!need(at, 8)) return fail(EPK_ERR_ARG, "load: cache file truncated");
+            const int64_t c = rd_le(b, at, 8);
+            at += 8;
+            if (c > 0) {
+                if (!need(at, 12)) return fail(EPK_ERR_ARG, "load: cache file truncated");
+                const int64_t dd = rd_le(b, at + 8, 4);
+                if (dim < 0) dim = dd;
+                if (dd != dim) return fail(EPK_ERR_UNSUPPORTED, "load: ragged key dimensions");
+            }
+            cnt.push_back(c);
+            off.push_back(at);
+            const int64_t ebytes = 12 + 16 * std::max<int64_t>(dim, 0);
+            if (c < 0 || !need(at, c * ebytes)) return fail(EPK_ERR_ARG, "load: cache file truncated");
+            at += c * ebytes;
+        }
+    }
+    info[0] = L;
+    info[1] = std::max<int64_t>(H, 0);
+    info[2] = std::max<int64_t>(dim, 1);
+    info[3] = header;
+    if (counts) std::copy(cnt.begin(), cnt.end(), counts);
+    if (entry_off) std::copy(off.begin(), off.end(), entry_off);
+    return EPK_OK;
+}
+
+int launch_load_epkv(epk_ctx* ctx, const uint8_t* dev_file, int64_t pad, const int64_t* entry_off,
+                     const epk_cache_desc* c) {
+    const int L = c->layers, H = c->kv_heads, d = c->head_dim;
+    if ((reinterpret_cast<uintptr_t>(dev_file) + pad + entry_off[0]) % 4 != 0)
+        return fail(EPK_ERR_ARG, "load: the device copy of the file must put its body on a 4-byte boundary");
+    std::vector<int64_t> word(size_t(L) * H);
+    for (size_t i = 0; i < word.size(); ++i) word[i] = (pad + entry_off[i]) / 4;
+    std::vector<int32_t> len(size_t(L) * H);
+    EPK_CUDA_CHECK(cudaMemcpyAsync(len.data(), c->head_len, len.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    int rc = ws_require(ctx, int64_t(word.size()) * 8 + 256);
+    if (rc) return rc;
+    WsCarver carve(ctx->ws);
+    int64_t* d_word = carve.take<int64_t>(int64_t(word.size()));
+    EPK_CUDA_CHECK(cudaMemcpyAsync(d_word, word.data(), word.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    EPK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    LoadParams P;
+    if ((rc = make_layer_table(c, &P.lt))) return rc;
+    P.H = H;
+    P.d = d;
+    P.head_off = c->head_off;
+    P.head_len = c->head_len;
+    P.head_word = d_word;
+    P.words = reinterpret_cast<const uint32_t*>(dev_file);
+    P.k = c->k;
+    P.v = c->v;
+    P.pos = c->pos;
+    P.err_flag = ctx->err_flag;
+    int max_len = 1;
+    for (int32_t x : len) max_len = std::max(max_len, x);
+    const dim3 grid(unsigned((max_len + kStoreEntriesPerCta - 1) / kStoreEntriesPerCta), unsigned(H), unsigned(L));
+    EPK_PROF(ctx, "epkv_read");
+    if (c->dtype == EPK_BF16)
+        epkv_read_kernel<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(P);
+    else if (c->dtype == EPK_F32)
+        epkv_read_kernel<float><<<grid, 256, 0, ctx->stream>>>(P);
+    else
+        epkv_read_kernel<double><<<grid, 256, 0, ctx->stream>>>(P);
+    EPK_LAUNCH_CHECK(ctx);
+    return EPK_OK;
+}
+
 }  // namespace epk

@@ -136,11 +136,84 @@ def parse(buf: bytes, path="<bytes>"):
     return meta, per_layer
 
 
+def _parse_header(buf, path) -> CacheMeta:
+    r = _Reader(buf, path)
+    if bytes(r.take(4)) != _MAGIC:
+        raise IoError(f"load: bad magic in {path}")
+    if r.u(2) != _VERSION:
+        raise IoError(f"load: version mismatch in {path}")
+    meta = CacheMeta(episode_id=r.u(8))
+    layers = r.u(4)
+    r.u(4)
+    meta.scorer = bytes(r.take(r.u(4))).decode()
+    meta.budget_per_head = r.u(8)
+    meta.layer_budgets = [r.u(8) for _ in range(r.u(4))]
+    return meta, layers, r.p
+
+
+def retrieve(path, dtype=torch.bfloat16, device="cuda", slack: int = 0, ctx: Context | None = None):
+    """load_cache on the GPU (Phase B "KVs Retrieve"): the file is read into
+    pinned memory, its structure walked on the host (epk_epkv_scan), the bytes
+    cross PCIe in one copy and epk_load_epkv narrows every entry into a device
+    cache (values must round-trip to `dtype`, like load_cache(exact=True)).
+    -> (EpisodeCache, CacheMeta)."""
+    dev = torch.device(device)
+    ctx = ctx or default_context(dev.index if dev.index is not None else torch.cuda.current_device())
+    try:
+        size = os.path.getsize(path)
+        host = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+        with open(path, "rb") as f:
+            got = f.readinto(memoryview(host.numpy()))
+    except OSError as e:
+        raise IoError(f"load: cannot open {path}") from e
+    if got != size:
+        raise IoError("cache file truncated")
+    hb = host.numpy()
+    info = (C.c_int64 * 4)()
+    rc = _lib.load().epk_epkv_scan(C.c_void_p(host.data_ptr()), size, C.cast(info, C.c_void_p), None, None)
+    if rc != 0:
+        raise IoError(_lib.load().epk_last_error().decode())
+    L, H, d = int(info[0]), int(info[1]), int(info[2])
+    counts = np.zeros(max(1, L * H), np.int64)
+    eoff = np.zeros(max(1, L * H), np.int64)
+    _lib.call("epk_epkv_scan", C.c_void_p(host.data_ptr()), size, C.cast(info, C.c_void_p),
+              counts.ctypes.data_as(C.c_void_p), eoff.ctypes.data_as(C.c_void_p))
+    meta, _, _ = _parse_header(bytes(hb[:int(info[3])]), path)
+    if L < 1:
+        raise Error("load: cache has no layers")
+    counts = counts[:L * H].reshape(L, H)
+    cap = [int(counts[l].sum()) + slack * H for l in range(L)]
+    cache = EpisodeCache(L, H, d, cap, dtype, dev)
+    offs = np.zeros((L, H + 1), np.int32)
+    offs[:, 1:] = np.cumsum(counts + slack, axis=1)
+    cache.head_off.copy_(torch.from_numpy(offs))
+    cache.head_len.copy_(torch.from_numpy(counts.astype(np.int32)))
+    pad = (-int(eoff[0])) % 4
+    dfile = torch.empty(size + pad, dtype=torch.uint8, device=dev)
+    dfile[pad:].copy_(host, non_blocking=True)
+    desc = cache.desc()
+    _lib.call("epk_load_epkv", ctx.handle, ptr(dfile), pad, eoff.ctypes.data_as(C.c_void_p), C.byref(desc))
+    ctx.poll_error()  # fails closed: a value that does not round-trip to dtype
+    meta.layer_budget_fields = _layer_budget_fields(hb, int(info[3]), L, H, counts, d)  # kvcache.hpp:304
+    return cache, meta
+
+
+def _layer_budget_fields(hb, at, L, H, counts, d):
+    out = []
+    for l in range(L):
+        out.append(int.from_bytes(bytes(hb[at:at + 8]), "little"))
+        at += 12
+        for h in range(H):
+            at += 8 + int(counts[l, h]) * (12 + 16 * d)
+    return out
+
+
 def load_cache(path, dtype=torch.bfloat16, device="cuda", slack: int = 0, exact: bool = True):
     """load_cache (kvcache.hpp:321): -> (EpisodeCache, CacheMeta).  The fp64
     reals narrow to `dtype`; with exact=True a value that does not round-trip
     raises (a bf16/fp32 cache persisted by `persist` always round-trips).
-    Each head gets `slack` free rows after its entries (room for appends)."""
+    Each head gets `slack` free rows after its entries (room for appends).
+    Host-side parse (numpy); `retrieve` is the same on the GPU."""
     try:
         with open(path, "rb") as f:
             buf = f.read()

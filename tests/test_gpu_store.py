@@ -107,3 +107,34 @@ def test_cache_store_and_route(gpu, tmp_path):
     assert state.resident.entries_per_layer() == [4 + 2 + 2]
     with pytest.raises(gpu.IoError, match="unknown episode id"):
         st.load(9)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "f64"])
+def test_device_retrieve_equals_host_load(gpu, tmp_path, dtype):
+    """Phase B retrieve on the GPU (epk_epkv_scan + epk_load_epkv): the same
+    cache, positions, metadata and per-layer budget fields as the host
+    load_cache; values that do not round-trip to the dtype fail closed; a
+    truncated file fails closed."""
+    rng = np.random.default_rng({"bf16": 4, "f32": 5, "f64": 6}[dtype])
+    L, H, d = 3, 4, 128 if dtype != "f64" else 16
+    pl = _data(rng, L, H, d, [[30, 0, 7, 12], [1, 1, 1, 1], [0, 0, 0, 5]], dtype)
+    cache = gpu.EpisodeCache(L, H, d, [int(c.sum()) + 8 * H for c, _, _, _ in pl], TORCH[dtype], "cuda")
+    cache.load_layers(pl, slack=8)
+    src = tmp_path / "c.epkv"
+    gpu.persist(cache, src, episode_id=5, scorer="patched", budget_per_head=9, layer_budgets=[3, 4, 5])
+    a, ma = gpu.load_cache(src, dtype=TORCH[dtype], slack=4)
+    b, mb = gpu.retrieve(src, dtype=TORCH[dtype], slack=4)
+    assert ma == mb
+    assert torch.equal(a.head_off, b.head_off) and torch.equal(a.head_len, b.head_len)
+    for l in range(L):
+        ra, rb = a.live_rows(l), b.live_rows(l)
+        assert torch.equal(a.pos[ra], b.pos[rb])
+        assert torch.equal(a.k[ra].view(torch.uint8), b.k[rb].view(torch.uint8))
+        assert torch.equal(a.v[ra].view(torch.uint8), b.v[rb].view(torch.uint8))
+    if dtype == "f64":  # fp64 values do not fit bf16: fail closed like load_cache(exact=True)
+        with pytest.raises(gpu.Error):
+            gpu.retrieve(src, dtype=torch.bfloat16)
+    cut = tmp_path / "cut.epkv"
+    cut.write_bytes(src.read_bytes()[:-7])
+    with pytest.raises(gpu.IoError):
+        gpu.retrieve(cut)
