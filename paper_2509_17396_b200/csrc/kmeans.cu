@@ -486,6 +486,22 @@ int launch_key_cosine(epk_ctx* ctx, const void* kf, const void* kb, int dtype, i
     if ((rc = ensure_aux_stream(ctx)) || (rc = k5_preload())) return rc;
     cudaStream_t main = ctx->stream;
     EPK_CUDA_CHECK(cudaMemsetAsync(P.ready, 0, size_t(tiles * layers) * 4, main));
+    // EPK_K5_SERIAL=1 (profilers that serialise kernels, e.g. ncu): pairs first,
+    // then the chain on the same stream -- same results, no overlap
+    static const bool serial = std::getenv("EPK_K5_SERIAL") != nullptr;
+    if (serial) {
+        if (dtype == EPK_F64) rc = k5_launch_pair<double>(ctx, P);
+        else if (dtype == EPK_F32) rc = k5_launch_pair<float>(ctx, P);
+        else rc = k5_launch_pair<__nv_bfloat16>(ctx, P);
+        if (rc) return rc;
+        EPK_PROF(ctx, "cosine_chain");
+        cosine_chain_kernel<<<layers, 64, 0, main>>>(P, tr);
+        EPK_LAUNCH_CHECK(ctx);
+        EPK_PROF(ctx, "cosine_total");
+        cosine_skip_total_kernel<<<1, 32, 0, main>>>(P.skipped_per_layer, layers, skipped);
+        EPK_LAUNCH_CHECK(ctx);
+        return EPK_OK;
+    }
     // the chain CTAs follow the pair tiles' ready flags from the aux stream
     EPK_CUDA_CHECK(cudaEventRecord(ctx->ev_aux_fork, main));
     EPK_CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->ev_aux_fork, 0));

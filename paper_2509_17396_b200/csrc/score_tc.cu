@@ -620,6 +620,7 @@ __global__ void __maxnreg__(128)
                                                      s_slot + cg * kMaxSlots, n)
                                        : merge_lse2(P, x.hk, r, T1);
                         }
+                        if (v != v) atomicCAS(P.err_flag, 0, EPK_ERR_NAN);  // a NaN logit poisoned the row's sum
                         s_lse[r] = -v;  // negated: the epilogue adds it with FFMA2
                     }
                     named_bar_sync(1, 32 * kEpiWarps);

@@ -161,14 +161,14 @@ def retrieve(path, dtype=torch.bfloat16, device="cuda", slack: int = 0, ctx: Con
     ctx = ctx or default_context(dev.index if dev.index is not None else torch.cuda.current_device())
     try:
         size = os.path.getsize(path)
-        host = torch.empty(size, dtype=torch.uint8, pin_memory=True)
         with open(path, "rb") as f:
-            got = f.readinto(memoryview(host.numpy()))
+            hb = np.empty(size, np.uint8)
+            got = f.readinto(memoryview(hb))
     except OSError as e:
         raise IoError(f"load: cannot open {path}") from e
     if got != size:
         raise IoError("cache file truncated")
-    hb = host.numpy()
+    host = torch.from_numpy(hb)
     info = (C.c_int64 * 4)()
     rc = _lib.load().epk_epkv_scan(C.c_void_p(host.data_ptr()), size, C.cast(info, C.c_void_p), None, None)
     if rc != 0:
@@ -190,12 +190,38 @@ def retrieve(path, dtype=torch.bfloat16, device="cuda", slack: int = 0, ctx: Con
     cache.head_len.copy_(torch.from_numpy(counts.astype(np.int32)))
     pad = (-int(eoff[0])) % 4
     dfile = torch.empty(size + pad, dtype=torch.uint8, device=dev)
-    dfile[pad:].copy_(host, non_blocking=True)
+    _staged_h2d(dfile[pad:], host)
     desc = cache.desc()
     _lib.call("epk_load_epkv", ctx.handle, ptr(dfile), pad, eoff.ctypes.data_as(C.c_void_p), C.byref(desc))
     ctx.poll_error()  # fails closed: a value that does not round-trip to dtype
     meta.layer_budget_fields = _layer_budget_fields(hb, int(info[3]), L, H, counts, d)  # kvcache.hpp:304
     return cache, meta
+
+
+_STAGE = []
+
+
+def _staged_h2d(dst: torch.Tensor, src: torch.Tensor, chunk: int = 64 << 20) -> None:
+    """Pageable host bytes -> device through two reused pinned 64 MB buffers
+    (the memcpy into one overlaps the DMA out of the other)."""
+    if not _STAGE:
+        _STAGE.extend(torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2))
+        _STAGE.extend(torch.cuda.Event() for _ in range(2))
+    bufs, evs = _STAGE[:2], _STAGE[2:]
+    stream = torch.cuda.current_stream(dst.device)
+    used = [False, False]
+    for i, a in enumerate(range(0, src.numel(), chunk)):
+        j = i % 2
+        n = min(chunk, src.numel() - a)
+        if used[j]:
+            evs[j].synchronize()
+        bufs[j][:n].copy_(src[a:a + n])
+        dst[a:a + n].copy_(bufs[j][:n], non_blocking=True)
+        evs[j].record(stream)
+        used[j] = True
+    for j in range(2):
+        if used[j]:
+            evs[j].synchronize()
 
 
 def _layer_budget_fields(hb, at, L, H, counts, d):
