@@ -152,36 +152,35 @@ def _parse_header(buf, path) -> CacheMeta:
 
 
 def retrieve(path, dtype=torch.bfloat16, device="cuda", slack: int = 0, ctx: Context | None = None):
-    """load_cache on the GPU (Phase B "KVs Retrieve"): the file is read into
-    pinned memory, its structure walked on the host (epk_epkv_scan), the bytes
-    cross PCIe in one copy and epk_load_epkv narrows every entry into a device
-    cache (values must round-trip to `dtype`, like load_cache(exact=True)).
-    -> (EpisodeCache, CacheMeta)."""
+    """load_cache on the GPU (Phase B "KVs Retrieve"): the file's structure is
+    walked on the host through a memory map (epk_epkv_scan touches only the
+    header and count fields), the bytes stream from the file into reused
+    pinned buffers and across PCIe, and epk_load_epkv narrows every entry into
+    a device cache (values must round-trip to `dtype`, like
+    load_cache(exact=True)).  -> (EpisodeCache, CacheMeta)."""
     dev = torch.device(device)
     ctx = ctx or default_context(dev.index if dev.index is not None else torch.cuda.current_device())
     try:
         size = os.path.getsize(path)
-        with open(path, "rb") as f:
-            hb = np.empty(size, np.uint8)
-            got = f.readinto(memoryview(hb))
-    except OSError as e:
+        mm = np.memmap(path, dtype=np.uint8, mode="r") if size else np.zeros(0, np.uint8)
+    except (OSError, ValueError) as e:
         raise IoError(f"load: cannot open {path}") from e
-    if got != size:
-        raise IoError("cache file truncated")
-    host = torch.from_numpy(hb)
     info = (C.c_int64 * 4)()
-    rc = _lib.load().epk_epkv_scan(C.c_void_p(host.data_ptr()), size, C.cast(info, C.c_void_p), None, None)
+    base = C.c_void_p(mm.ctypes.data if size else 0)
+    rc = _lib.load().epk_epkv_scan(base, size, C.cast(info, C.c_void_p), None, None)
     if rc != 0:
         raise IoError(_lib.load().epk_last_error().decode())
     L, H, d = int(info[0]), int(info[1]), int(info[2])
     counts = np.zeros(max(1, L * H), np.int64)
     eoff = np.zeros(max(1, L * H), np.int64)
-    _lib.call("epk_epkv_scan", C.c_void_p(host.data_ptr()), size, C.cast(info, C.c_void_p),
-              counts.ctypes.data_as(C.c_void_p), eoff.ctypes.data_as(C.c_void_p))
-    meta, _, _ = _parse_header(bytes(hb[:int(info[3])]), path)
+    _lib.call("epk_epkv_scan", base, size, C.cast(info, C.c_void_p), counts.ctypes.data_as(C.c_void_p),
+              eoff.ctypes.data_as(C.c_void_p))
+    meta, _, _ = _parse_header(bytes(mm[:int(info[3])]), path)
     if L < 1:
         raise Error("load: cache has no layers")
     counts = counts[:L * H].reshape(L, H)
+    meta.layer_budget_fields = _layer_budget_fields(mm, int(info[3]), L, H, counts, d)  # kvcache.hpp:304
+    del mm
     cap = [int(counts[l].sum()) + slack * H for l in range(L)]
     cache = EpisodeCache(L, H, d, cap, dtype, dev)
     offs = np.zeros((L, H + 1), np.int32)
@@ -190,32 +189,37 @@ def retrieve(path, dtype=torch.bfloat16, device="cuda", slack: int = 0, ctx: Con
     cache.head_len.copy_(torch.from_numpy(counts.astype(np.int32)))
     pad = (-int(eoff[0])) % 4
     dfile = torch.empty(size + pad, dtype=torch.uint8, device=dev)
-    _staged_h2d(dfile[pad:], host)
+    try:
+        with open(path, "rb", buffering=0) as f:
+            _file_to_device(f, size, dfile[pad:])
+    except OSError as e:
+        raise IoError(f"load: cannot read {path}") from e
     desc = cache.desc()
     _lib.call("epk_load_epkv", ctx.handle, ptr(dfile), pad, eoff.ctypes.data_as(C.c_void_p), C.byref(desc))
     ctx.poll_error()  # fails closed: a value that does not round-trip to dtype
-    meta.layer_budget_fields = _layer_budget_fields(hb, int(info[3]), L, H, counts, d)  # kvcache.hpp:304
     return cache, meta
 
 
 _STAGE = []
 
 
-def _staged_h2d(dst: torch.Tensor, src: torch.Tensor, chunk: int = 64 << 20) -> None:
-    """Pageable host bytes -> device through two reused pinned 64 MB buffers
-    (the memcpy into one overlaps the DMA out of the other)."""
+def _file_to_device(f, size: int, dst: torch.Tensor, chunk: int = 64 << 20) -> None:
+    """File bytes -> device through two reused pinned 64 MB buffers: the read
+    into one overlaps the DMA out of the other."""
     if not _STAGE:
         _STAGE.extend(torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2))
         _STAGE.extend(torch.cuda.Event() for _ in range(2))
     bufs, evs = _STAGE[:2], _STAGE[2:]
     stream = torch.cuda.current_stream(dst.device)
     used = [False, False]
-    for i, a in enumerate(range(0, src.numel(), chunk)):
+    for i, a in enumerate(range(0, size, chunk)):
         j = i % 2
-        n = min(chunk, src.numel() - a)
+        n = min(chunk, size - a)
         if used[j]:
             evs[j].synchronize()
-        bufs[j][:n].copy_(src[a:a + n])
+        got = f.readinto(memoryview(bufs[j].numpy())[:n])
+        if got != n:
+            raise IoError("cache file truncated")
         dst[a:a + n].copy_(bufs[j][:n], non_blocking=True)
         evs[j].record(stream)
         used[j] = True
