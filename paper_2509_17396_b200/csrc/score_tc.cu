@@ -110,8 +110,17 @@ struct TcParams {
     const int32_t* head_len;
     int32_t* p1_pre;  // [p1_runs + 1] run prefix of the STATS launch over this layer range (its CTA 0 writes it)
     float c2;         // d^-1/2 * log2(e)
-    float* part_m;    // [L*H*NQ*128][slots]
+    float* part_m;    // [slots][prow]: slot-major, so P1's writes and the merge's reads coalesce over rows
     float* part_z;
+    int64_t prow;     // query rows of the whole plan (L*H*NQ*128)
+    int sj, sj_n0, sj_nl;  // SCORE MMA jobs per K tile: count, N of all but the last, N of the last
+    // SCORE: per (head, query row) -lse2/c2 split into three bf16 terms, in
+    // the no-swizzle K-major operand layout of a 16-wide MMA K-step (32 B per
+    // row; tc_bias_kernel writes it between the passes, P2 loads it next to
+    // each query chunk):
+    // the lse subtraction runs inside the MMA as one extra K-step.
+    const uint8_t* bias;  // [L*H][NQ*128 rows][32 B]
+    uint8_t* bias_out;    // tc_bias_kernel's output (the same buffer)
     float* scores;
     int agg_max;
     // SCORE, fused selection histogram (threshold select, select.cu): per
@@ -213,8 +222,6 @@ __device__ __forceinline__ Seg seg_at(const TcParams& P, const int32_t* s_pre, i
     return x;
 }
 
-constexpr int kMaxSlots = 16;  // P1 CTAs per run held in the P2 slot list
-
 // SCORE output of one live row: the score, and (fused selection) its key and
 // histogram counts.
 __device__ __forceinline__ void emit_score(const TcParams& P, int layer, int64_t row, float sc, uint32_t* s_coarse) {
@@ -238,53 +245,123 @@ __device__ __forceinline__ void flush_coarse(const TcParams& P, int layer, uint3
     }
 }
 
-// lse2 from a row's partials at the listed slots.
-__device__ __forceinline__ float merge_slots(const float* pm, const float* pz, const int* slot, int n) {
+// lse2 of STATS query row rq of head hk (launch-local) from the partials of
+// every P1 CTA that covered the row's run: `pre` = the P1 launch's run prefix,
+// `grid` its CTAs, `run_hk_base` its heads before this launch's first.  The
+// partials of other CTAs are read through L2 (ld.cg).
+__device__ float merge_lse2(const TcParams& P, const int32_t* pre, int grid, int run_hk_base, int hk, int rq,
+                            int64_t T1) {
+    const int cg = (rq / kChunk) / P.cg_chunks;
+    const int run = (hk + run_hk_base) * P.cgroups + cg;
+    const int R0 = pre[run], R1 = pre[run + 1];
+    if (R1 <= R0) return INFINITY;
+    const int b0 = part_cnt(T1, grid, R0) - 1, b1 = part_cnt(T1, grid, R1 - 1) - 1;
+    const int64_t row = int64_t(hk + P.hk_base) * (P.NQ * kChunk) + rq;
+    const float* pm = P.part_m + row;
+    const float* pz = P.part_z + row;
     float M = -INFINITY;
-    for (int i = 0; i < n; ++i)
-#pragma unroll
-        for (int u = 0; u < kStatGroups; ++u) M = fmaxf(M, pm[slot[i] + u]);
+    for (int b = b0; b <= b1; ++b) {
+        const int lo = max(R0, part_bound(T1, grid, b)), hi = min(R1, part_bound(T1, grid, b + 1));
+        if (lo >= hi) continue;
+        const int s = kStatGroups * (b - b0);
+        for (int u = 0; u < kStatGroups; ++u) M = fmaxf(M, __ldcg(pm + (s + u) * P.prow));
+    }
     if (M == -INFINITY) return INFINITY;
     float Z = 0.f;
-    for (int i = 0; i < n; ++i) {
+    for (int b = b0; b <= b1; ++b) {
+        const int lo = max(R0, part_bound(T1, grid, b)), hi = min(R1, part_bound(T1, grid, b + 1));
+        if (lo >= hi) continue;
+        const int s = kStatGroups * (b - b0);
 #pragma unroll
         for (int u = 0; u < kStatGroups; ++u) {
-            const float mu = pm[slot[i] + u];
-            if (mu != -INFINITY) Z += pz[slot[i] + u] * ex2(mu - M);
+            const float mu = __ldcg(pm + (s + u) * P.prow);
+            if (mu != -INFINITY) Z += __ldcg(pz + (s + u) * P.prow) * ex2(mu - M);
         }
     }
     return M + log2f(Z);
 }
 
-// lse2 of STATS query row rq of head hk (launch-local) from the partials of
-// every P1 CTA that covered the row's run (general path: any number of P1 CTAs).
-__device__ float merge_lse2(const TcParams& P, int hk, int rq, int64_t T1) {
-    const int cg = (rq / kChunk) / P.cg_chunks;
-    const int run = (hk + P.run_hk_base) * P.cgroups + cg;
-    const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
-    if (R1 <= R0) return INFINITY;
-    const int b0 = part_cnt(T1, P.p1_grid, R0) - 1, b1 = part_cnt(T1, P.p1_grid, R1 - 1) - 1;
-    const int64_t row = int64_t(hk + P.hk_base) * (P.NQ * kChunk) + rq;
-    const float* pm = P.part_m + row * P.slots;
-    const float* pz = P.part_z + row * P.slots;
-    float M = -INFINITY;
-    for (int b = b0; b <= b1; ++b) {
-        const int lo = max(R0, part_bound(T1, P.p1_grid, b)), hi = min(R1, part_bound(T1, P.p1_grid, b + 1));
-        if (lo >= hi) continue;
-        const int s = kStatGroups * (b - b0);
-        for (int u = 0; u < kStatGroups; ++u) M = fmaxf(M, pm[s + u]);
+// P2's bias operand row of (head hk, query row rq) from its lse2:
+// -lse2/c2 = h + m + l (bf16 parts; each residual is exact in fp32, so the sum
+// carries ~24 bits).  Padding rows (>= G*p) and rows with no live column get
+// h = -1e30 (finite: the zero K elements of A' multiply it), so their columns
+// never win the max.
+__device__ void write_bias_row(const TcParams& P, int hk, int rq, float lse2) {
+    float h = -1e30f, m = 0.f, l = 0.f;
+    if (rq < P.Gp) {
+        if (lse2 != lse2) atomicCAS(P.err_flag, 0, EPK_ERR_NAN);  // a NaN logit poisoned the row's sum
+        if (lse2 != INFINITY) {
+            const float v = __fdiv_rn(-lse2, P.c2);
+            const __nv_bfloat16 bh = __float2bfloat16_rn(v);
+            const float r1 = __fsub_rn(v, __bfloat162float(bh));
+            const __nv_bfloat16 bm = __float2bfloat16_rn(r1);
+            const float r2 = __fsub_rn(r1, __bfloat162float(bm));
+            h = __bfloat162float(bh);
+            m = __bfloat162float(bm);
+            l = __bfloat162float(__float2bfloat16_rn(r2));
+        }
     }
-    if (M == -INFINITY) return INFINITY;
-    float Z = 0.f;
-    for (int b = b0; b <= b1; ++b) {
-        const int lo = max(R0, part_bound(T1, P.p1_grid, b)), hi = min(R1, part_bound(T1, P.p1_grid, b + 1));
-        if (lo >= hi) continue;
-        const int s = kStatGroups * (b - b0);
+    const __nv_bfloat162 hm = __floats2bfloat162_rn(h, m), l0 = __floats2bfloat162_rn(l, 0.f);
+    uint8_t* row = P.bias_out + int64_t(hk + P.hk_base) * (P.NQ * kChunk) * kBiasRowB + bias_off(rq);
+    *reinterpret_cast<uint4*>(row) =
+        make_uint4(*reinterpret_cast<const uint32_t*>(&hm), *reinterpret_cast<const uint32_t*>(&l0), 0u, 0u);
+    *reinterpret_cast<uint4*>(row + 128) = make_uint4(0u, 0u, 0u, 0u);  // K elements 8..15
+}
+
+// Between P1 and P2, one CTA per head (NQ*128 threads, a query row each): the
+// row's lse2 from its P1 partials, written as its bias operand row.  The
+// covering P1 CTAs of each chunk group (the partial slots to merge) are
+// listed once per CTA, so the per-row work is the merge loads alone.
+constexpr int kBiasMaxCov = 32;
+__global__ void tc_bias_kernel(const __grid_constant__ TcParams P) {
+    __shared__ int s_cov[16][kBiasMaxCov];  // per chunk group: slot base of each covering P1 CTA
+    __shared__ int s_ncov[16];
+    pdl_wait();
+    const int hk = blockIdx.x;
+    const int64_t T1 = P.p1_pre[P.p1_runs];
+    if (threadIdx.x < P.cgroups) {
+        const int run = (hk + P.run_hk_base) * P.cgroups + threadIdx.x;
+        const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
+        int n = 0;
+        if (R1 > R0) {
+            const int b0 = part_cnt(T1, P.p1_grid, R0) - 1, b1 = part_cnt(T1, P.p1_grid, R1 - 1) - 1;
+            for (int b = b0; b <= b1 && n >= 0; ++b) {
+                if (max(R0, part_bound(T1, P.p1_grid, b)) >= min(R1, part_bound(T1, P.p1_grid, b + 1))) continue;
+                if (n == kBiasMaxCov) n = -1;  // more covering CTAs than listed: the general merge
+                else s_cov[threadIdx.x][n++] = kStatGroups * (b - b0);
+            }
+        }
+        s_ncov[threadIdx.x] = n;
+    }
+    __syncthreads();
+    for (int rq = threadIdx.x; rq < P.NQ * kChunk; rq += blockDim.x) {
+    float lse2 = INFINITY;
+    if (rq < P.Gp) {
+        const int cg = (rq / kChunk) / P.cg_chunks;
+        const int n = s_ncov[cg];
+        if (n < 0) {
+            lse2 = merge_lse2(P, P.p1_pre, P.p1_grid, P.run_hk_base, hk, rq, T1);
+        } else if (n > 0) {
+            const int64_t row = int64_t(hk + P.hk_base) * (P.NQ * kChunk) + rq;
+            float M = -INFINITY;
+            for (int i = 0; i < n; ++i)
 #pragma unroll
-        for (int u = 0; u < kStatGroups; ++u)
-            if (pm[s + u] != -INFINITY) Z += pz[s + u] * ex2(pm[s + u] - M);
+                for (int u = 0; u < kStatGroups; ++u) M = fmaxf(M, P.part_m[(s_cov[cg][i] + u) * P.prow + row]);
+            if (M != -INFINITY) {
+                float Z = 0.f;
+                for (int i = 0; i < n; ++i)
+#pragma unroll
+                    for (int u = 0; u < kStatGroups; ++u) {
+                        const int64_t o = (s_cov[cg][i] + u) * P.prow + row;
+                        const float mu = P.part_m[o];
+                        if (mu != -INFINITY) Z += P.part_z[o] * ex2(mu - M);
+                    }
+                lse2 = M + log2f(Z);
+            }
+        }
     }
-    return M + log2f(Z);
+    write_bias_row(P, hk, rq, lse2);
+    }
 }
 
 // <= 128 registers (45K of the SM's 64K) and <= kSmemBudget of shared memory,
@@ -293,6 +370,11 @@ __device__ float merge_lse2(const TcParams& P, int hk, int rq, int64_t T1) {
 #define P1PROF(...) __VA_ARGS__
 #else
 #define P1PROF(...)
+#endif
+#ifdef EPK_P2_PROF
+#define P2PROF(...) __VA_ARGS__
+#else
+#define P2PROF(...)
 #endif
 #ifdef EPK_NO_BACKOFF
 #define mbar_wait_pm mbar_wait
@@ -314,8 +396,9 @@ __global__ void __maxnreg__(128)
     const uint32_t k_stage = 2 * k_half;
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + 2 * q_half;
-    float* s_lse = reinterpret_cast<float*>(sK + P.kstages * k_stage);  // SCORE: NQ*128 lse2
-    float* s_pair = s_lse + (MODE == MODE_SCORE ? P.NQ * kChunk : 0);  // SCORE: [2][128] half maxima
+    uint8_t* s_bias = sK + P.kstages * k_stage;  // SCORE: bias rows of the Q region's chunks
+    uint8_t* s_aone = s_bias + (MODE == MODE_SCORE ? P.qcap * kBiasRowB : 0);  // SCORE: A' = [1 1 1 0..] x 128 rows
+    float* s_pair = reinterpret_cast<float*>(s_aone + (MODE == MODE_SCORE ? kBiasChunkB : 0));  // SCORE: [2][128] half maxima
     float* s_avg = s_pair + (MODE == MODE_SCORE ? 2 * kChunk : 0);     // SCORE avg: G*128 sums
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_avg + (MODE == MODE_SCORE && !P.agg_max ? P.G * kChunk : 0));
     uint64_t* k_full = bars;
@@ -327,8 +410,6 @@ __global__ void __maxnreg__(128)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 4);
     int32_t* s_pre = reinterpret_cast<int32_t*>(tmem_holder + 4);  // [runs + 1]
 
-    __shared__ int s_slot[16 * kMaxSlots];  // SCORE: P1 slot lists per chunk group
-    __shared__ int s_nslot[16];
     __shared__ uint32_t s_coarse[256];      // SCORE: coarse histogram of the current layer
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool resident = MODE == MODE_STATS || P.resident;
@@ -360,6 +441,18 @@ __global__ void __maxnreg__(128)
     if (MODE == MODE_SCORE && !P.agg_max)
         for (int i = threadIdx.x; i < P.G * kChunk; i += blockDim.x) s_avg[i] = 0.f;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_coarse[i] = 0;
+    if (MODE == MODE_SCORE) {
+        // A' rows: bf16 1.0 in K elements 0..2, zeros elsewhere (written by
+        // threads, read by the tensor core: async-proxy fence before the barrier)
+        for (int i = threadIdx.x; i < kBiasChunkB / 4; i += blockDim.x) {
+            const int byte = i * 4, r = ((byte & 255) >> 4) + 8 * (byte >> 8), kb = byte & 15, khi = byte & 128;
+            uint32_t w = 0;
+            if (!khi && kb == 0) w = 0x3F803F80u;  // K 0, 1
+            if (!khi && kb == 4) w = 0x00003F80u;  // K 2
+            reinterpret_cast<uint32_t*>(s_aone)[i] = w;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -388,8 +481,12 @@ __global__ void __maxnreg__(128)
                     for (int c = 0; c < x.nq; ++c) {
                         mbar_wait_pm(&q_empty[c], (qload[c] & 1) ^ 1);
                         if (leader) {
-                            mbar_expect_tx(&q_full[c], 2 * kChunk * kRowB);
+                            mbar_expect_tx(&q_full[c], 2 * kChunk * kRowB + (MODE == MODE_SCORE ? kBiasChunkB : 0));
                             load_rows(sQ + c * kChunk * kRowB, q_half, &tm_q, &q_full[c], qrow0 + (x.c0 + c) * kChunk);
+                            if (MODE == MODE_SCORE)
+                                bulk_load_1d(s_bias + c * kBiasChunkB,
+                                             P.bias + (int64_t(x.hk + P.hk_base) * P.NQ + x.c0 + c) * kBiasChunkB,
+                                             kBiasChunkB, &q_full[c]);
                         }
                         __syncwarp();
                         ++qload[c];
@@ -417,10 +514,14 @@ __global__ void __maxnreg__(128)
                             const int nch = min(2, P.NQ - 2 * j);
                             mbar_wait_pm(&q_empty[slot], (qload[slot] & 1) ^ 1);
                             if (leader) {
-                                mbar_expect_tx(&q_full[slot], nch * 2 * kChunk * kRowB);
-                                for (int cc = 0; cc < nch; ++cc)
+                                mbar_expect_tx(&q_full[slot], nch * (2 * kChunk * kRowB + kBiasChunkB));
+                                for (int cc = 0; cc < nch; ++cc) {
                                     load_rows(sQ + (slot * 2 + cc) * kChunk * kRowB, q_half, &tm_q, &q_full[slot],
                                               qrow0 + (2 * j + cc) * kChunk);
+                                    bulk_load_1d(s_bias + (slot * 2 + cc) * kBiasChunkB,
+                                                 P.bias + (int64_t(x.hk + P.hk_base) * P.NQ + 2 * j + cc) * kBiasChunkB,
+                                                 kBiasChunkB, &q_full[slot]);
+                                }
                             }
                             __syncwarp();
                             ++qload[slot];
@@ -443,6 +544,7 @@ __global__ void __maxnreg__(128)
             int key = -1;
             int held = 0;
             const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK);
+            P2PROF(long long wk = 0, wt = 0, m_beg = clock64(); int ntile = 0);
             for (int g = it_beg; g < it_end;) {
                 const Seg x = seg_at<MODE>(P, s_pre, g, it_end, T);
                 g += x.ntiles();
@@ -456,7 +558,9 @@ __global__ void __maxnreg__(128)
                     fresh = true;
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
+                    P2PROF(long long c0 = clock64());
                     mbar_wait_pm(&k_full[ks], kph);
+                    P2PROF(wk += clock64() - c0; ++ntile);
                     const uint32_t kst = k0 + uint32_t(ks) * k_stage;
                     if (MODE == MODE_STATS) {
                         for (int c = 0; c < x.nq; ++c, ++job) {
@@ -476,29 +580,34 @@ __global__ void __maxnreg__(128)
                             __syncwarp();
                         }
                     } else {
-                        for (int j = 0; 2 * j < x.nq; ++j, ++job) {
-                            const int nch = min(2, x.nq - 2 * j);
-                            if (resident && fresh && t == 0)
-                                for (int cc = 0; cc < nch; ++cc) {
-                                    mbar_wait_pm(&q_full[2 * j + cc], qload[2 * j + cc] & 1);
-                                    ++qload[2 * j + cc];
-                                }
+                        if (resident && fresh && t == 0)
+                            for (int c = 0; c < x.nq; ++c) {
+                                mbar_wait_pm(&q_full[c], qload[c] & 1);
+                                ++qload[c];
+                            }
+                        for (int j = 0; j < P.sj; ++j, ++job) {
+                            const int jn = j + 1 < P.sj ? P.sj_n0 : P.sj_nl;  // query rows (MMA N) of the job
                             if ((job & 1) != mw) continue;
-                            uint32_t qb;
+                            uint32_t qb, bb;
                             const int slot = int(mw);  // streamed pair slot == TMEM slot == this warp
                             if (resident) {
-                                qb = q0 + uint32_t(2 * j * kChunk * kRowB);
+                                const int row0 = j * P.sj_n0;
+                                qb = q0 + uint32_t(row0 * kRowB);
+                                bb = smem_u32(s_bias) + uint32_t(bias_off(row0));
                             } else {
                                 mbar_wait_pm(&q_full[slot], qload[slot] & 1);
                                 ++qload[slot];
                                 qb = q0 + uint32_t(slot * 2 * kChunk * kRowB);
+                                bb = smem_u32(s_bias) + uint32_t(slot * 2 * kBiasChunkB);
                             }
                             const int ts = int(mw);
+                            P2PROF(long long c1 = clock64());
                             mbar_wait_pm(&t_empty[ts], ((job >> 1) & 1) ^ 1);
+                            P2PROF(wt += clock64() - c1);
                             tc_fence_after();
                             if (leader) {
-                                mma_128xN(tmem + uint32_t(ts * 256), kst, k_half, qb, q_half,
-                                          idesc_bf16_f32(128, uint32_t(nch * kChunk)));
+                                mma_128xN_bias(tmem + uint32_t(ts * 256), kst, k_half, qb, q_half, smem_u32(s_aone), bb,
+                                               idesc_bf16_f32(128, uint32_t(jn)));
                                 mma_commit(&t_full[ts]);
                                 if (!resident) mma_commit(&q_empty[slot]);
                             }
@@ -513,6 +622,9 @@ __global__ void __maxnreg__(128)
                     }
                 }
             }
+            P2PROF(if (MODE == MODE_SCORE && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
+                       printf("P2PROF cta %d mma%d tiles %d total %lld wait_k %lld wait_tempty %lld\n", blockIdx.x, mw,
+                              ntile, clock64() - m_beg, wk, wt));
         }
     } else {  // ------------------------- epilogue warps -------------------------
         const int e = warp - 1 - mma_warps<MODE>();
@@ -525,7 +637,7 @@ __global__ void __maxnreg__(128)
         uint32_t tcount = 0;  // SCORE: tiles done (emitting half, partial buffer)
         int lkey = -1;
         const float inv_p = 1.0f / float(P.p);
-        const int64_t T1 = MODE == MODE_SCORE ? int64_t(P.p1_pre[P.p1_runs]) : 0;
+        P2PROF(long long ewf = 0, ebar = 0, ehead = 0; int etiles = 0; const long long e_beg = clock64());
         P1PROF(long long pw = 0, pl = 0, pc = 0, pj = 0, po = 0, pfirst = 0; const long long p_beg = clock64(); long long c_prev = p_beg;
                uint64_t g_beg; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_beg)));
         for (int g = it_beg; g < it_end;) {
@@ -584,73 +696,62 @@ __global__ void __maxnreg__(128)
                 for (int cc = 0; cc < kMaxQRes; ++cc) {
                     if (cc < x.nq) {
                         const int rq = (x.c0 + cc) * kChunk + r_local;
-                        const int64_t o = (int64_t(x.hk + P.hk_base) * (P.NQ * kChunk) + rq) * P.slots + x.slot + half;
+                        const int64_t o = int64_t(x.slot + half) * P.prow + int64_t(x.hk + P.hk_base) * (P.NQ * kChunk) + rq;
                         P.part_m[o] = m[cc];
                         P.part_z[o] = z[cc];
                     }
                 }
             } else {
-                if (x.hk != lkey) {  // the head's lse2 from the P1 partials (all 8 warps)
+                P2PROF(long long ch = clock64());
+                if (P.keys && x.l != lkey) {  // a new layer: flush the previous layer's coarse histogram
                     named_bar_sync(1, 32 * kEpiWarps);
-                    if (P.keys && lkey >= 0 && lkey / P.H != x.l) flush_coarse(P, lkey / P.H, s_coarse, etid);
-                    if (etid < P.cgroups) {  // slot list of each P1 run (head, chunk group)
-                        const int run = (x.hk + P.run_hk_base) * P.cgroups + etid;  // in the P1 launch's run order
-                        const int R0 = P.p1_pre[run], R1 = P.p1_pre[run + 1];
-                        int n = 0;
-                        if (R1 > R0) {
-                            const int b0 = part_cnt(T1, P.p1_grid, R0) - 1, b1 = part_cnt(T1, P.p1_grid, R1 - 1) - 1;
-                            for (int b = b0; b <= b1 && n >= 0; ++b) {
-                                const int lo = max(R0, part_bound(T1, P.p1_grid, b));
-                                const int hi = min(R1, part_bound(T1, P.p1_grid, b + 1));
-                                if (lo >= hi) continue;
-                                if (n == kMaxSlots) n = -1;  // too many: rows take the general path
-                                else s_slot[etid * kMaxSlots + n++] = kStatGroups * (b - b0);
-                            }
-                        }
-                        s_nslot[etid] = n;
-                    }
+                    if (lkey >= 0) flush_coarse(P, lkey, s_coarse, etid);
                     named_bar_sync(1, 32 * kEpiWarps);
-                    for (int r = etid; r < P.NQ * kChunk; r += 32 * kEpiWarps) {
-                        float v = INFINITY;
-                        if (r < P.Gp) {
-                            const int cg = (r / kChunk) / P.cg_chunks;
-                            const int n = s_nslot[cg];
-                            const int64_t row = int64_t(x.hk + P.hk_base) * (P.NQ * kChunk) + r;
-                            v = n >= 0 ? merge_slots(P.part_m + row * P.slots, P.part_z + row * P.slots,
-                                                     s_slot + cg * kMaxSlots, n)
-                                       : merge_lse2(P, x.hk, r, T1);
-                        }
-                        if (v != v) atomicCAS(P.err_flag, 0, EPK_ERR_NAN);  // a NaN logit poisoned the row's sum
-                        s_lse[r] = -v;  // negated: the epilogue adds it with FFMA2
-                    }
-                    named_bar_sync(1, 32 * kEpiWarps);
-                    lkey = x.hk;
+                    lkey = x.l;
                 }
+                P2PROF(ehead += clock64() - ch);
                 for (int t = 0; t < x.ntiles(); ++t) {
+                    P2PROF(++etiles);
                     float best = -INFINITY;
-                    for (int j = 0; 2 * j < x.nq; ++j) {
-                        const int ncols = min(2, x.nq - 2 * j) * kChunk;  // query rows of the job
-                        const int hw = ncols / 2;                         // columns per warp half
+                    for (int j = 0; j < P.sj; ++j) {
+                        const int hw = (j + 1 < P.sj ? P.sj_n0 : P.sj_nl) / 2;  // columns per warp half: 32..128
                         const int ts = int(job & 1);
+                        P2PROF(long long c0 = clock64());
                         mbar_wait(&t_full[ts], (job >> 1) & 1);
+                        P2PROF(ewf += clock64() - c0);
                         tc_fence_after();
-                        const int r0 = 2 * j * kChunk + half * hw;  // first query row of this warp's columns
-                        if (hw == 128) {
+                        const int r0 = j * P.sj_n0 + half * hw;  // first query row of this warp's columns
+                        const uint32_t ta = tmem + lane_addr + uint32_t(ts * 256 + half * hw);
+                        if (hw >= 64) {
                             float v[64];
-                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + half * hw), v);
-                            score_cols<64>(v, s_lse + r0, r0, P, best, s_avg, r_local);
-                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + half * hw + 64), v);
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(&t_empty[ts]);  // slot free: values are in registers
-                            score_cols<64>(v, s_lse + r0 + 64, r0 + 64, P, best, s_avg, r_local);
+                            tmem_ld64(ta, v);
+                            if (hw == 64) {
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive(&t_empty[ts]);  // slot free: values are in registers
+                            }
+                            score_cols<64>(v, r0, P, best, s_avg, r_local);
+                            if (hw == 128) {
+                                tmem_ld64(ta + 64, v);
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive(&t_empty[ts]);
+                                score_cols<64>(v, r0 + 64, P, best, s_avg, r_local);
+                            } else if (hw == 96) {
+                                float w[32];
+                                tmem_ld32(ta + 64, w);
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive(&t_empty[ts]);
+                                score_cols<32>(w, r0 + 64, P, best, s_avg, r_local);
+                            }
                         } else {
-                            float v[64];
-                            tmem_ld64(tmem + lane_addr + uint32_t(ts * 256 + half * hw), v);
+                            float w[32];
+                            tmem_ld32(ta, w);
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&t_empty[ts]);
-                            score_cols<64>(v, s_lse + r0, r0, P, best, s_avg, r_local);
+                            score_cols<32>(w, r0, P, best, s_avg, r_local);
                         }
                         ++job;
                     }
@@ -664,9 +765,11 @@ __global__ void __maxnreg__(128)
                         const int em = int(tcount & 1);
                         float* sp = s_pair + em * kChunk;
                         if (half != em) sp[r_local] = best;
+                        P2PROF(long long cb = clock64());
                         named_bar_sync(2 + quarter, 64);
+                        P2PROF(ebar += clock64() - cb);
                         if (half == em && jrow < x.n_h)
-                            emit_score(P, x.l, x.krow0 + jrow, ex2(fmaxf(best, sp[r_local])), s_coarse);
+                            emit_score(P, x.l, x.krow0 + jrow, ex2(fmaxf(best, sp[r_local]) * P.c2), s_coarse);
                         ++tcount;
                     } else {
                         named_bar_sync(2 + quarter, 64);
@@ -685,8 +788,11 @@ __global__ void __maxnreg__(128)
         }
         if (MODE == MODE_SCORE && P.keys && lkey >= 0) {  // last layer's coarse histogram
             named_bar_sync(1, 32 * kEpiWarps);
-            flush_coarse(P, lkey / P.H, s_coarse, etid);
+            flush_coarse(P, lkey, s_coarse, etid);
         }
+        P2PROF(if (MODE == MODE_SCORE && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
+                   printf("P2PROF cta %d epi%d tiles %d total %lld wait_tfull %lld bar %lld head %lld\n", blockIdx.x, e,
+                          etiles, clock64() - e_beg, ewf, ebar, ehead));
         P1PROF(uint64_t g_end; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end)); const long long p_end = clock64();
                if (MODE == MODE_STATS && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
                    printf("P1PROF cta %d warp %2d jobs %lld total %lld wait %lld ld %lld compute %lld between %lld first %lld\n",
@@ -707,7 +813,7 @@ __global__ void __maxnreg__(128)
 // ---------------------------------------------------------------------------
 static int smem_bytes(const TcParams& P, int mode) {
     return 1024 + 2 * P.qcap * kRowB + P.kstages * 2 * P.krows * kRowB +
-           (mode == MODE_SCORE ? (P.NQ + 2 + (P.agg_max ? 0 : P.G)) * kChunk * 4 : 0) +
+           (mode == MODE_SCORE ? (2 + (P.agg_max ? 0 : P.G)) * kChunk * 4 + P.qcap * kBiasRowB + kBiasChunkB : 0) +
            (2 * P.kstages + 2 * kMaxQRes + 8) * 8 + 16 + (P.runs + 1) * 4;
 }
 
@@ -839,12 +945,15 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.slots = kStatGroups * grid;
     const int64_t rows = int64_t(P.L) * H * P.NQ * kChunk;
     const int64_t pre_n = int64_t(P.L) * (int64_t(H) * P.cgroups + 1) + 1;
-    rc = ws_require(ctx, 2 * rows * P.slots * 4 + pre_n * 4 + 4096);
+    rc = ws_require(ctx, 2 * rows * P.slots * 4 + pre_n * 4 + rows * kBiasRowB + 4096);
     if (rc) return rc;
     WsCarver carve(ctx->ws);
+    P.prow = rows;
     P.part_m = carve.take<float>(rows * P.slots);
     P.part_z = carve.take<float>(rows * P.slots);
     P.p1_pre = carve.take<int32_t>(pre_n);
+    P.bias_out = carve.take<uint8_t>(rows * kBiasRowB);
+    P.bias = P.bias_out;
     out->p1_pre_all = P.p1_pre;
     out->grid = grid;
     T.P1 = P;
@@ -861,10 +970,23 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.runs = P.L * H;
     P.resident = P.NQ <= kMaxQRes;
     P.qcap = P.resident ? P.NQ * kChunk : 4 * kChunk;
+    if (P.resident) {  // query rows (64-row units) split evenly over <= 256-row MMA jobs: 384 -> 2 x 192
+        const int R = (P.Gp + 63) / 64 * 64;
+        P.sj = (R + 255) / 256;
+        P.sj_n0 = (R / 64 + P.sj - 1) / P.sj * 64;
+        P.sj_nl = R - (P.sj - 1) * P.sj_n0;
+    } else {  // streamed chunk pairs
+        P.sj = (P.NQ + 1) / 2;
+        P.sj_n0 = 256;
+        P.sj_nl = (P.NQ & 1) ? 128 : 256;
+    }
     P.kstages = 1;
-    while (P.kstages < 4) {
+    // P2 keeps three K stages next to the resident queries and their bias
+    // rows (a little over the P1 co-residency budget)
+    const int budget2 = std::min(limit, std::max(budget, 216 * 1024));
+    while (P.kstages < 3) {
         ++P.kstages;
-        if (smem_bytes(P, MODE_SCORE) > budget) {
+        if (smem_bytes(P, MODE_SCORE) > budget2) {
             --P.kstages;
             break;
         }
@@ -945,6 +1067,10 @@ static int tc_launch_p2(epk_ctx* ctx, const TcPlan& T, int l0, int l1, int p0, i
     CUtensorMap tm_q, tm_kp;
     int rc = tc_view(T, MODE_SCORE, l0, l1, p0, p1, &P, &tm_q, &tm_kp);
     if (rc) return rc;
+    EPK_PROF(ctx, "p2_bias");
+    EPK_CUDA_CHECK(launch_pdl(tc_bias_kernel, dim3(unsigned(P.L * P.H)), dim3(unsigned(std::min(P.NQ * kChunk, 1024))), 0, ctx->stream,
+                              P));
+    EPK_LAUNCH_CHECK(ctx);
     EPK_PROF(ctx, "p2_colscore");
     EPK_CUDA_CHECK(launch_pdl(T.score_fn, dim3(T.grid), dim3(kThreads), T.smem2, ctx->stream, P, T.tm_k, tm_q,
                               T.tm_kp));

@@ -36,6 +36,32 @@ __device__ __forceinline__ void mma_128xN(uint32_t d_tmem, uint32_t a, uint32_t 
     }
 }
 
+// ---- the lse bias K-step (P2) ---------------------------------------------------
+// P2 needs x - lse2/c2 for every (cache row, query row).  The query-side term
+// -lse2_r/c2 = h + m + l (three bf16 parts, exact to ~2^-24 relative) rides
+// in an extra 16-wide MMA K-step: A' = [1 1 1 0 ...] for every cache row, B' =
+// [h m l 0 ...] for every query row, so D = bias + q.k accumulates in fp32 and
+// the epilogue is a bare max.  Both operands use the no-swizzle K-major layout:
+// row r of a 128-row chunk at (r/8)*256 + (r%8)*16, K elements 8..15 at +128.
+constexpr int kBiasRowB = 32;                    // bytes per row (16 bf16)
+constexpr int kBiasChunkB = kChunk * kBiasRowB;  // 4 KB per 128 rows
+constexpr uint32_t kBiasLbo = 128, kBiasSbo = 256;
+__host__ __device__ constexpr int bias_off(int r) { return (r >> 3) * 256 + (r & 7) * 16; }
+
+// D = A' B'^T (bias) + A B^T over K = 128: the bias K-step first, then the 8
+// K-steps of mma_128xN accumulating onto it.
+__device__ __forceinline__ void mma_128xN_bias(uint32_t d_tmem, uint32_t a, uint32_t a_half, uint32_t b,
+                                               uint32_t b_half, uint32_t a_bias, uint32_t b_bias, uint32_t idesc) {
+    mma_bf16_ss(d_tmem, sdesc_k_none(a_bias, kBiasLbo, kBiasSbo), sdesc_k_none(b_bias, kBiasLbo, kBiasSbo), idesc, 0u);
+    const uint64_t da = sdesc_k_sw128(a), db = sdesc_k_sw128(b);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t k = uint32_t((kk & 3) * 32);
+        const uint32_t h = uint32_t(kk >> 2);
+        mma_bf16_ss(d_tmem, da + ((h * a_half + k) >> 4), db + ((h * b_half + k) >> 4), idesc, 1u);
+    }
+}
+
 // Loads `rows` rows (both d-halves) of a [*, 128] bf16 tensor into a
 // [d-half][rows] region whose halves are `half_bytes` apart.
 __device__ __forceinline__ void load_rows(uint8_t* dst, uint32_t half_bytes, const CUtensorMap* map, uint64_t* bar,
@@ -44,26 +70,20 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, uint32_t half_bytes, con
     tma_load_2d(dst + half_bytes, map, bar, 64, row);
 }
 
-// SCORE epilogue on W columns of one cache row (query rows r0 .. r0+W),
-// nlse = -lse2 of those rows: Max: best = max(best, x c2 - lse2) as FFMA2 +
-// three-input max (1.25 issue slots per column); Avg: per-window sums of
-// 2^(x c2 - lse2) accumulated per query head in shared memory.
+// SCORE epilogue on W columns of one cache row (query rows r0 .. r0+W); the
+// values are x - lse2/c2 (bias K-step): Max: best = max(best, x) as three-input
+// max chains (0.5 issue slots per column); Avg: per-window sums of 2^(x c2)
+// accumulated per query head in shared memory.
 template <int W, typename PT>
-__device__ __forceinline__ void score_cols(const float (&v)[W], const float* nlse, int r0, const PT& P,
-                                           float& best, float* s_avg, int r_local) {
+__device__ __forceinline__ void score_cols(const float (&v)[W], int r0, const PT& P, float& best, float* s_avg,
+                                           int r_local) {
     if (P.agg_max) {
-        const uint64_t c2x2 = f2_pack(P.c2, P.c2);
         // four independent three-input-max chains (short dependency chains)
         float b[4] = {best, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int i = 0; i < W; i += 4) {
-            const float4 l4 = *reinterpret_cast<const float4*>(nlse + i);
-            float a0, a1, a2, a3;
-            f2_unpack(ffma2(f2_pack(v[i], v[i + 1]), c2x2, f2_pack(l4.x, l4.y)), a0, a1);
-            f2_unpack(ffma2(f2_pack(v[i + 2], v[i + 3]), c2x2, f2_pack(l4.z, l4.w)), a2, a3);
-            const int j = (i / 4) & 1;
-            b[2 * j] = fmaxf(fmaxf(b[2 * j], a0), a1);
-            b[2 * j + 1] = fmaxf(fmaxf(b[2 * j + 1], a2), a3);
+        for (int i = 0; i < W; i += 8) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = fmaxf(fmaxf(b[j], v[i + 2 * j]), v[i + 2 * j + 1]);
         }
         best = fmaxf(fmaxf(b[0], b[1]), fmaxf(b[2], b[3]));
     } else {
@@ -79,7 +99,7 @@ __device__ __forceinline__ void score_cols(const float (&v)[W], const float* nls
                     acc = 0.f;
                     gcur = gg;
                 }
-                acc += ex2(fmaf(v[i], P.c2, nlse[i]));
+                acc += ex2(v[i] * P.c2);
             }
         }
         if (gcur < P.G) atomicAdd(&s_avg[gcur * kChunk + r_local], acc);
