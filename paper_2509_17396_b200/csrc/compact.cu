@@ -7,24 +7,30 @@
 // block's append_to_cache (toymodel.hpp:428-443) lands in place without
 // moving the cache again.
 //
-// Three launches per call, all free of shared memory so their small CTAs can
-// co-reside on an SM with a scorer CTA of the next layer group (the step
-// overlaps HBM-bound compaction with tensor/SFU-bound scoring):
+// Launches, all free of shared memory (their small CTAs may share an SM with
+// a scorer CTA of a next layer group):
 //   count   one warp per 128-row chunk: kept rows in the chunk;
 //   plan    one CTA per layer: exclusive scan of the chunk counts and the kept
 //           count in front of every head region -> output head_off/head_len;
 //   gather  one warp per 128-row chunk: ballot prefix per 32 rows, then
 //           16-byte vector copies of K and V (8 in flight per lane) and the
 //           positions.
-// keep[] must be 0 on gap rows (both select modes guarantee it).
+// Given a keep[] mask (generic select) all three run; keep[] must be 0 on gap
+// rows.  In threshold mode (the tensor-core step) select_threshold_kernel has
+// already written the plan and the gather evaluates the keep rule itself from
+// the scorer's keys, so the gather is the only launch here.
 #include <algorithm>
 
 #include "epk_internal.cuh"
 
 namespace epk {
 
-constexpr int kChunkRows = 128;   // rows per warp chunk
 constexpr int kWarpsPerCta = 4;
+#ifndef EPK_GATHER_U
+#define EPK_GATHER_U 8  // measured cfg2: 4 -> 8 takes the gather from 0.307 to 0.298 ms (16 spills)
+#endif
+constexpr int kGatherU = EPK_GATHER_U;  // kept rows per half-warp in flight (K and V: 2 x 16 B per lane each)
+static_assert(32 % (2 * kGatherU) == 0, "gather unroll");
 
 struct CompactParams {
     LayerTable in_lt;
@@ -49,13 +55,11 @@ struct CompactParams {
     int32_t* chunk_prefix;  // [layers][max_chunks]
     int32_t* layer_bad;     // [layers] plan: kept rows + slack exceed the output layer (gather skips it)
     int* err_flag;
-    // threshold mode (the tensor-core step): keep[] is derived here from the
-    // scorer's keys and the per-layer threshold (select_threshold_kernel)
+    // threshold mode (the tensor-core step): the gather derives keep from
+    // the scorer's keys and the per-layer threshold, and select_threshold_kernel
+    // (select.cu) wrote the plan (chunk prefixes, output heads, layer_bad)
     const uint32_t* keys;  // [rows] global, or null (keep[] given)
     const uint64_t* thr;   // [layers][2]
-    uint8_t* keep_out;
-    uint32_t* hist_fine;    // threshold mode: [layers][65536], zeroed here for the next step
-    uint32_t* hist_coarse;  // [layers][256]
 };
 
 __device__ __forceinline__ int head_of_row(const int32_t* off, int H, int64_t r) {
@@ -70,49 +74,13 @@ __device__ __forceinline__ int head_of_row(const int32_t* off, int H, int64_t r)
 __global__ void __launch_bounds__(32 * kWarpsPerCta) compact_count_kernel(const __grid_constant__ CompactParams P) {
     pdl_wait();
     const int layer = blockIdx.y;
-    if (P.hist_fine) {  // threshold mode: this CTA's share of the layer's histogram reset
-        const int per = (65536 / 4 + gridDim.x - 1) / gridDim.x;
-        uint4* hf4 = reinterpret_cast<uint4*>(P.hist_fine + int64_t(layer) * 65536);
-        for (int i = blockIdx.x * per + threadIdx.x; i < min(65536 / 4, (blockIdx.x + 1) * per); i += blockDim.x)
-            hf4[i] = make_uint4(0, 0, 0, 0);
-        if (blockIdx.x == 0)
-            for (int i = threadIdx.x; i < 256; i += blockDim.x) P.hist_coarse[layer * 256 + i] = 0;
-    }
     const int chunk = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (chunk >= P.max_chunks) return;
     const int64_t rows = P.in_off[layer * (P.H + 1) + P.H];
     const int64_t r0 = int64_t(chunk) * kChunkRows;
     int c = 0;
-    if (r0 < rows && P.keys) {
-        // keep = live && (key < T || (key == T && (position << 8 | head) <= U))
-        const int64_t base = P.in_lt.base[layer];
-        const int32_t* off = P.in_off + layer * (P.H + 1);
-        const uint64_t t0 = P.thr[2 * layer], U = P.thr[2 * layer + 1];
-        const bool all = ((t0 >> 32) & 1) != 0;
-        const bool none = ((t0 >> 33) & 1) != 0;  // layer budget 0
-        const uint32_t T = uint32_t(t0);
-        uint8_t* kp = P.keep_out + base;
-        // the chunk's first head (warp-uniform) and where the next starts: the
-        // per-row binary search only past a head boundary
-        const int h0 = head_of_row(off, P.H, r0);
-        const int64_t h0_end = off[h0 + 1];
-#pragma unroll
-        for (int i = 0; i < kChunkRows / 32; ++i) {
-            const int64_t r = r0 + i * 32 + lane;
-            uint8_t k = 0;
-            if (r < rows) {
-                const int h = r < h0_end ? h0 : head_of_row(off, P.H, r);
-                if (!none && r - off[h] < P.in_len[layer * P.H + h]) {
-                    const uint32_t key = __ldcg(P.keys + base + r);
-                    k = (all || key < T ||
-                         (key == T && ((uint64_t(uint32_t(P.in_pos[base + r])) << 8) | uint64_t(h)) <= U)) ? 1 : 0;
-                }
-                kp[r] = k;
-            }
-            c += k;
-        }
-    } else if (r0 < rows) {
+    if (r0 < rows) {
         const uint8_t* kp = P.keep + P.in_lt.base[layer];
 #pragma unroll
         for (int i = 0; i < kChunkRows / 32; ++i) {
@@ -214,41 +182,64 @@ __global__ void __launch_bounds__(512) compact_gather_kernel(const __grid_consta
         const int64_t in_base = P.in_lt.base[layer];
         const int64_t out_base = P.out_lt.base[layer];
         const uint8_t* kp = P.keep + in_base;
-        int32_t run = P.chunk_prefix[layer * P.max_chunks + chunk];
+        int32_t run = __ldcg(P.chunk_prefix + layer * P.max_chunks + chunk);
         const int rv = P.row_vec;
         const int hl = lane >> 4, cl = lane & 15;
+        // threshold mode: keep = live && (key < T || key == T && (position << 8 | head) <= U)
+        // (thr[2l] bit 32: keep every live row, bit 33: keep none)
+        const bool thr_mode = P.keys != nullptr;
+        uint64_t t0 = 0, U = 0;
+        if (thr_mode) {
+            t0 = __ldcg(P.thr + 2 * layer);
+            U = __ldcg(P.thr + 2 * layer + 1);
+        }
         // the chunk's first head and where the next one starts (a chunk rarely
         // crosses a head boundary: rows past it take the binary search)
-        const int h0 = P.slack ? head_of_row(off, P.H, r0) : 0;
-        const int64_t h0_end = P.slack ? int64_t(off[h0 + 1]) : 0;
+        const bool need_h = P.slack || thr_mode;
+        const int h0 = need_h ? head_of_row(off, P.H, r0) : 0;
+        const int64_t h0_end = need_h ? int64_t(off[h0 + 1]) : 0;
         for (int sc = 0; sc < kChunkRows / 32; ++sc) {
             const int64_t rs = r0 + sc * 32;
             if (rs >= rows) break;
             const int64_t r = rs + lane;
-            const bool k = r < rows && kp[r];
+            const int h = (need_h && r < rows) ? (r < h0_end ? h0 : head_of_row(off, P.H, r)) : 0;
+            int32_t ps = 0;
+            bool k;
+            if (thr_mode) {
+                k = false;
+                if (r < rows && !((t0 >> 33) & 1) && r - off[h] < P.in_len[layer * P.H + h]) {
+                    ps = P.in_pos[in_base + r];
+                    const uint32_t key = __ldcg(P.keys + in_base + r);
+                    k = ((t0 >> 32) & 1) || key < uint32_t(t0) ||
+                        (key == uint32_t(t0) && ((uint64_t(uint32_t(ps)) << 8) | uint64_t(h)) <= U);
+                }
+            } else {
+                k = r < rows && kp[r];
+                if (k) ps = P.in_pos[in_base + r];
+            }
             const unsigned bal = __ballot_sync(0xffffffffu, k);
             if (bal == 0) continue;
             int64_t dst = 0;
             if (k) {
                 dst = out_base + run + __popc(bal & ((1u << lane) - 1u));
-                if (P.slack) dst += int64_t(P.slack) * (r < h0_end ? h0 : head_of_row(off, P.H, r));
-                P.out_pos[dst] = P.in_pos[in_base + r];
+                if (P.slack) dst += int64_t(P.slack) * h;
+                P.out_pos[dst] = ps;
             }
             run += __popc(bal);
-            // copy the kept rows: a half-warp per row, 4 rows per half-warp in flight
-            for (int k0 = 0; k0 < 32; k0 += 8) {
-                uint4 kv[4], vv[4];
-                int64_t dsts[4];
-                bool ok[4];
+            // copy the kept rows: a half-warp per row, kGatherU rows per half-warp in flight
+            for (int k0 = 0; k0 < 32; k0 += 2 * kGatherU) {
+                uint4 kv[kGatherU], vv[kGatherU];
+                int64_t dsts[kGatherU];
+                bool ok[kGatherU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kGatherU; ++u) {
                     const int idx = k0 + 2 * u + hl;
                     ok[u] = (bal >> idx) & 1u;
                     dsts[u] = __shfl_sync(0xffffffffu, dst, idx);
                 }
                 for (int c = cl; c < rv; c += 16) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kGatherU; ++u) {
                         if (ok[u]) {
                             const int64_t src = (in_base + rs + k0 + 2 * u + hl) * rv + c;
                             kv[u] = __ldg(P.in_k + src);
@@ -256,7 +247,7 @@ __global__ void __launch_bounds__(512) compact_gather_kernel(const __grid_consta
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kGatherU; ++u) {
                         if (ok[u]) {
                             P.out_k[dsts[u] * rv + c] = kv[u];
                             P.out_v[dsts[u] * rv + c] = vv[u];
@@ -266,6 +257,21 @@ __global__ void __launch_bounds__(512) compact_gather_kernel(const __grid_consta
             }
         }
     }
+}
+
+int compact_ws(epk_ctx* ctx, const epk_cache_desc* in, CompactWs* w) {
+    int64_t max_rows = 0;
+    for (int l = 0; l < in->layers; ++l)
+        max_rows = std::max<int64_t>(max_rows, in->layer_base[l + 1] - in->layer_base[l]);
+    w->max_chunks = int(std::max<int64_t>(1, (max_rows + kChunkRows - 1) / kChunkRows));
+    const int64_t ws = 2 * int64_t(in->layers) * w->max_chunks * 4 + int64_t(in->layers) * 4 + 1024;
+    int rc = ws2_require(ctx, ws);
+    if (rc) return rc;
+    WsCarver carve(ctx->ws2);
+    w->chunk_cnt = carve.take<int32_t>(int64_t(in->layers) * w->max_chunks);
+    w->chunk_prefix = carve.take<int32_t>(int64_t(in->layers) * w->max_chunks);
+    w->layer_bad = carve.take<int32_t>(in->layers);
+    return EPK_OK;
 }
 
 int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc* out, const uint8_t* keep,
@@ -282,10 +288,10 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     if (rc) return rc;
     rc = make_layer_table(out, &P.out_lt);
     if (rc) return rc;
-    int64_t max_rows = 0;
-    for (int l = 0; l < in->layers; ++l) max_rows = std::max<int64_t>(max_rows, P.in_lt.base[l + 1] - P.in_lt.base[l]);
+    CompactWs w;
+    if ((rc = compact_ws(ctx, in, &w))) return rc;
     P.H = in->kv_heads;
-    P.max_chunks = int(std::max<int64_t>(1, (max_rows + kChunkRows - 1) / kChunkRows));
+    P.max_chunks = w.max_chunks;
     P.layers = in->layers;
     P.slack = slack;
     P.row_vec = int(row_bytes / 16);
@@ -303,16 +309,11 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     P.err_flag = ctx->err_flag;
     P.keys = keys;
     P.thr = thr;
-    P.keep_out = const_cast<uint8_t*>(keep);
-    P.hist_fine = hist_fine;
-    P.hist_coarse = hist_coarse;
-    const int64_t ws = 2 * int64_t(in->layers) * P.max_chunks * 4 + int64_t(in->layers) * 4 + 1024;
-    rc = ws2_require(ctx, ws);
-    if (rc) return rc;
-    WsCarver carve(ctx->ws2);
-    P.chunk_cnt = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
-    P.chunk_prefix = carve.take<int32_t>(int64_t(in->layers) * P.max_chunks);
-    P.layer_bad = carve.take<int32_t>(in->layers);
+    (void)hist_fine;  // zeroed for the next step by the P1 launch (score_tc.cu)
+    (void)hist_coarse;
+    P.chunk_cnt = w.chunk_cnt;
+    P.chunk_prefix = w.chunk_prefix;
+    P.layer_bad = w.layer_bad;
     dim3 grid((P.max_chunks + kWarpsPerCta - 1) / kWarpsPerCta, in->layers);
 #ifdef EPK_COMPACT_CARVEOUT
     // experiment: a shared-memory carveout matching the scorer's, so the
@@ -324,12 +325,14 @@ int launch_compact(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     EPK_CUDA_CHECK(cudaFuncSetAttribute(compact_gather_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                         EPK_COMPACT_CARVEOUT));
 #endif
-    EPK_PROF(ctx, "compact_count");
-    EPK_CUDA_CHECK(launch_pdl(compact_count_kernel, grid, dim3(32 * kWarpsPerCta), 0, ctx->stream, P));
-    EPK_LAUNCH_CHECK(ctx);
-    EPK_PROF(ctx, "compact_plan");
-    EPK_CUDA_CHECK(launch_pdl(compact_plan_kernel, dim3(in->layers), dim3(256), 0, ctx->stream, P));
-    EPK_LAUNCH_CHECK(ctx);
+    if (!keys) {  // threshold mode: select_threshold_kernel planned the compaction already
+        EPK_PROF(ctx, "compact_count");
+        EPK_CUDA_CHECK(launch_pdl(compact_count_kernel, grid, dim3(32 * kWarpsPerCta), 0, ctx->stream, P));
+        EPK_LAUNCH_CHECK(ctx);
+        EPK_PROF(ctx, "compact_plan");
+        EPK_CUDA_CHECK(launch_pdl(compact_plan_kernel, dim3(in->layers), dim3(256), 0, ctx->stream, P));
+        EPK_LAUNCH_CHECK(ctx);
+    }
     EPK_PROF(ctx, "compact_gather");
     if (ctx->gather_ctas > 0) {  // persistent (experiments: an SM-partitioned overlapped gather)
         if (ctx->gather_smem > 0)

@@ -128,12 +128,13 @@ int launch_select(epk_ctx*, const epk_cache_desc*, const void*, int, const int64
                   int32_t*, int);
 int launch_compact(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*, int, const uint32_t*,
                    const uint64_t*, uint32_t*, uint32_t*);
-int launch_select_threshold(epk_ctx*, const epk_cache_desc*, const FusedSelect*, const int64_t*, uint64_t*, int32_t*);
+int launch_select_threshold(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, int, const FusedSelect*,
+                            const int64_t*, uint64_t*, int32_t*);
 int launch_step_tc_grouped(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const void*, const void*, int, int,
                            int, const int64_t*, int, cudaStream_t, cudaEvent_t, int, float*, uint8_t*,
                            const FusedSelect&, uint64_t*, int32_t*,
-                           int (*)(epk_ctx*, const epk_cache_desc*, const FusedSelect*, const int64_t*, uint64_t*,
-                                   int32_t*),
+                           int (*)(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, int, const FusedSelect*,
+                                   const int64_t*, uint64_t*, int32_t*),
                            int (*)(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*, int,
                                    const uint32_t*, const uint64_t*, uint32_t*, uint32_t*),
                            epk_cache_desc (*)(const epk_cache_desc*, int, int));
@@ -475,8 +476,8 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
     const bool fused = mode == EPK_SCORE_TC_BF16 && n_pins == 0 && in->kv_heads <= 64 && !pooled;
     // Step buffers live in their own allocation so the kernels' workspace
     // growth never aliases them.  Layout: histograms at fixed offsets for
-    // kMaxLayers layers (zeroed once here, re-zeroed by every threshold
-    // select), thresholds, then the row-indexed scores / keep mask / keys.
+    // kMaxLayers layers (zeroed once here, re-zeroed by every step's P1
+    // launch), thresholds, then the row-indexed scores / keep mask / keys.
     const int64_t o_hc = int64_t(kMaxLayers) * 65536 * 4;
     const int64_t o_thr = o_hc + int64_t(kMaxLayers) * 256 * 4;
     const int64_t o_cand = o_thr + int64_t(kMaxLayers) * 16;             // [kMaxLayers][1024] uint4
@@ -600,7 +601,8 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
             ctx->stream = ctx->side;
         }
         if (fused) {
-            rc = launch_select_threshold(ctx, &vin, &fs, budgets + l0, thr + 2 * l0, kept ? kept + l0 : nullptr);
+            rc = launch_select_threshold(ctx, &vin, &vout, out_slack, &fs, budgets + l0, thr + 2 * l0,
+                                         kept ? kept + l0 : nullptr);
             if (rc == EPK_OK)
                 rc = launch_compact(ctx, &vin, &vout, keep, out_slack, keys, thr + 2 * l0, fs.hist_fine, fs.hist_coarse);
         } else {

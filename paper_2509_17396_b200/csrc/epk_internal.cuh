@@ -138,6 +138,20 @@ struct LayerTable {
 
 int make_layer_table(const epk_cache_desc* c, LayerTable* t);
 
+// Compaction plan buffers (compact.cu), per launch in the context's second
+// workspace: per (layer, 128-row chunk) kept counts and their exclusive
+// prefix, and a per-layer "does not fit the output" flag.  The threshold
+// select (select.cu) fills them itself for the tensor-core step; the generic
+// path's count/plan kernels fill them otherwise.
+constexpr int kChunkRows = 128;
+struct CompactWs {
+    int32_t* chunk_cnt;     // [layers][max_chunks]
+    int32_t* chunk_prefix;  // [layers][max_chunks]
+    int32_t* layer_bad;     // [layers]
+    int max_chunks;
+};
+int compact_ws(epk_ctx* ctx, const epk_cache_desc* in, CompactWs* w);
+
 // Threshold-select buffers the tensor-core scorer fills in its SCORE pass
 // (select.cu select_threshold_kernel consumes them).  Pointers are for the
 // launch's first layer.

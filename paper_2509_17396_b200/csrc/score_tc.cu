@@ -72,8 +72,12 @@ constexpr int kStatGroups = kEpiWarpsStats / 4;
 // phases apart (with slot = job % 4 and three groups a group could reach its
 // next job on a slot while another group's job there was still in flight; with
 // three slots and jobs alternating MMA warps an MMA warp could skip a phase).
+#ifdef EPK_STATS_SLOTS
+constexpr int kStatSlots = EPK_STATS_SLOTS;
+#else
 constexpr int kStatSlots = kStatGroups == 2 ? 4 : kStatGroups;
-static_assert(kStatSlots % kStatGroups == 0 && kStatSlots * 128 <= 512, "STATS TMEM slots");
+#endif
+static_assert(kStatSlots * 128 <= 512, "STATS TMEM slots");
 constexpr int kMmaWarps = 2;  // SCORE: MMA issuers alternate jobs: one issues while the other synchronises
 #ifndef EPK_STATS_MMA_WARPS
 #define EPK_STATS_MMA_WARPS 3
@@ -82,6 +86,10 @@ constexpr int kMmaWarps = 2;  // SCORE: MMA issuers alternate jobs: one issues w
 // holds back the MMA of another slot (no head-of-line blocking; 16 warps x 128
 // registers = the whole register file; P1 0.285 -> 0.277 ms at cfg2)
 constexpr int kMmaWarpsStats = EPK_STATS_MMA_WARPS;
+// more slots than groups (a group's jobs rotate over the slots): one MMA warp
+// issues every job in order, so a slot's phases complete in job order and a
+// group can never wait on a phase two ahead of the slot's barrier
+static_assert(kStatSlots % kStatGroups == 0 || kMmaWarpsStats == 1, "STATS slots/groups/MMA warps");
 template <int MODE>
 constexpr int mma_warps() { return MODE == 0 ? kMmaWarpsStats : kMmaWarps; }
 constexpr int kThreads = 32 * (1 + kMmaWarps + kEpiWarps);
@@ -376,6 +384,11 @@ __global__ void tc_bias_kernel(const __grid_constant__ TcParams P) {
 #else
 #define P2PROF(...)
 #endif
+#if defined(EPK_P1_PROF) || defined(EPK_P2_PROF)
+#define MPROF(...) __VA_ARGS__
+#else
+#define MPROF(...)
+#endif
 #ifdef EPK_NO_BACKOFF
 #define mbar_wait_pm mbar_wait
 #else
@@ -437,6 +450,18 @@ __global__ void __maxnreg__(128)
             fence_barrier_init();
         }
     }
+    if (MODE == MODE_STATS && P.hist_fine) {
+        // the fused selection's score histograms start every step at zero:
+        // P1 clears them (its CTAs are SFU-bound, the stores are free) for the
+        // P2 launch that fills them; the previous step's select read them
+        // before this launch's pdl_wait returned
+        const int64_t n4 = int64_t(P.L) * (65536 / 4), per = (n4 + gridDim.x - 1) / gridDim.x;
+        uint4* hf4 = reinterpret_cast<uint4*>(P.hist_fine);
+        for (int64_t i = blockIdx.x * per + threadIdx.x; i < min(n4, (blockIdx.x + 1) * per); i += blockDim.x)
+            hf4[i] = make_uint4(0, 0, 0, 0);
+        if (blockIdx.x == 0)
+            for (int i = threadIdx.x; i < P.L * 256; i += blockDim.x) P.hist_coarse[i] = 0;
+    }
     if (warp == 1) tmem_alloc(tmem_holder, 512);
     if (MODE == MODE_SCORE && !P.agg_max)
         for (int i = threadIdx.x; i < P.G * kChunk; i += blockDim.x) s_avg[i] = 0.f;
@@ -472,6 +497,7 @@ __global__ void __maxnreg__(128)
             int key = -1;
             int64_t pj = 0;
             const int npairs = (P.NQ + 1) / 2;
+            MPROF(long long pw = 0; const long long p_beg = clock64());
             for (int g = it_beg; g < it_end;) {
                 const Seg x = seg_at<MODE>(P, s_pre, g, it_end, T);
                 g += x.ntiles();
@@ -493,7 +519,9 @@ __global__ void __maxnreg__(128)
                     }
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
+                    MPROF(long long c0 = clock64());
                     mbar_wait_pm(&k_empty[ks], kph ^ 1);
+                    MPROF(pw += clock64() - c0);
                     if (leader) {
                         mbar_expect_tx(&k_full[ks], k_stage);
                         if (t < x.nc)
@@ -529,6 +557,9 @@ __global__ void __maxnreg__(128)
                     }
                 }
             }
+            MPROF(if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
+                      printf("%sPROF cta %d producer total %lld wait_kempty %lld\n", MODE == MODE_SCORE ? "P2" : "P1",
+                             blockIdx.x, clock64() - p_beg, pw));
         }
     } else if (warp <= mma_warps<MODE>()) {
         // STATS: MMA warp mw issues the jobs of slot mw (job % 3); SCORE: the
@@ -544,7 +575,7 @@ __global__ void __maxnreg__(128)
             int key = -1;
             int held = 0;
             const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK);
-            P2PROF(long long wk = 0, wt = 0, m_beg = clock64(); int ntile = 0);
+            MPROF(long long wk = 0, wt = 0, m_beg = clock64(); int ntile = 0);
             for (int g = it_beg; g < it_end;) {
                 const Seg x = seg_at<MODE>(P, s_pre, g, it_end, T);
                 g += x.ntiles();
@@ -558,9 +589,9 @@ __global__ void __maxnreg__(128)
                     fresh = true;
                 }
                 for (int t = 0; t < x.ntiles(); ++t) {
-                    P2PROF(long long c0 = clock64());
+                    MPROF(long long c0 = clock64());
                     mbar_wait_pm(&k_full[ks], kph);
-                    P2PROF(wk += clock64() - c0; ++ntile);
+                    MPROF(wk += clock64() - c0; ++ntile);
                     const uint32_t kst = k0 + uint32_t(ks) * k_stage;
                     if (MODE == MODE_STATS) {
                         for (int c = 0; c < x.nq; ++c, ++job) {
@@ -570,11 +601,15 @@ __global__ void __maxnreg__(128)
                             }
                             const int ts = int(job % kStatSlots);  // 128-column slots, one group each
                             if (ts % mma_warps<MODE>() != int(mw)) continue;
+                            MPROF(long long c1 = clock64());
                             mbar_wait_pm(&t_empty[ts], ((job / kStatSlots) & 1) ^ 1);
+                            MPROF(wt += clock64() - c1);
                             tc_fence_after();
                             if (leader) {
+#if !defined(EPK_XP_NOMMA)  // experiment: P1 without its MMAs (wrong values)
                                 mma_128xN(tmem + uint32_t(ts * 128), q0 + uint32_t(c * kChunk * kRowB), q_half, kst,
                                           k_half, idesc_bf16_f32(128, 128));
+#endif
                                 mma_commit(&t_full[ts]);
                             }
                             __syncwarp();
@@ -622,9 +657,9 @@ __global__ void __maxnreg__(128)
                     }
                 }
             }
-            P2PROF(if (MODE == MODE_SCORE && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
-                       printf("P2PROF cta %d mma%d tiles %d total %lld wait_k %lld wait_tempty %lld\n", blockIdx.x, mw,
-                              ntile, clock64() - m_beg, wk, wt));
+            MPROF(if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
+                       printf("%sPROF cta %d mma%d tiles %d total %lld wait_k %lld wait_tempty %lld\n",
+                              MODE == MODE_SCORE ? "P2" : "P1", blockIdx.x, mw, ntile, clock64() - m_beg, wk, wt));
         }
     } else {  // ------------------------- epilogue warps -------------------------
         const int e = warp - 1 - mma_warps<MODE>();
@@ -797,7 +832,7 @@ __global__ void __maxnreg__(128)
                if (MODE == MODE_STATS && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
                    printf("P1PROF cta %d warp %2d jobs %lld total %lld wait %lld ld %lld compute %lld between %lld first %lld\n",
                           blockIdx.x, warp, pj, p_end - p_beg, pw, pl, pc, po, pfirst);
-               if (MODE == MODE_STATS && lane == 0 && warp == 3) {
+               if (MODE == MODE_STATS && lane == 0 && warp == 1 + kMmaWarpsStats) {
                    uint32_t smid; asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
                    printf("P1GT %d %llu %llu %u %lld %lld %lld %d %d\n", blockIdx.x, (unsigned long long)g_beg, (unsigned long long)g_end, smid, pj, pw, p_end - p_beg, it_beg, it_end);
                });
@@ -1098,8 +1133,8 @@ int launch_step_tc_grouped(epk_ctx* ctx, const epk_cache_desc* in, const epk_cac
                            const void* kp, int hq, int p, int agg_max, const int64_t* budgets, int group,
                            cudaStream_t side, cudaEvent_t ev_fork, int out_slack, float* scores, uint8_t* keep,
                            const FusedSelect& fs_all, uint64_t* thr, int32_t* kept,
-                           int (*select_fn)(epk_ctx*, const epk_cache_desc*, const FusedSelect*, const int64_t*,
-                                            uint64_t*, int32_t*),
+                           int (*select_fn)(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, int,
+                                            const FusedSelect*, const int64_t*, uint64_t*, int32_t*),
                            int (*compact_fn)(epk_ctx*, const epk_cache_desc*, const epk_cache_desc*, const uint8_t*,
                                              int, const uint32_t*, const uint64_t*, uint32_t*, uint32_t*),
                            epk_cache_desc (*view_fn)(const epk_cache_desc*, int, int)) {
@@ -1119,7 +1154,8 @@ int launch_step_tc_grouped(epk_ctx* ctx, const epk_cache_desc* in, const epk_cac
                              fs_all.cand + int64_t(l0) * 1024,
                              fs_all.cand_n + l0,
                              fs_all.done + l0};
-        if ((rc = select_fn(ctx, &vin, &fs, budgets + l0, thr + 2 * l0, kept ? kept + l0 : nullptr))) return rc;
+        if ((rc = select_fn(ctx, &vin, &vout, out_slack, &fs, budgets + l0, thr + 2 * l0, kept ? kept + l0 : nullptr)))
+            return rc;
         if (side) {
             EPK_CUDA_CHECK(cudaEventRecord(ev_fork, main));
             EPK_CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork, 0));

@@ -533,29 +533,37 @@ int launch_select(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int
 }
 
 // ---------------------------------------------------------------------------
-// Threshold select (the tensor-core step, no pins).  The scorer (score_tc.cu,
-// SCORE pass) already wrote each live row's key and counted
-// float_bits(score) >> 14 into a 65536-bin per-layer histogram (+ a 256-bin
-// coarse one).  Scores are softmax weights in [0, 1] (bin and key prefix agree
-// for any score in [0, 2)), so bin b holds exactly the keys with
-// key >> 14 == 0x1FFFF - b.  Grid: kTSParts CTAs per layer (128 threads):
-//   every CTA   finds the threshold bin and its rank from the coarse and fine
-//               histograms (two 1 KB reads) and appends the candidates of
-//               its slice of the layer (live rows in that bin) to the layer's
-//               candidate list;
+// Threshold select (the tensor-core step, no pins), with the compaction plan
+// folded in.  The scorer (score_tc.cu, SCORE pass) already wrote each live
+// row's key and counted float_bits(score) >> 14 into a 65536-bin per-layer
+// histogram (+ a 256-bin coarse one).  Scores are softmax weights in [0, 1]
+// (bin and key prefix agree for any score in [0, 2)), so bin b holds exactly
+// the keys with key >> 14 == 0x1FFFF - b.  Grid: `parts` CTAs per layer (128
+// threads), each owning a chunk-aligned slice of the layer's rows:
+//   every CTA   finds the threshold bin kb and its rank from the coarse and
+//               fine histograms (two 1 KB reads); over its slice it counts,
+//               per 128-row compaction chunk, the live rows certainly kept
+//               (key bin < kb) and appends the undecided ones (bin == kb) to
+//               the layer's candidate list {key, row, position << 8 | head};
 //   last CTA    (per-layer arrival counter) resolves the exact threshold key T
 //               and tiebreak U among the candidates (8-bit radix on the
-//               remaining 14 key bits, then on position << 8 | head), writes
-//               thr[l] = {T | keep_all << 32, U} and resets the counters for
-//               the next step (compact_count_kernel zeroes the histograms).
-// The compaction then keeps live rows with key < T || (key == T && tiebreak
-// <= U).
+//               remaining 14 key bits, then on position << 8 | head), adds
+//               the kept candidates to their chunks, scans the chunk counts
+//               into the compaction plan (chunk prefixes, output head
+//               offsets/lengths, the does-not-fit flag -- the former
+//               count/plan launches), writes thr[l] = {T | flags << 32, U}
+//               and resets the counters for the next step (the next P1
+//               launch zeroes the histograms).
+// The gather (compact.cu) then keeps live rows with key < T || (key == T &&
+// tiebreak <= U).
 // ---------------------------------------------------------------------------
 constexpr int kTSThreads = 128;
 constexpr int kTSCand = 1024;  // candidates resolved in shared memory
+constexpr int kTSBlk = 16;     // 128-row chunks per slice iteration
 
 struct ThreshParams {
     LayerTable lt;
+    LayerTable out_lt;  // output cache capacity layout (the plan's fit check)
     int64_t budget[kMaxLayers];
     const int32_t* head_off;
     const int32_t* head_len;
@@ -564,10 +572,19 @@ struct ThreshParams {
     uint32_t* hist_fine;     // [layers][65536]
     uint32_t* hist_coarse;   // [layers][256]
     uint64_t* thr;           // [layers][2]
-    uint4* cand;             // [layers][kTSCand] {key, 0, tiebreak lo, tiebreak hi}
+    uint4* cand;             // [layers][kTSCand] {key, layer row, tiebreak lo, tiebreak hi}
     unsigned* cand_n;        // [layers]
     unsigned* done;          // [layers]
     int32_t* kept_per_layer;
+    // compaction plan (CompactWs) and the output head layout
+    int32_t* chunk_cnt;
+    int32_t* chunk_prefix;
+    int32_t* layer_bad;
+    int32_t* out_off;  // [layers][H + 1]
+    int32_t* out_len;  // [layers][H]
+    int max_chunks;
+    int rpp;  // rows per CTA slice (a multiple of kChunkRows)
+    int slack;
     int H;
     int parts;
     int* err_flag;
@@ -579,8 +596,11 @@ struct TSShared {
     uint32_t tot[256];
     uint32_t hist[256];
     uint32_t ck[kTSCand];
+    int32_t cr[kTSCand];
     uint64_t ct[kTSCand];
     int64_t red[kTSThreads / 32];
+    int64_t head_prefix[kMaxHeads + 1];
+    int32_t wc[kTSBlk][kTSThreads / 32];  // per (chunk of the iteration, warp): certainly kept rows
     int bucket;
     int64_t before, eq;
     int last;
@@ -622,7 +642,7 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
     __shared__ TSShared S;
     const int l = blockIdx.y, part = blockIdx.x;
     const int H = P.H;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i <= H; i += kTSThreads) S.off[i] = P.head_off[l * (H + 1) + i];
     for (int i = tid; i < H; i += kTSThreads) S.len[i] = P.head_len[l * H + i];
     __syncthreads();
@@ -632,6 +652,7 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
     const int64_t base = P.lt.base[l];
     const uint32_t* keys = P.keys + base;
     const int32_t* pos = P.pos + base;
+    int32_t* ccnt = P.chunk_cnt + int64_t(l) * P.max_chunks;
     const int64_t limit = int64_t(H) * P.budget[l];
     auto head_of = [&](int r) -> int {
         int lo = 0, hi = H - 1;
@@ -647,6 +668,7 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
     // no threshold bin exists, the resolve below emits the "none" flag
     const bool none = n_live > limit && limit == 0;
     const bool select = n_live > limit && !none;
+    const bool all = n_live <= limit;  // every live row stays
     if (select) {
         // threshold bin: coarse then fine histogram, bins in key order
         for (int i = tid; i < 256; i += kTSThreads) S.tot[i] = __ldcg(P.hist_coarse + l * 256 + 255 - i);
@@ -661,39 +683,58 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
         k_rem -= S.before;
         eq = S.eq;
         kb = uint32_t(0x1FFFF - (cb * 256 + 255 - S.bucket));
-        // this part's slice: candidates -> the layer's list (keys loaded 16 per
-        // thread up front, one memory round trip per 2048 rows)
-        const int r_beg = int(int64_t(region) * part / P.parts), r_end = int(int64_t(region) * (part + 1) / P.parts);
-        for (int b0 = r_beg; b0 < r_end; b0 += 16 * kTSThreads) {  // warp-uniform
-            uint32_t kv[16];
+    }
+    // this CTA's chunk-aligned slice: per chunk the rows certainly kept, and
+    // the threshold bin's candidates -> the layer's list (keys loaded 16 per
+    // thread up front, one memory round trip per 2048 rows)
+    const int r_beg = part * P.rpp, r_end = min(region, r_beg + P.rpp);
+    for (int b0 = r_beg; b0 < r_end; b0 += kTSBlk * kTSThreads) {  // block-uniform
+        uint32_t kv[kTSBlk];
+        if (select) {
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < kTSBlk; ++u) {
                 const int rr = b0 + u * kTSThreads + tid;
                 kv[u] = rr < r_end ? __ldcg(keys + rr) : 0u;
             }
-            int h = head_of(min(b0 + tid, max(r_end - 1, 0)));
+        }
+        int h = head_of(min(b0 + tid, max(r_end - 1, 0)));
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const int rr = b0 + u * kTSThreads + tid;
-                bool c = false;
-                if (rr < r_end) {
-                    while (h + 1 < H && S.off[h + 1] <= rr) ++h;
-                    c = rr - S.off[h] < S.len[h] && (kv[u] >> 14) == kb;
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, c);
-                if (bal == 0) continue;
-                const int leader = __ffs(bal) - 1;
-                unsigned at = 0;
-                if (lane == leader) at = atomicAdd(P.cand_n + l, unsigned(__popc(bal)));
-                at = __shfl_sync(0xffffffffu, at, leader) + __popc(bal & ((1u << lane) - 1u));
-                if (c && at < unsigned(kTSCand)) {
-                    const uint64_t tb = (uint64_t(uint32_t(pos[rr])) << 8) | uint64_t(h);
-                    P.cand[int64_t(l) * kTSCand + at] = make_uint4(kv[u], 0u, uint32_t(tb), uint32_t(tb >> 32));
+        for (int u = 0; u < kTSBlk; ++u) {
+            const int rr = b0 + u * kTSThreads + tid;
+            bool c = false, def = false;
+            if (rr < r_end) {
+                while (h + 1 < H && S.off[h + 1] <= rr) ++h;
+                const bool live = rr - S.off[h] < S.len[h];
+                if (select) {
+                    c = live && (kv[u] >> 14) == kb;
+                    def = live && (kv[u] >> 14) < kb;
+                } else {
+                    def = live && all;
                 }
             }
+            const unsigned dball = __ballot_sync(0xffffffffu, def);
+            if (lane == 0) S.wc[u][warp] = __popc(dball);
+            const unsigned bal = __ballot_sync(0xffffffffu, c);
+            if (bal == 0) continue;
+            const int leader = __ffs(bal) - 1;
+            unsigned at = 0;
+            if (lane == leader) at = atomicAdd(P.cand_n + l, unsigned(__popc(bal)));
+            at = __shfl_sync(0xffffffffu, at, leader) + __popc(bal & ((1u << lane) - 1u));
+            if (c && at < unsigned(kTSCand)) {
+                const uint64_t tb = (uint64_t(uint32_t(pos[rr])) << 8) | uint64_t(h);
+                P.cand[int64_t(l) * kTSCand + at] = make_uint4(kv[u], uint32_t(rr), uint32_t(tb), uint32_t(tb >> 32));
+            }
         }
+        __syncthreads();
+        if (tid < kTSBlk && b0 + tid * kTSThreads < r_end) {
+            int32_t v = 0;
+#pragma unroll
+            for (int w = 0; w < kTSThreads / 32; ++w) v += S.wc[tid][w];
+            ccnt[(b0 + tid * kTSThreads) / kChunkRows] = v;
+        }
+        __syncthreads();
     }
-    // the last CTA of the layer resolves
+    // the last CTA of the layer resolves and plans
     __threadfence();
     __syncthreads();
     if (tid == 0) S.last = atomicAdd(P.done + l, 1u) == unsigned(P.parts - 1);
@@ -711,20 +752,21 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
             for (int i = tid; i < int(n); i += kTSThreads) {
                 const uint4 cv = __ldcg(P.cand + int64_t(l) * kTSCand + i);
                 S.ck[i] = cv.x;
+                S.cr[i] = int32_t(cv.y);
                 S.ct[i] = (uint64_t(cv.w) << 32) | cv.z;
             }
             __syncthreads();
         }
-        // for_each(f): f(key, tiebreak) over the bin's candidates
+        // for_each(f): f(key, tiebreak, layer row) over the bin's candidates
         auto each = [&](auto&& f) {
             if (listed) {
-                for (int i = tid; i < int(n); i += kTSThreads) f(S.ck[i], S.ct[i]);
+                for (int i = tid; i < int(n); i += kTSThreads) f(S.ck[i], S.ct[i], S.cr[i]);
             } else {  // list overflow: the layer's rows in global memory
                 for (int rr = tid; rr < region; rr += kTSThreads) {
                     const int h = head_of(rr);
                     if (rr - S.off[h] >= S.len[h]) continue;
                     const uint32_t key = __ldcg(keys + rr);
-                    if ((key >> 14) == kb) f(key, (uint64_t(uint32_t(pos[rr])) << 8) | uint64_t(h));
+                    if ((key >> 14) == kb) f(key, (uint64_t(uint32_t(pos[rr])) << 8) | uint64_t(h), rr);
                 }
             }
         };
@@ -736,7 +778,7 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
             const uint32_t dmask = (1u << (hi - lo)) - 1;
             for (int i = tid; i < 256; i += kTSThreads) S.hist[i] = 0;
             __syncthreads();
-            each([&](uint32_t k, uint64_t) {
+            each([&](uint32_t k, uint64_t, int) {
                 if (((k ^ prefix) & mask) == 0) atomicAdd(&S.hist[(k >> lo) & dmask], 1u);
             });
             __syncthreads();
@@ -753,7 +795,7 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
             for (int shift = 32; shift >= 0; shift -= 8) {
                 for (int i = tid; i < 256; i += kTSThreads) S.hist[i] = 0;
                 __syncthreads();
-                each([&](uint32_t k, uint64_t tb) {
+                each([&](uint32_t k, uint64_t tb, int) {
                     if (k == T && ((tb ^ tp) & tm) == 0) atomicAdd(&S.hist[(tb >> shift) & 0xFF], 1u);
                 });
                 __syncthreads();
@@ -766,30 +808,113 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
         }
         t0 = T;
         t1 = U;
+        // the kept candidates join their chunks' counts
+        each([&](uint32_t k, uint64_t tb, int rr) {
+            if (k < T || (k == T && tb <= U)) atomicAdd(ccnt + rr / kChunkRows, 1);
+        });
+        __threadfence();
+        __syncthreads();
     }
+    // ---- compaction plan: chunk prefixes, output head offsets / lengths ----
+    const uint32_t T = uint32_t(t0);
+    auto keep_row = [&](int r) -> bool {  // the gather's keep rule
+        const int h = head_of(r);
+        if (none || r - S.off[h] >= S.len[h]) return false;
+        if (all) return true;
+        const uint32_t key = __ldcg(keys + r);
+        return key < T || (key == T && ((uint64_t(uint32_t(pos[r])) << 8) | uint64_t(h)) <= t1);
+    };
+    const int nchunks = (region + kChunkRows - 1) / kChunkRows;
+    int32_t* cpre = P.chunk_prefix + int64_t(l) * P.max_chunks;
+    {  // block-wide exclusive scan, each thread owns a contiguous run of chunks
+        const int per = (nchunks + kTSThreads - 1) / kTSThreads;
+        const int c0 = tid * per, c1 = min(nchunks, c0 + per);
+        int64_t mine = 0;
+        for (int c = c0; c < c1; ++c) mine += __ldcg(ccnt + c);
+        int64_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) S.red[warp] = incl;
+        __syncthreads();
+        int64_t run = incl - mine;
+        for (int w = 0; w < warp; ++w) run += S.red[w];
+        for (int c = c0; c < c1; ++c) {
+            cpre[c] = int32_t(run);
+            run += __ldcg(ccnt + c);
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    // kept rows before every head start: the chunk prefix plus a warp-wide
+    // count of the kept rows in [chunk start, head start)
+    for (int h = warp; h <= H; h += kTSThreads / 32) {
+        const int x = S.off[h];
+        const int c = x / kChunkRows;
+        int64_t v;
+        if (c >= nchunks) {
+            v = nchunks == 0 ? 0 : int64_t(__ldcg(cpre + nchunks - 1)) + __ldcg(ccnt + nchunks - 1);
+        } else {
+            int cnt = 0;
+            for (int r = c * kChunkRows + lane; r < x; r += 32) cnt += keep_row(r) ? 1 : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            v = int64_t(__ldcg(cpre + c)) + cnt;
+        }
+        if (lane == 0) S.head_prefix[h] = v;
+    }
+    __syncthreads();
     if (tid == 0) {
         P.thr[2 * l] = t0;
         P.thr[2 * l + 1] = t1;
         if (P.kept_per_layer) P.kept_per_layer[l] = int32_t(min(n_live, limit));
         P.cand_n[l] = 0;
         P.done[l] = 0;
+        const int64_t cap = P.out_lt.base[l + 1] - P.out_lt.base[l];
+        const int64_t need = S.head_prefix[H] + int64_t(P.slack) * H;
+        const bool bad = need > cap;
+        P.layer_bad[l] = bad;
+        if (bad) {
+            // the output layer cannot hold the kept rows: flag it, leave the
+            // layer empty and let the gather skip it (no store past the layer)
+            atomicCAS(P.err_flag, 0, EPK_ERR_ARG);
+            for (int h = 0; h <= H; ++h) P.out_off[l * (H + 1) + h] = 0;
+            for (int h = 0; h < H; ++h) P.out_len[l * H + h] = 0;
+        } else {
+            for (int h = 0; h < H; ++h) {
+                P.out_off[l * (H + 1) + h] = int32_t(S.head_prefix[h] + int64_t(P.slack) * h);
+                P.out_len[l * H + h] = int32_t(S.head_prefix[h + 1] - S.head_prefix[h]);
+            }
+            P.out_off[l * (H + 1) + H] = int32_t(S.head_prefix[H] + int64_t(P.slack) * H);
+        }
     }
-    // (the histograms are zeroed for the next step by compact_count_kernel,
-    // spread over its CTAs)
 }
 
-int launch_select_threshold(epk_ctx* ctx, const epk_cache_desc* c, const FusedSelect* fs, const int64_t* budgets,
-                            uint64_t* thr, int32_t* kept) {
+int launch_select_threshold(epk_ctx* ctx, const epk_cache_desc* c, const epk_cache_desc* out, int out_slack,
+                            const FusedSelect* fs, const int64_t* budgets, uint64_t* thr, int32_t* kept) {
     if (c->kv_heads > kMaxHeads) return fail(EPK_ERR_UNSUPPORTED, "select: more than 64 kv heads");
+    if (out_slack < 0) return fail(EPK_ERR_ARG, "compact: negative slack");
     ThreshParams P;
     int rc = make_layer_table(c, &P.lt);
     if (rc) return rc;
+    if ((rc = make_layer_table(out, &P.out_lt))) return rc;
     int64_t max_region = 0;
     for (int l = 0; l < c->layers; ++l) {
         if (budgets[l] < 0) return fail(EPK_ERR_ARG, "select: negative budget");
         P.budget[l] = budgets[l];
         max_region = std::max<int64_t>(max_region, P.lt.base[l + 1] - P.lt.base[l]);
     }
+    CompactWs w;
+    if ((rc = compact_ws(ctx, c, &w))) return rc;
+    P.chunk_cnt = w.chunk_cnt;
+    P.chunk_prefix = w.chunk_prefix;
+    P.layer_bad = w.layer_bad;
+    P.max_chunks = w.max_chunks;
+    P.out_off = out->head_off;
+    P.out_len = out->head_len;
+    P.slack = out_slack;
     P.head_off = c->head_off;
     P.head_len = c->head_len;
     P.pos = c->pos;
@@ -803,8 +928,11 @@ int launch_select_threshold(epk_ctx* ctx, const epk_cache_desc* c, const FusedSe
     P.kept_per_layer = kept;
     P.H = c->kv_heads;
     // one CTA per 4096-row slice (measured: 8192 -> 4096 rows takes the cfg2
-    // select from 35 to 27 us; smaller slices no longer help)
+    // select from 35 to 27 us; smaller slices no longer help), slices aligned
+    // to the compaction chunks, at most 64 per layer
     P.parts = int(std::max<int64_t>(1, std::min<int64_t>(64, (max_region + 4095) / 4096)));
+    const int64_t per = (max_region + P.parts - 1) / P.parts;
+    P.rpp = int(std::max<int64_t>(kChunkRows, (per + kChunkRows - 1) / kChunkRows * kChunkRows));
     P.err_flag = ctx->err_flag;
     EPK_PROF(ctx, "select");
     EPK_CUDA_CHECK(launch_pdl(select_threshold_kernel, dim3(P.parts, c->layers), dim3(kTSThreads), 0, ctx->stream, P));
