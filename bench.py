@@ -713,9 +713,9 @@ def main():
     work = {
         "p1_rowstats": ("sfu", G * p * (live + L * H * p * n_ep) / 1e12, "Tex2/s", sfu_peak / 1e12),
         "p2_colscore": ("tensor", 2.0 * G * p * d * live / 1e12, "TFLOP/s", tc_burst),
-        "compact_gather": ("hbm", (4.0 * keep * d * 2 + 8.0 * keep + live) / 1e9, "GB/s", hbm),
+        # gather: K and V rows read + written, positions of the kept rows read + written, every live row's key
+        "compact_gather": ("hbm", (4.0 * keep * d * 2 + 8.0 * keep + 4.0 * live) / 1e9, "GB/s", hbm),
         "select": ("hbm", (4.0 * live) / 1e9, "GB/s", hbm),
-        "compact_count": ("hbm", (4.0 * live + live) / 1e9, "GB/s", hbm),
     }
     for k, (bound, amount, unit, peak) in work.items():
         if k in kernels and kernels[k]["ms_per_step"] > 0:

@@ -167,7 +167,9 @@ __global__ void __launch_bounds__(256) compact_plan_kernel(const __grid_constant
 // Warps walk the flattened (layer, chunk) items; the default launch gives
 // every warp one item, a persistent launch (ctx->gather_ctas) strides.
 __global__ void __launch_bounds__(512) compact_gather_kernel(const __grid_constant__ CompactParams P) {
+    TL_BEGIN();
     pdl_wait();
+    TL_GO();
     const int wpb = blockDim.x >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t items = int64_t(P.layers) * P.max_chunks;
@@ -208,10 +210,14 @@ __global__ void __launch_bounds__(512) compact_gather_kernel(const __grid_consta
             if (thr_mode) {
                 k = false;
                 if (r < rows && !((t0 >> 33) & 1) && r - off[h] < P.in_len[layer * P.H + h]) {
-                    ps = P.in_pos[in_base + r];
                     const uint32_t key = __ldcg(P.keys + in_base + r);
-                    k = ((t0 >> 32) & 1) || key < uint32_t(t0) ||
-                        (key == uint32_t(t0) && ((uint64_t(uint32_t(ps)) << 8) | uint64_t(h)) <= U);
+                    k = ((t0 >> 32) & 1) || key < uint32_t(t0);
+                    if (!k && key == uint32_t(t0)) {  // inside the threshold tie: (position, head) decides
+                        ps = P.in_pos[in_base + r];
+                        k = ((uint64_t(uint32_t(ps)) << 8) | uint64_t(h)) <= U;
+                    } else if (k) {
+                        ps = P.in_pos[in_base + r];
+                    }
                 }
             } else {
                 k = r < rows && kp[r];
@@ -257,6 +263,7 @@ __global__ void __launch_bounds__(512) compact_gather_kernel(const __grid_consta
             }
         }
     }
+    TL_END(6);
 }
 
 int compact_ws(epk_ctx* ctx, const epk_cache_desc* in, CompactWs* w) {

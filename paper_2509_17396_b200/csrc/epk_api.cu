@@ -309,6 +309,29 @@ int epk_ctx_poll_error(epk_ctx* ctx) {
 
 int64_t epk_ctx_launch_count(epk_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+#ifdef EPK_TIMELINE
+extern "C++" {
+namespace epk {
+static std::vector<int (*)(int, unsigned long long*, int)>& tl_readers() {
+    static std::vector<int (*)(int, unsigned long long*, int)> r;
+    return r;
+}
+int tl_register(int (*reader)(int, unsigned long long*, int)) {
+    tl_readers().push_back(reader);
+    return 1;
+}
+}  // namespace epk
+}
+// experiment builds only: copies every translation unit's timeline records
+// out (reset != 0 clears the rings after copying); returns the record count
+extern "C" int epk_debug_timeline(int reset, unsigned long long* out, int max_records) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    int n = 0;
+    for (auto f : epk::tl_readers()) n += f(reset, out ? out + int64_t(n) * 4 : nullptr, max_records - n);
+    return n;
+}
+#endif
+
 int epk_ctx_profile(epk_ctx* ctx, int32_t enable) {
     int rc = check_ctx(ctx);
     if (rc) return rc;

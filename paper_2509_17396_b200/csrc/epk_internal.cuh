@@ -109,6 +109,56 @@ void prof_end(epk_ctx* ctx);
 // gives ~0.5 %.  EPK_NO_PDL=1 disables the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Experiment builds only (-DEPK_TIMELINE): lane 0 of every warp records its
+// kernel's globaltimer at entry, after pdl_wait, and at exit into a device
+// ring read back by epk_debug_timeline (scripts/tl_step.py prints the step's
+// per-kernel critical path).
+#ifdef EPK_TIMELINE
+// one ring per translation unit (no relocatable device code), each reader
+// registered with epk_api.cu's epk_debug_timeline at load time
+constexpr int kTlMax = 1 << 15;
+static __device__ unsigned long long g_tl[kTlMax][4];  // {kernel id << 32 | cta << 8 | warp, entry, go, end}
+static __device__ unsigned int g_tl_n;
+int tl_register(int (*reader)(int, unsigned long long*, int));
+static int tl_read_local(int reset, unsigned long long* out, int max_records) {
+    unsigned int n = 0;
+    cudaMemcpyFromSymbol(&n, g_tl_n, sizeof(n));
+    n = n < unsigned(kTlMax) ? n : unsigned(kTlMax);
+    const unsigned m = n < unsigned(max_records > 0 ? max_records : 0) ? n : unsigned(max_records > 0 ? max_records : 0);
+    if (out && m) cudaMemcpyFromSymbol(out, g_tl, size_t(m) * 32);
+    if (reset) {
+        const unsigned z = 0;
+        cudaMemcpyToSymbol(g_tl_n, &z, sizeof(z));
+    }
+    return int(m);
+}
+static const int tl_registered = tl_register(tl_read_local);
+__device__ __forceinline__ uint64_t tl_now() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL_BEGIN() const uint64_t tl_t0 = tl_now()
+#define TL_GO() const uint64_t tl_t1 = tl_now()
+#define TL_END(id)                                                                                        \
+    do {                                                                                                  \
+        if ((threadIdx.x & 31) == 0) {                                                                    \
+            const unsigned i_ = atomicAdd(&g_tl_n, 1u);                                                   \
+            if (i_ < unsigned(kTlMax)) {                                                                  \
+                g_tl[i_][0] = (uint64_t(id) << 32) | (uint64_t(blockIdx.x + blockIdx.y * gridDim.x) << 8) | \
+                              uint64_t(threadIdx.x >> 5);                                                 \
+                g_tl[i_][1] = tl_t0;                                                                      \
+                g_tl[i_][2] = tl_t1;                                                                      \
+                g_tl[i_][3] = tl_now();                                                                   \
+            }                                                                                             \
+        }                                                                                                 \
+    } while (0)
+#else
+#define TL_BEGIN()
+#define TL_GO()
+#define TL_END(id)
+#endif
+
 bool pdl_enabled();
 
 template <typename... KArgs, typename... Args>

@@ -324,7 +324,9 @@ constexpr int kBiasMaxCov = 32;
 __global__ void tc_bias_kernel(const __grid_constant__ TcParams P) {
     __shared__ int s_cov[16][kBiasMaxCov];  // per chunk group: slot base of each covering P1 CTA
     __shared__ int s_ncov[16];
+    TL_BEGIN();
     pdl_wait();
+    TL_GO();
     const int hk = blockIdx.x;
     const int64_t T1 = P.p1_pre[P.p1_runs];
     if (threadIdx.x < P.cgroups) {
@@ -370,6 +372,7 @@ __global__ void tc_bias_kernel(const __grid_constant__ TcParams P) {
     }
     write_bias_row(P, hk, rq, lse2);
     }
+    TL_END(3);
 }
 
 // <= 128 registers (45K of the SM's 64K) and <= kSmemBudget of shared memory,
@@ -402,7 +405,9 @@ __global__ void __maxnreg__(128)
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte aligned (SWIZZLE_128B atoms), derived from smem_raw by pointer
     // arithmetic so the compiler keeps shared-space (LDS/STS) addressing.
+    TL_BEGIN();
     pdl_wait();  // every input may come from the previous kernel in the stream
+    TL_GO();
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t q_half = uint32_t(P.qcap) * kRowB;   // Q d-half stride
     const uint32_t k_half = uint32_t(P.krows) * kRowB;  // K d-half stride
@@ -841,6 +846,7 @@ __global__ void __maxnreg__(128)
     __syncthreads();
     tc_fence_after();
     if (warp == 1) tmem_dealloc(tmem, 512);
+    TL_END(MODE == MODE_STATS ? 1 : 2);
 }
 
 // ---------------------------------------------------------------------------

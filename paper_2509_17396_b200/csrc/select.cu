@@ -638,7 +638,9 @@ __device__ void ts_find_bucket(TSShared& S, const uint32_t* tot, int nbins, int6
 }
 
 __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __grid_constant__ ThreshParams P) {
+    TL_BEGIN();
     pdl_wait();
+    TL_GO();
     __shared__ TSShared S;
     const int l = blockIdx.y, part = blockIdx.x;
     const int H = P.H;
@@ -739,7 +741,10 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
     __syncthreads();
     if (tid == 0) S.last = atomicAdd(P.done + l, 1u) == unsigned(P.parts - 1);
     __syncthreads();
-    if (!S.last) return;
+    if (!S.last) {
+        TL_END(4);
+        return;
+    }
     __threadfence();
     // thr[2l] bit 32: keep every live row; bit 33: keep none; else the exact
     // threshold key T in the low word and the (position << 8 | head) tiebreak U
@@ -890,6 +895,7 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
             P.out_off[l * (H + 1) + H] = int32_t(S.head_prefix[H] + int64_t(P.slack) * H);
         }
     }
+    TL_END(5);
 }
 
 int launch_select_threshold(epk_ctx* ctx, const epk_cache_desc* c, const epk_cache_desc* out, int out_slack,

@@ -5,7 +5,8 @@ evict_to_budget's semantics at the extremes:
   default tensor-core step (threshold select) as on the generic select;
 * an output cache too small for the kept rows raises EPK_ERR_ARG and the
   gather writes nothing past the offending layer (the next layer's rows stay
-  intact and correct);
+  intact and correct), on the generic compaction and on the default step
+  (whose threshold select plans the compaction);
 * the exact-f32 scorer refuses a head longer than n_max_per_head instead of
   overrunning its scratch;
 * epk_append honours its slack argument;
@@ -94,6 +95,41 @@ def test_compact_overflow_fails_closed(gpu):
     assert out.retained_positions()[1] == cin.retained_positions()[1]
     ra, rb = out.live_rows(1), cin.live_rows(1)
     assert torch.equal(out.k[ra].view(torch.int16), cin.k[rb].view(torch.int16))
+
+
+def test_tc_step_overflow_fails_closed(gpu):
+    """The default tensor-core step plans the compaction inside its threshold
+    select: an output layer too small for its kept rows is flagged
+    (EPK_ERR_ARG), left empty and never written past, and the other layers
+    equal the generic select + compaction on the step's own scores."""
+    from paper_2509_17396_b200.step import evict_step
+    rng = np.random.default_rng(11)
+    L, H, Hq, p, slack = 3, 4, 8, 16, 8
+    counts = [[300, 250, 0, 90], [120, 120, 120, 120], [40, 41, 42, 43]]
+    budgets = [100, 60, 50]  # layer 2 is under budget: everything kept
+    cin, cap = _cache(gpu, rng, counts, slack)
+    small = list(cap)
+    small[1] = 60 * H + slack * H - 1  # one row short of layer 1's kept rows + slack
+    q = torch.randn(L, Hq, p, 128, device="cuda").bfloat16()
+    kp = torch.randn(L, H, p, 128, device="cuda").bfloat16()
+    out = gpu.EpisodeCache(L, H, 128, small, torch.bfloat16, "cuda")
+    out.k.fill_(7.0)
+    scores = torch.zeros(cin.rows, dtype=torch.float32, device="cuda")
+    evict_step(cin, out, q, kp, budgets, mode="tc_bf16", slack=slack, scores=scores)
+    torch.cuda.synchronize()
+    with pytest.raises(gpu.Error):
+        gpu.default_context(0).poll_error()
+    assert out.head_len[1].sum().item() == 0
+    b1, b2 = int(out.layer_base[1]), int(out.layer_base[2])
+    assert bool((out.k[b1:b2] == 7.0).all())  # nothing landed in (or past) layer 1
+    ref = gpu.EpisodeCache(L, H, 128, cap, torch.bfloat16, "cuda")
+    gpu.compact(cin, gpu.select_pooled(cin, scores, budgets), ref, slack=slack)
+    torch.cuda.synchronize()
+    for l in (0, 2):
+        assert out.retained_positions()[l] == ref.retained_positions()[l]
+        ra, rb = out.live_rows(l), ref.live_rows(l)
+        assert torch.equal(out.k[ra].view(torch.int16), ref.k[rb].view(torch.int16))
+        assert torch.equal(out.v[ra].view(torch.int16), ref.v[rb].view(torch.int16))
 
 
 def test_f32_scorer_refuses_short_n_max(gpu):

@@ -1,5 +1,5 @@
 """The default tensor-core block step (epk_evict_step: P1 -> P2 with fused
-histograms -> threshold select -> count/plan/gather) at the edges of its
+histograms -> threshold select + compaction plan -> gather) at the edges of its
 layout limits -- 128 layers (kMaxLayers), 64 kv heads (kMaxHeads), heads that
 are empty or under budget, a whole layer under budget -- bit-exact against the
 generic pooled select + compaction (themselves pinned to evict_to_budget by

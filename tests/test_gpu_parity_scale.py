@@ -9,7 +9,7 @@ the CPU oracle -- not GPU against GPU.
     - fp32 parity scorer bit-exact with the EPK-F32 restatement and within
       1e-5 relative of fp64 (north_star).
 * the DEFAULT block step (epk_evict_step: tensor-core scores with fused
-  histograms -> threshold select -> count/plan/gather) at the full cfg2 size
+  histograms -> threshold select + compaction plan -> gather) at the full cfg2 size
   (28 layers) with tie stress -- 1 % of K rows duplicated within heads, whole
   heads duplicated across heads (same positions, identical query groups, so
   equal (score, position) pairs resolved by the head), plus a layer whose
