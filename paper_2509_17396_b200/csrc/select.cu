@@ -559,7 +559,10 @@ int launch_select(epk_ctx* ctx, const epk_cache_desc* c, const void* scores, int
 // ---------------------------------------------------------------------------
 constexpr int kTSThreads = 128;
 constexpr int kTSCand = 1024;  // candidates resolved in shared memory
-constexpr int kTSBlk = 16;     // 128-row chunks per slice iteration
+#ifndef EPK_TS_BLK
+#define EPK_TS_BLK 16  // 32 spills at the 4-CTA/SM register budget
+#endif
+constexpr int kTSBlk = EPK_TS_BLK;  // 128-row chunks per slice iteration (keys loaded up front: one round trip)
 
 struct ThreshParams {
     LayerTable lt;
@@ -595,9 +598,15 @@ struct TSShared {
     int32_t len[kMaxHeads];
     uint32_t tot[256];
     uint32_t hist[256];
-    uint32_t ck[kTSCand];
-    int32_t cr[kTSCand];
-    uint64_t ct[kTSCand];
+    union {
+        struct {  // last CTA: the layer's candidates
+            uint32_t ck[kTSCand];
+            int32_t cr[kTSCand];
+            uint64_t ct[kTSCand];
+        };
+        uint4 lc[kTSCand];  // every CTA: its slice's candidates {key, row, head, 0} before they go global
+    };
+    unsigned nlc;
     int64_t red[kTSThreads / 32];
     int64_t head_prefix[kMaxHeads + 1];
     int32_t wc[kTSBlk][kTSThreads / 32];  // per (chunk of the iteration, warp): certainly kept rows
@@ -637,7 +646,7 @@ __device__ void ts_find_bucket(TSShared& S, const uint32_t* tot, int nbins, int6
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __grid_constant__ ThreshParams P) {
+__global__ void __launch_bounds__(kTSThreads, 4) select_threshold_kernel(const __grid_constant__ ThreshParams P) {
     TL_BEGIN();
     pdl_wait();
     TL_GO();
@@ -645,14 +654,28 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
     const int l = blockIdx.y, part = blockIdx.x;
     const int H = P.H;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // independent loads first, in flight together: the head layout, the
+    // coarse histogram and the keys of this CTA's first slice block (rows of
+    // the layer's capacity; the slice bound is applied once the layout is in)
     for (int i = tid; i <= H; i += kTSThreads) S.off[i] = P.head_off[l * (H + 1) + i];
     for (int i = tid; i < H; i += kTSThreads) S.len[i] = P.head_len[l * H + i];
+    const int64_t base = P.lt.base[l];
+    const uint32_t* keys = P.keys + base;
+    const int cap_l = int(P.lt.base[l + 1] - base);
+    const int r_beg = part * P.rpp;
+    uint32_t kv[kTSBlk];
+#pragma unroll
+    for (int u = 0; u < kTSBlk; ++u) {
+        const int rr = r_beg + u * kTSThreads + tid;
+        kv[u] = rr < cap_l ? __ldcg(keys + rr) : 0u;
+    }
+    uint32_t hc[256 / kTSThreads];
+#pragma unroll
+    for (int j = 0; j < 256 / kTSThreads; ++j) hc[j] = __ldcg(P.hist_coarse + l * 256 + 255 - (tid + j * kTSThreads));
     __syncthreads();
     int64_t n_live = 0;
     for (int h = 0; h < H; ++h) n_live += S.len[h];
     const int region = S.off[H];
-    const int64_t base = P.lt.base[l];
-    const uint32_t* keys = P.keys + base;
     const int32_t* pos = P.pos + base;
     int32_t* ccnt = P.chunk_cnt + int64_t(l) * P.max_chunks;
     const int64_t limit = int64_t(H) * P.budget[l];
@@ -673,7 +696,8 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
     const bool all = n_live <= limit;  // every live row stays
     if (select) {
         // threshold bin: coarse then fine histogram, bins in key order
-        for (int i = tid; i < 256; i += kTSThreads) S.tot[i] = __ldcg(P.hist_coarse + l * 256 + 255 - i);
+#pragma unroll
+        for (int j = 0; j < 256 / kTSThreads; ++j) S.tot[tid + j * kTSThreads] = hc[j];
         __syncthreads();
         ts_find_bucket(S, S.tot, 256, k_rem);
         k_rem -= S.before;
@@ -686,13 +710,15 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
         eq = S.eq;
         kb = uint32_t(0x1FFFF - (cb * 256 + 255 - S.bucket));
     }
+    TL_END(7);
     // this CTA's chunk-aligned slice: per chunk the rows certainly kept, and
     // the threshold bin's candidates -> the layer's list (keys loaded 16 per
-    // thread up front, one memory round trip per 2048 rows)
-    const int r_beg = part * P.rpp, r_end = min(region, r_beg + P.rpp);
+    // thread at a time, the first block's before the histograms)
+    const int r_end = min(region, r_beg + P.rpp);
+    if (tid == 0) S.nlc = 0;
+    __syncthreads();
     for (int b0 = r_beg; b0 < r_end; b0 += kTSBlk * kTSThreads) {  // block-uniform
-        uint32_t kv[kTSBlk];
-        if (select) {
+        if (select && b0 != r_beg) {
 #pragma unroll
             for (int u = 0; u < kTSBlk; ++u) {
                 const int rr = b0 + u * kTSThreads + tid;
@@ -700,6 +726,7 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
             }
         }
         int h = head_of(min(b0 + tid, max(r_end - 1, 0)));
+        TL_END(8);
 #pragma unroll
         for (int u = 0; u < kTSBlk; ++u) {
             const int rr = b0 + u * kTSThreads + tid;
@@ -720,12 +747,9 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
             if (bal == 0) continue;
             const int leader = __ffs(bal) - 1;
             unsigned at = 0;
-            if (lane == leader) at = atomicAdd(P.cand_n + l, unsigned(__popc(bal)));
+            if (lane == leader) at = atomicAdd(&S.nlc, unsigned(__popc(bal)));  // shared memory: no round trip
             at = __shfl_sync(0xffffffffu, at, leader) + __popc(bal & ((1u << lane) - 1u));
-            if (c && at < unsigned(kTSCand)) {
-                const uint64_t tb = (uint64_t(uint32_t(pos[rr])) << 8) | uint64_t(h);
-                P.cand[int64_t(l) * kTSCand + at] = make_uint4(kv[u], uint32_t(rr), uint32_t(tb), uint32_t(tb >> 32));
-            }
+            if (c && at < unsigned(kTSCand)) S.lc[at] = make_uint4(kv[u], uint32_t(rr), uint32_t(h), 0u);
         }
         __syncthreads();
         if (tid < kTSBlk && b0 + tid * kTSThreads < r_end) {
@@ -736,6 +760,24 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
         }
         __syncthreads();
     }
+    // the slice's candidates -> the layer's list: one global reservation per
+    // CTA, positions loaded for all of them at once.  A slice with more than
+    // kTSCand candidates pushes the count past kTSCand, so the last CTA takes
+    // the unlisted path (it rescans the layer's rows).
+    if (select) {
+        if (tid == 0) {
+            const unsigned n = S.nlc;
+            S.before = n ? int64_t(atomicAdd(P.cand_n + l, n <= unsigned(kTSCand) ? n : n + kTSCand + 1)) : 0;
+        }
+        __syncthreads();
+        const unsigned n = min(S.nlc, unsigned(kTSCand)), at0 = unsigned(S.before);
+        for (unsigned i = tid; i < n && at0 + i < unsigned(kTSCand); i += kTSThreads) {
+            const uint4 e = S.lc[i];
+            const uint64_t tb = (uint64_t(uint32_t(pos[e.y])) << 8) | uint64_t(e.z);
+            P.cand[int64_t(l) * kTSCand + at0 + i] = make_uint4(e.x, e.y, uint32_t(tb), uint32_t(tb >> 32));
+        }
+    }
+    TL_END(9);
     // the last CTA of the layer resolves and plans
     __threadfence();
     __syncthreads();
@@ -813,6 +855,7 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
         }
         t0 = T;
         t1 = U;
+        TL_END(10);
         // the kept candidates join their chunks' counts
         each([&](uint32_t k, uint64_t tb, int rr) {
             if (k < T || (k == T && tb <= U)) atomicAdd(ccnt + rr / kChunkRows, 1);
@@ -829,13 +872,22 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
         const uint32_t key = __ldcg(keys + r);
         return key < T || (key == T && ((uint64_t(uint32_t(pos[r])) << 8) | uint64_t(h)) <= t1);
     };
+    TL_END(11);
     const int nchunks = (region + kChunkRows - 1) / kChunkRows;
     int32_t* cpre = P.chunk_prefix + int64_t(l) * P.max_chunks;
     {  // block-wide exclusive scan, each thread owns a contiguous run of chunks
+       // (loaded kScanU at a time, so a run costs one L2 round trip per kScanU)
+        constexpr int kScanU = 8;
         const int per = (nchunks + kTSThreads - 1) / kTSThreads;
         const int c0 = tid * per, c1 = min(nchunks, c0 + per);
         int64_t mine = 0;
-        for (int c = c0; c < c1; ++c) mine += __ldcg(ccnt + c);
+        for (int cb = c0; cb < c1; cb += kScanU) {
+            int32_t v[kScanU];
+#pragma unroll
+            for (int u = 0; u < kScanU; ++u) v[u] = cb + u < c1 ? __ldcg(ccnt + cb + u) : 0;
+#pragma unroll
+            for (int u = 0; u < kScanU; ++u) mine += v[u];
+        }
         int64_t incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -846,13 +898,20 @@ __global__ void __launch_bounds__(kTSThreads) select_threshold_kernel(const __gr
         __syncthreads();
         int64_t run = incl - mine;
         for (int w = 0; w < warp; ++w) run += S.red[w];
-        for (int c = c0; c < c1; ++c) {
-            cpre[c] = int32_t(run);
-            run += __ldcg(ccnt + c);
+        for (int cb = c0; cb < c1; cb += kScanU) {
+            int32_t v[kScanU];
+#pragma unroll
+            for (int u = 0; u < kScanU; ++u) v[u] = cb + u < c1 ? __ldcg(ccnt + cb + u) : 0;
+#pragma unroll
+            for (int u = 0; u < kScanU; ++u) {
+                if (cb + u < c1) cpre[cb + u] = int32_t(run);
+                run += v[u];
+            }
         }
     }
     __threadfence();
     __syncthreads();
+    TL_END(12);
     // kept rows before every head start: the chunk prefix plus a warp-wide
     // count of the kept rows in [chunk start, head start)
     for (int h = warp; h <= H; h += kTSThreads / 32) {

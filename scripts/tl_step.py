@@ -75,3 +75,14 @@ for step in (0, 1):
               f"end med {np.median(end) / 1e3:8.2f} max {end.max() / 1e3:8.2f} us{gap}")
         prev = end.max()
     print(f"step span {prev / 1e3:.2f} us")
+    # select sub-phases (ids 7..12: after the histograms, after the key loads,
+    # slice done, resolve done, candidates added, scan done): median of
+    # (mark - go) over the warps of this step's select launch
+    go_sel = rows["select"][:, 2].min() if "select" in rows else None
+    for mid, what in ((7, "hist"), (8, "keys"), (9, "slice"), (10, "resolve"), (11, "cand add"), (12, "scan")):
+        r = rec[kid == mid].astype(np.int64)
+        if len(r) and go_sel is not None:
+            r = r[(r[:, 2] >= go_sel) & (r[:, 2] < go_sel + 200000)]
+            if len(r):
+                d = (r[:, 3] - r[:, 2]) / 1e3
+                print(f"   select {what:8s} mark-go med {np.median(d):6.2f} max {d.max():6.2f} us (n={len(r)})")
