@@ -284,14 +284,8 @@ def run_ours(args, c, rank, world, device, torch, dist):
         return float(t.item()), launches, clk
 
     ms_max, launches, clk = timed(args.steps)
-    # the same step over a long power-capped run (clocks settle under the 1 kW cap)
-    sustained = None
-    if args.sustained_steps > 0:
-        s_ms, _, s_clk = timed(args.sustained_steps)
-        sustained = {"steps": args.sustained_steps, "ms_per_step": s_ms / args.sustained_steps,
-                     "value": None, "clocks": s_clk}
-
-    # per-kernel live timing: a separate pass with events around every launch
+    # per-kernel live timing: a separate pass with events around every launch,
+    # right after the timed steps (the same thermal state as the headline)
     prof_steps = min(args.steps, 30)
     ctx.profile(True)
     for i in range(prof_steps):
@@ -306,6 +300,13 @@ def run_ours(args, c, rank, world, device, torch, dist):
     prof_total = sum(x["ms_per_step"] for x in kernels.values())
     for k in kernels:
         kernels[k]["share"] = kernels[k]["ms_per_step"] / prof_total if prof_total else None
+
+    # the same step over a long power-capped run (clocks settle under the 1 kW cap)
+    sustained = None
+    if args.sustained_steps > 0:
+        s_ms, _, s_clk = timed(args.sustained_steps)
+        sustained = {"steps": args.sustained_steps, "ms_per_step": s_ms / args.sustained_steps,
+                     "value": None, "clocks": s_clk}
 
     if args.timeline:  # one profiled step's launch timeline (start, duration, stream)
         ctx.profile(True)

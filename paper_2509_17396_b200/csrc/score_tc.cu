@@ -475,7 +475,7 @@ __global__ void __maxnreg__(128)
         // A' rows: bf16 1.0 in K elements 0..2, zeros elsewhere (written by
         // threads, read by the tensor core: async-proxy fence before the barrier)
         for (int i = threadIdx.x; i < kBiasChunkB / 4; i += blockDim.x) {
-            const int byte = i * 4, r = ((byte & 255) >> 4) + 8 * (byte >> 8), kb = byte & 15, khi = byte & 128;
+            const int byte = i * 4, kb = byte & 15, khi = byte & 128;  // every row of the chunk alike
             uint32_t w = 0;
             if (!khi && kb == 0) w = 0x3F803F80u;  // K 0, 1
             if (!khi && kb == 4) w = 0x00003F80u;  // K 2

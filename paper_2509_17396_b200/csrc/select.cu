@@ -279,7 +279,6 @@ template <typename ScoreT>
 __global__ void __launch_bounds__(kSelThreads, 4) select_kernel(const __grid_constant__ SelectParams P) {
     using KeyT = typename KeyOf<ScoreT>::T;
     constexpr int kKeyBits = int(sizeof(KeyT) * 8);
-    constexpr int kTieBits = 40;  // (position < 2^31) << 8 | head (< 256)
     const KeyT kNone = ~KeyT(0);  // no finite or infinite score maps to it
     __shared__ SelShared<KeyT> S;
 
