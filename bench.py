@@ -123,6 +123,7 @@ class ClockSampler:
         sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
         load = [s for s in sm if s > 600] or sm
+        pw = [float(r[3]) for r in rows if r[3].strip().replace(".", "").isdigit()]
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
@@ -130,7 +131,35 @@ class ClockSampler:
                 if "Active" in r[5 + i] and "Not" not in r[5 + i]:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+                "power_w_median": statistics.median(pw) if pw else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+class EnergyMeter:
+    """NVML total-energy counter (mJ) of one GPU and its enforced power limit;
+    every method returns None where NVML is unavailable."""
+
+    def __init__(self, gpu: int):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+        except Exception:  # noqa: BLE001 (no NVML: energy is simply not reported)
+            self.h = None
+
+    def mj(self):
+        try:
+            return float(self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)) if self.h is not None else None
+        except Exception:  # noqa: BLE001
+            return None
+
+    def limit_w(self):
+        try:
+            return self.nv.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0 if self.h is not None else None
+        except Exception:  # noqa: BLE001
+            return None
 
 
 # ---------------------------------------------------------------------------
@@ -259,6 +288,8 @@ def run_ours(args, c, rank, world, device, torch, dist):
     ctx.poll_error()
     stream = torch.cuda.current_stream(device)
 
+    meter = EnergyMeter(device.index)
+
     def timed(steps):
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         clocks = ClockSampler(device.index)
@@ -268,15 +299,21 @@ def run_ours(args, c, rank, world, device, torch, dist):
             dist.barrier()
         torch.cuda.synchronize()
         launches0 = ctx.launches
+        e0 = meter.mj()
         ev0.record(stream)
         for i in range(steps):
             step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
+        e1 = meter.mj()
         if dist is not None:
             dist.barrier()
         launches = ctx.launches - launches0
         clk = clocks.stop()
+        # board energy of this GPU over the timed steps (NVML counter; coarse
+        # for a short burst), with the enforced power limit it runs against
+        clk["energy_j_per_step"] = (e1 - e0) / 1000.0 / steps if e0 is not None and e1 is not None else None
+        clk["power_limit_w"] = meter.limit_w()
         t = torch.tensor([ev0.elapsed_time(ev1)], device=device, dtype=torch.float64)
         if dist is not None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -307,6 +344,11 @@ def run_ours(args, c, rank, world, device, torch, dist):
         s_ms, _, s_clk = timed(args.sustained_steps)
         sustained = {"steps": args.sustained_steps, "ms_per_step": s_ms / args.sustained_steps,
                      "value": None, "clocks": s_clk}
+        # power-bound check: the step's board energy at the enforced power
+        # limit; ms_per_step close to this means the run is energy-bound (the
+        # 1 kW cap), not bound by any one unit's rate
+        if s_clk.get("energy_j_per_step") and s_clk.get("power_limit_w"):
+            sustained["ms_at_power_limit"] = s_clk["energy_j_per_step"] / s_clk["power_limit_w"] * 1000.0
 
     if args.timeline:  # one profiled step's launch timeline (start, duration, stream)
         ctx.profile(True)
