@@ -26,7 +26,8 @@ for li, L in enumerate(launches[-3:]):
     print(f"launch {li}: CTAs {len(L)}  begin us min/med/max {begs[0]:.1f}/{statistics.median(begs):.1f}/{begs[-1]:.1f}"
           f"  end us min/med/max {ends[0]:.1f}/{statistics.median(ends):.1f}/{ends[-1]:.1f}"
           f"  dur us min/med/max {durs[0]:.1f}/{statistics.median(durs):.1f}/{durs[-1]:.1f}"
-          f"  wait cyc med {statistics.median(waits)}")
+          f"  wait cyc med {statistics.median(waits)}"
+          f"  SM clock GHz med {statistics.median(x[6] / max(1, x[2] - x[1]) for x in L):.3f}")
     slow = sorted(L, key=lambda x: x[2])[-5:]
     print("  last-ending CTAs (cta, sm, begin us, dur us, tiles):",
           [(x[0], x[3], round((x[1] - t0) / 1e3, 1), round((x[2] - x[1]) / 1e3, 1), x[8] - x[7]) for x in slow])
