@@ -123,7 +123,6 @@ class ClockSampler:
         sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
         load = [s for s in sm if s > 600] or sm
-        pw = [float(r[3]) for r in rows if r[3].strip().replace(".", "").isdigit()]
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
@@ -131,7 +130,7 @@ class ClockSampler:
                 if "Active" in r[5 + i] and "Not" not in r[5 + i]:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
-                "power_w_median": statistics.median(pw) if pw else None, "reasons": sorted(reasons),
+                "reasons": sorted(reasons),
                 "samples": len(rows)}
 
 
@@ -312,7 +311,8 @@ def run_ours(args, c, rank, world, device, torch, dist):
         clk = clocks.stop()
         # board energy of this GPU over the timed steps (NVML counter; coarse
         # for a short burst), with the enforced power limit it runs against
-        clk["energy_j_per_step"] = (e1 - e0) / 1000.0 / steps if e0 is not None and e1 is not None else None
+        clk["energy_j_per_step"] = ((e1 - e0) / 1000.0 / steps
+                                    if e0 is not None and e1 is not None and e1 > e0 else None)
         clk["power_limit_w"] = meter.limit_w()
         t = torch.tensor([ev0.elapsed_time(ev1)], device=device, dtype=torch.float64)
         if dist is not None:
@@ -350,6 +350,10 @@ def run_ours(args, c, rank, world, device, torch, dist):
         if s_clk.get("energy_j_per_step") and s_clk.get("power_limit_w"):
             sustained["ms_at_power_limit"] = s_clk["energy_j_per_step"] / s_clk["power_limit_w"] * 1000.0
 
+    energy_costs = None
+    if sustained is not None and not args.no_power_roofline and meter.mj() is not None:
+        energy_costs = calibrate_energy(torch, device, meter)
+
     if args.timeline:  # one profiled step's launch timeline (start, duration, stream)
         ctx.profile(True)
         for i in range(3):
@@ -366,7 +370,40 @@ def run_ours(args, c, rank, world, device, torch, dist):
     e2e = run_e2e(args, c, epk, torch, device, ctx, dist) if not args.no_e2e else None
     phase_a = run_phase_a(c, epk, torch, device) if c.get("E", 1) > 1 and rank == 0 else None
     return dict(ms=ms_max, launches=launches, clocks=clk, kernels=kernels, e2e=e2e, live=live * n_ep, keep=keep,
-                sustained=sustained, exact=exact, phase_a=phase_a, episodes=n_ep)
+                sustained=sustained, exact=exact, phase_a=phase_a, episodes=n_ep, energy_costs=energy_costs)
+
+
+def calibrate_energy(torch, device, meter, secs=1.5):
+    """Board energy per byte of a plain HBM copy (b.copy_(a), 1 Gi bf16: 4 GiB
+    read + written per 2 launches) and per bf16 FLOP of a dense GEMM (8192^3),
+    each run back to back for ~secs on this GPU (NVML energy counter).  These
+    board-level costs (static power included) price the step's algorithmic
+    bytes and tensor FLOPs for the power roofline."""
+    out = {}
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device=device).normal_()
+    b = torch.empty_like(a)
+    x = torch.randn(8192, 8192, dtype=torch.bfloat16, device=device)
+    y = torch.randn(8192, 8192, dtype=torch.bfloat16, device=device)
+    for name, fn, work in (("pj_per_byte", lambda: b.copy_(a), 2.0 * (1 << 31)),
+                           ("pj_per_flop", lambda: torch.matmul(x, y), 2.0 * 8192 ** 3)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        t = time.time()
+        n = 0
+        e0 = meter.mj()
+        while time.time() - t < secs:
+            for _ in range(10):
+                fn()
+            n += 10
+            torch.cuda.synchronize()
+        e1 = meter.mj()
+        out[name] = (e1 - e0) * 1e9 / n / work  # mJ -> pJ per unit
+    del a, b, x, y
+    torch.cuda.empty_cache()
+    out["how"] = ("NVML board energy over ~1.5 s of back-to-back torch b.copy_(a) (1 Gi bf16) and torch.matmul "
+                  "bf16 8192^3 on this GPU, right after the sustained step run")
+    return out
 
 
 def run_exact_f32(args, c, epk, torch, device, ctx, dist):
@@ -686,6 +723,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--no-power-roofline", action="store_true",
+                    help="skip the copy / GEMM energy calibration behind the power roofline")
     ap.add_argument("--sustained-steps", type=int, default=1000,
                     help="a second, long timed run of the same step (power-capped clocks); 0 = skip")
     ap.add_argument("--no-e2e", action="store_true")
@@ -788,6 +827,21 @@ def main():
     if sus is not None:
         sus["value"] = units_all / (sus["ms_per_step"] / 1000.0)
         sus["step_roofline_frac"] = B / (sus["ms_per_step"] / 1000.0) / 1e9 / hbm
+    # power roofline: the step's algorithmic HBM bytes and its two MMA passes
+    # priced at this board's measured energy per copied byte and per GEMM
+    # FLOP; at the enforced power limit that energy takes model_ms.  The
+    # sustained step runs at the 1 kW cap, so its time is its energy / limit.
+    power_roof = None
+    ec = r.get("energy_costs")
+    if ec and sus is not None and sus["clocks"].get("energy_j_per_step") and sus["clocks"].get("power_limit_w"):
+        model_j = B * ec["pj_per_byte"] * 1e-12 + 2.0 * F * ec["pj_per_flop"] * 1e-12
+        meas_j = sus["clocks"]["energy_j_per_step"]
+        lim = sus["clocks"]["power_limit_w"]
+        power_roof = {"bound": "board energy at the power limit", "model_j_per_step": model_j,
+                      "measured_j_per_step": meas_j, "frac": model_j / meas_j, "power_limit_w": lim,
+                      "model_ms_at_limit": model_j / lim * 1000.0, "sustained_ms_per_step": sus["ms_per_step"],
+                      "algorithmic_bytes": B, "tensor_flops_two_passes": 2.0 * F,
+                      "pj_per_byte": ec["pj_per_byte"], "pj_per_flop": ec["pj_per_flop"], "how": ec["how"]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(dict(c, E=1))
@@ -798,7 +852,7 @@ def main():
             "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": config, "score_mode": "tc_bf16", "episodes_per_gpu": n_ep,
-            "roofline": roof, "step_roofline": step_roof, "kernels": kernels, "cpu_baseline": cpu,
+            "roofline": roof, "step_roofline": step_roof, "power_roofline": power_roof, "kernels": kernels, "cpu_baseline": cpu,
             "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
             "sustained": sus, "exact_f32": r["exact"], "phase_a": r["phase_a"],
         }

@@ -5,6 +5,8 @@ Each mode runs back to back for ~SECS seconds on the same resident inputs
   step    epk_evict_step (P1 -> bias -> P2 -> threshold select -> gather)
   score   epk_score (P1 -> bias -> P2 only)
   gather  epk_compact with a fixed keep mask (79 % kept: count -> plan -> gather)
+  copy    torch b.copy_(a), 1 Gi bf16 (2 GiB of HBM traffic): board pJ per byte moved
+  gemm    torch.matmul bf16 8192^3: board pJ per FLOP
 and reports ms per iteration, mean board power, energy per iteration (NVML
 total-energy counter), median SM clock and the throttle reasons seen.
 Usage: python scripts/power_probe.py [modes...]"""
@@ -49,8 +51,20 @@ def main(modes):
             live_mask[caches[r].live_rows(l)] = True
         keeps.append(((torch.rand(caches[r].rows, generator=g, device=dev) < 0.79) & live_mask).to(torch.uint8))
 
+    ca = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev).normal_() if "copy" in modes else None
+    cb = torch.empty_like(ca) if ca is not None else None
+    ga = torch.randn(8192, 8192, dtype=torch.bfloat16, device=dev) if "gemm" in modes else None
+    gb = torch.randn(8192, 8192, dtype=torch.bfloat16, device=dev) if "gemm" in modes else None
+    work = {"copy": ("pj_per_byte", 2.0 * (1 << 31)), "gemm": ("pj_per_flop", 2.0 * 8192 ** 3)}
+
     def run(mode, i):
         r = i % 3
+        if mode == "copy":
+            cb.copy_(ca)
+            return
+        if mode == "gemm":
+            torch.matmul(ga, gb)
+            return
         if mode == "step":
             evict_step(caches[r], out, qs[r], kps[r], budgets, mode="tc_bf16", slack=c["block"], n_max_per_head=n_h,
                        plan=plans[r], ctx=ctx)
@@ -105,6 +119,9 @@ def main(modes):
         res[mode] = dict(iters=n, ms_per_iter=round(ms, 4), wall_s=round(t1 - t0, 2),
                          energy_mj_per_iter=round((e1 - e0) / n, 3), mean_w=round(sum(watts) / len(watts), 1),
                          sm_mhz_median=clocks[len(clocks) // 2], sm_mhz_min=clocks[0], reasons=reasons)
+        if mode in work:
+            res[mode][work[mode][0]] = round((e1 - e0) / n * 1e9 / work[mode][1], 3)
+            res[mode]["rate_per_s"] = work[mode][1] / (ms / 1000.0)
         ctx.poll_error()  # a flagged (skipped) layer would make the timing meaningless
         print(mode, json.dumps(res[mode]), flush=True)
     print(json.dumps(res))
