@@ -398,7 +398,7 @@ __global__ void tc_bias_kernel(const __grid_constant__ TcParams P) {
 #define mbar_wait_pm mbar_wait_backoff
 #endif
 
-template <int MODE, int POLY>
+template <int MODE>
 __global__ void __maxnreg__(128)
     tc_score_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kp) {
@@ -717,14 +717,14 @@ __global__ void __maxnreg__(128)
                             P1PROF(long long c_1 = clock64());
                             tmem_ld64(tmem + lane_addr + uint32_t(ts * 128), v);
                             P1PROF(long long c_2 = clock64());
-                            stats_cols<64, POLY>(v, lim, P.c2, m[c], z[c]);
+                            stats_cols<64>(v, lim, P.c2, m[c], z[c]);
                             P1PROF(long long c_3 = clock64());
                             tmem_ld64(tmem + lane_addr + uint32_t(ts * 128 + 64), v);
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&t_empty[ts]);  // slot free: values are in registers
                             P1PROF(long long c_4 = clock64());
-                            stats_cols<64, POLY>(v, lim - 64, P.c2, m[c], z[c]);
+                            stats_cols<64>(v, lim - 64, P.c2, m[c], z[c]);
                             P1PROF(long long c_5 = clock64(); pw += c_1 - c_0; pl += (c_2 - c_1) + (c_4 - c_3);
                                    pc += (c_3 - c_2) + (c_5 - c_4); if (pj == 0) pfirst = c_1 - p_beg; ++pj; c_prev = c_5);
                         }
@@ -910,15 +910,9 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.run_hk_base = 0;
     const int grid = score_grid(ctx);  // persistent: one CTA per SM, tile-balanced ranges
 
-    // STATS kernels by exp2 split (POLY of every 4 column pairs on the FMA
-    // pipe); EPK_TC_POLY picks one (default 0: measured on B200 the FFMA2
-    // polynomial costs more issue than the SFU time it saves).
     using KernelFn = void (*)(TcParams, CUtensorMap, CUtensorMap, CUtensorMap);
-    static const KernelFn stats_fns[4] = {tc_score_kernel<MODE_STATS, 0>, tc_score_kernel<MODE_STATS, 1>,
-                                          tc_score_kernel<MODE_STATS, 2>, tc_score_kernel<MODE_STATS, 3>};
-    const KernelFn score_fn = tc_score_kernel<MODE_SCORE, 0>;
-    int poly = 0;
-    if (const char* e = std::getenv("EPK_TC_POLY")) poly = std::max(0, std::min(3, std::atoi(e)));
+    const KernelFn stats_fn = tc_score_kernel<MODE_STATS>;
+    const KernelFn score_fn = tc_score_kernel<MODE_SCORE>;
     // Dynamic shared memory limit: the per-block opt-in maximum minus the
     // kernels' static shared memory.  Function attributes are per device, so
     // the opt-in is made once per device (contexts of several GPUs may share
@@ -932,18 +926,14 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
         if (!dev_limit[ctx->device]) {
             int optin = 0;
             EPK_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-            size_t stat = 0;
-            for (KernelFn f : stats_fns) {
-                cudaFuncAttributes fa;
-                EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f)));
-                stat = std::max(stat, fa.sharedSizeBytes);
-            }
+            cudaFuncAttributes fa0;
+            EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa0, reinterpret_cast<const void*>(stats_fn)));
+            const size_t stat = fa0.sharedSizeBytes;
             cudaFuncAttributes fa1;
             EPK_CUDA_CHECK(cudaFuncGetAttributes(&fa1, reinterpret_cast<const void*>(score_fn)));
             const int lim = optin - int(std::max(stat, fa1.sharedSizeBytes));
-            for (KernelFn f : stats_fns)
-                EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+            EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(stats_fn),
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
             EPK_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(score_fn),
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
             dev_limit[ctx->device] = lim;  // only once every attribute is set
@@ -999,7 +989,7 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     out->grid = grid;
     T.P1 = P;
     T.smem1 = smem_bytes(P, MODE_STATS);
-    T.stats_fn = stats_fns[poly];
+    T.stats_fn = stats_fn;
     if (std::getenv("EPK_TC_VERBOSE"))
         fprintf(stderr, "P1: NQ=%d cg_chunks=%d cgroups=%d kstages=%d smem=%d limit=%d runs=%d\n", P.NQ, P.cg_chunks,
                 P.cgroups, P.kstages, T.smem1, limit, P.runs);

@@ -108,9 +108,9 @@ __device__ __forceinline__ void score_cols(const float (&v)[W], int r0, const PT
 
 // STATS epilogue on W columns of one query row, `lim` of them valid:
 // online (max, sum 2^(x c2 - max)) update of (m, z).  Pairs of columns go
-// through FFMA2/FADD2; POLY of every 4 pairs take their exp2 on the FMA pipe
-// (exp2_poly2) so the SFU -- the bound of this pass -- carries only the rest.
-template <int W, int POLY>
+// through FFMA2/FADD2, every exp2 through MUFU.EX2 (the bound of this pass;
+// moving a share of them to an FMA-pipe polynomial measured slower).
+template <int W>
 __device__ __forceinline__ void stats_cols(float (&v)[W], int lim, float c2, float& m, float& z) {
     float mx = -INFINITY;
     if (lim >= W) {
@@ -151,14 +151,9 @@ __device__ __forceinline__ void stats_cols(float (&v)[W], int lim, float c2, flo
             uint64_t e[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                const uint64_t t = q ? t1 : t0;
-                if (((i / 2 + q) & 3) >= 4 - POLY) {
-                    e[q] = exp2_poly2(t);
-                } else {
-                    float a, b;
-                    f2_unpack(t, a, b);
-                    e[q] = f2_pack(ex2(a), ex2(b));
-                }
+                float a, b;
+                f2_unpack(q ? t1 : t0, a, b);
+                e[q] = f2_pack(ex2(a), ex2(b));
             }
             acc0 = fadd2(acc0, e[0]);
             acc1 = fadd2(acc1, e[1]);
