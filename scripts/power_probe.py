@@ -35,7 +35,9 @@ REASONS = {
 def main(modes):
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(0)
-    c = bench.CONFIGS["cfg2"]
+    c = dict(bench.CONFIGS["cfg2"])
+    if os.environ.get("PROBE_LAYERS"):  # e.g. 4: one step's K (84 MB) stays in L2 between P1 and P2
+        c["L"] = int(os.environ["PROBE_LAYERS"])
     dev = torch.device("cuda:0")
     ctx = epk.default_context(0)
     n_h, live, keep_n = bench.step_sizes(c)
@@ -116,7 +118,7 @@ def main(modes):
         clocks = sorted(s[0] for s in samples[len(samples) // 4:]) or [0]
         watts = [s[1] for s in samples[len(samples) // 4:]] or [0]
         reasons = sorted({k for s in samples for k, b in REASONS.items() if s[2] & b})
-        res[mode] = dict(iters=n, ms_per_iter=round(ms, 4), wall_s=round(t1 - t0, 2),
+        res[mode] = dict(layers=c["L"], iters=n, ms_per_iter=round(ms, 4), wall_s=round(t1 - t0, 2),
                          energy_mj_per_iter=round((e1 - e0) / n, 3), mean_w=round(sum(watts) / len(watts), 1),
                          sm_mhz_median=clocks[len(clocks) // 2], sm_mhz_min=clocks[0], reasons=reasons)
         if mode in work:
