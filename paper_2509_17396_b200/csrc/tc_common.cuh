@@ -106,6 +106,36 @@ __device__ __forceinline__ void score_cols(const float (&v)[W], int r0, const PT
     }
 }
 
+// EPK_P1_POLY3 (0 = off): that many column pairs of every EPK_P1_POLY3_OF take
+// their exp2 on the FMA pipe -- Cody-Waite split t = j + f (j by the 1.5*2^23
+// magic add, f in [-1/2, 1/2]), degree-3 minimax for 2^f (max rel. error
+// 7.5e-5, mean 5e-6), j added to the exponent bits -- so the SFU, the bound of
+// P1, carries the rest.  t is clamped at -126 (masked columns), NaN kept.
+#ifndef EPK_P1_POLY3
+#define EPK_P1_POLY3 3
+#endif
+#ifndef EPK_P1_POLY3_OF
+#define EPK_P1_POLY3_OF 16
+#endif
+__device__ __forceinline__ float clamp_lo_nan(float t) { return t < -126.f ? -126.f : t; }
+__device__ __forceinline__ uint64_t exp2_poly3x2(uint64_t t2) {
+    float a, b;
+    f2_unpack(t2, a, b);
+    const uint64_t t = f2_pack(clamp_lo_nan(a), clamp_lo_nan(b));
+    const uint64_t magic = f2_pack(12582912.f, 12582912.f);
+    const uint64_t r = fadd2(t, magic);
+    const uint64_t j = fadd2(r, f2_pack(-12582912.f, -12582912.f));
+    const uint64_t f = ffma2(j, f2_pack(-1.f, -1.f), t);
+    uint64_t p = ffma2(f2_pack(0x1.c3f76p-5f, 0x1.c3f76p-5f), f, f2_pack(0x1.f0de1ap-3f, 0x1.f0de1ap-3f));
+    p = ffma2(p, f, f2_pack(0x1.62f31ap-1f, 0x1.62f31ap-1f));
+    p = ffma2(p, f, f2_pack(0x1.fff692p-1f, 0x1.fff692p-1f));
+    float p0, p1, r0, r1;
+    f2_unpack(p, p0, p1);
+    f2_unpack(r, r0, r1);
+    return f2_pack(__uint_as_float(__float_as_uint(p0) + (__float_as_uint(r0) << 23)),
+                   __uint_as_float(__float_as_uint(p1) + (__float_as_uint(r1) << 23)));
+}
+
 // STATS epilogue on W columns of one query row, `lim` of them valid:
 // online (max, sum 2^(x c2 - max)) update of (m, z).  Pairs of columns go
 // through FFMA2/FADD2, every exp2 through MUFU.EX2 (the bound of this pass;
@@ -151,9 +181,13 @@ __device__ __forceinline__ void stats_cols(float (&v)[W], int lim, float c2, flo
             uint64_t e[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                float a, b;
-                f2_unpack(q ? t1 : t0, a, b);
-                e[q] = f2_pack(ex2(a), ex2(b));
+                if (((i / 2 + q) % EPK_P1_POLY3_OF) >= EPK_P1_POLY3_OF - EPK_P1_POLY3) {
+                    e[q] = exp2_poly3x2(q ? t1 : t0);
+                } else {
+                    float a, b;
+                    f2_unpack(q ? t1 : t0, a, b);
+                    e[q] = f2_pack(ex2(a), ex2(b));
+                }
             }
             acc0 = fadd2(acc0, e[0]);
             acc1 = fadd2(acc1, e[1]);
