@@ -55,6 +55,7 @@
 #include "epikv/scoring.hpp"
 #include "epikv/toymodel.hpp"
 #include "epk/epk.h"
+#include "epikv/epikv_device.hpp"
 
 namespace epikv {
 namespace gpu {
@@ -866,6 +867,58 @@ inline BuildResult build(const Model& model, const ConversationHistory& history,
     result.set.store_dir = store_dir;
     result.set.budget_per_head = budget_per_head;
     return result;
+}
+
+// The live cache of a DeviceEpisode (the throughput path, epikv_device.hpp)
+// as the reference's EpisodicCache: bf16 keys / values widened to double,
+// every head's entries in position order, budgets as the layer budgets.  For
+// persisting with the reference's CacheStore or decoding on the host.
+inline EpisodicCache to_episodic_cache(const DeviceEpisode& e, std::size_t episode_id = 0,
+                                       const std::string& scorer = "patched") {
+    e.synchronize();
+    const epk_cache_desc c = e.desc();
+    const std::size_t L = e.layers(), H = e.kv_heads(), d = e.head_dim();
+    const std::size_t rows = std::size_t(e.layer_base()[L]);
+    std::vector<std::int32_t> off(L * (H + 1)), len(L * H), pos(rows);
+    std::vector<std::uint16_t> k(rows * d), v(rows * d);
+    detail::cuda_check(cudaMemcpy(off.data(), c.head_off, off.size() * 4, cudaMemcpyDeviceToHost), "D2H head_off");
+    detail::cuda_check(cudaMemcpy(len.data(), c.head_len, len.size() * 4, cudaMemcpyDeviceToHost), "D2H head_len");
+    detail::cuda_check(cudaMemcpy(pos.data(), c.pos, rows * 4, cudaMemcpyDeviceToHost), "D2H pos");
+    detail::cuda_check(cudaMemcpy(k.data(), c.k, rows * d * 2, cudaMemcpyDeviceToHost), "D2H k");
+    detail::cuda_check(cudaMemcpy(v.data(), c.v, rows * d * 2, cudaMemcpyDeviceToHost), "D2H v");
+    auto widen = [](std::uint16_t b) {
+        const std::uint32_t u = std::uint32_t(b) << 16;
+        float f;
+        std::memcpy(&f, &u, 4);
+        return double(f);
+    };
+    EpisodicCache out;
+    out.episode_id = episode_id;
+    out.provenance.scorer = scorer;
+    std::size_t mx = 0;
+    for (std::size_t l = 0; l < L; ++l) {
+        const std::size_t m = std::size_t(e.budgets()[l]);
+        mx = std::max(mx, m);
+        out.provenance.layer_budgets.push_back(m);
+        LayerCache lc(H, m);
+        for (std::size_t h = 0; h < H; ++h) {
+            const std::size_t r0 = std::size_t(e.layer_base()[l]) + std::size_t(off[l * (H + 1) + h]);
+            for (std::size_t i = 0; i < std::size_t(len[l * H + h]); ++i) {
+                KVEntry en;
+                en.position = std::size_t(pos[r0 + i]);
+                en.key.resize(d);
+                en.value.resize(d);
+                for (std::size_t j = 0; j < d; ++j) {
+                    en.key[j] = widen(k[(r0 + i) * d + j]);
+                    en.value[j] = widen(v[(r0 + i) * d + j]);
+                }
+                lc.heads[h].push_back(std::move(en));
+            }
+        }
+        out.layers.push_back(std::move(lc));
+    }
+    out.provenance.budget_per_head = mx;
+    return out;
 }
 
 }  // namespace gpu

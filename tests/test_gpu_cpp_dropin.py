@@ -64,3 +64,20 @@ def test_cpp_device_forward_matches_reference(gpu):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "0 failed" in r.stdout
+
+
+D_BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_build", "test_device_episode")
+
+
+def test_cpp_device_episode_matches_reference(gpu):
+    """epikv::gpu::DeviceEpisode (include/epikv/epikv_device.hpp), the C++ host
+    API of the throughput path: 8 blocks of append -> fused tensor-core step,
+    each equal to the reference's evict_to_budget on the step's own scores
+    (entries, positions, widened bf16 keys / values); then the cfg2 workload
+    timed from C++ (append + step per block)."""
+    if not os.path.exists(D_BIN):
+        pytest.skip("C++ device-episode driver not built (needs /root/reference at build time)")
+    r = subprocess.run([D_BIN, "--timing", "50"], capture_output=True, text=True, timeout=900)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "0 failed" in r.stdout
