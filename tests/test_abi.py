@@ -46,3 +46,18 @@ def test_cpp_dropin_header_compiles(tmp_path):
     r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", f"-I{ROOT}/include", f"-I{ref}", f"-I{json_inc}",
                         "-I/usr/local/cuda/include", str(src)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-3000:]
+
+
+def test_device_episode_header_is_standalone_cxx17():
+    """include/epikv/epikv_device.hpp (the C++ throughput API) compiles on its
+    own as C++17 against epk.h and the CUDA runtime headers only."""
+    import shutil
+    import subprocess
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("g++ not available")
+    src = '#include "epikv/epikv_device.hpp"\nint main() { return sizeof(epikv::gpu::DeviceEpisode) > 0 ? 0 : 1; }\n'
+    r = subprocess.run([gxx, "-std=c++17", "-fsyntax-only", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+                        "-I", "/usr/local/cuda/include", "-x", "c++", "-"], input=src, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "warning" not in r.stderr, r.stderr
