@@ -106,7 +106,15 @@ struct TcParams {
     int krows;      // K tile rows: 256 (STATS) / 128 (SCORE)
     int kstages;    // K ring depth
     int qcap;       // rows per d-half in the Q region
-    int resident;   // SCORE: all query chunks resident (else streamed pairs)
+    int resident;   // SCORE: the launch's query chunks resident (else streamed pairs)
+    int qg0, qgn;   // SCORE: the launch's query chunks [qg0, qg0 + qgn) (a query group when NQ > kMaxQRes)
+    int qgroups;    // SCORE: resident query groups (0: streamed pairs)
+    // SCORE over several query groups (Max, NQ > kMaxQRes): per cache row the
+    // running max of x - lse2/c2 over the groups done so far; the launch of
+    // a non-last group writes it, of a non-first group reads it, and only the
+    // last group emits the score
+    float* best_io;
+    int best_read, best_write;
     int runs;       // runs of this launch
     int ptiles;     // STATS: causal prompt tiles per run
     int p1_grid;    // STATS grid (SCORE reads it to locate the partials)
@@ -223,8 +231,8 @@ __device__ __forceinline__ Seg seg_at(const TcParams& P, const int32_t* s_pre, i
         x.nq = min(P.cg_chunks, P.NQ - x.c0);
         x.slot = kStatGroups * (int(blockIdx.x) - (part_cnt(T, gridDim.x, R0) - 1));
     } else {
-        x.c0 = 0;
-        x.nq = P.NQ;
+        x.c0 = P.qg0;
+        x.nq = P.qgn;
         x.slot = 0;
     }
     return x;
@@ -808,8 +816,15 @@ __global__ void __maxnreg__(128)
                         P2PROF(long long cb = clock64());
                         named_bar_sync(2 + quarter, 64);
                         P2PROF(ebar += clock64() - cb);
-                        if (half == em && jrow < x.n_h)
-                            emit_score(P, x.l, x.krow0 + jrow, ex2(fmaxf(best, sp[r_local]) * P.c2), s_coarse);
+                        if (half == em && jrow < x.n_h) {
+                            const int64_t row = x.krow0 + jrow;
+                            float b2 = fmaxf(best, sp[r_local]);
+                            if (P.best_read) b2 = fmaxf(b2, __ldcg(P.best_io + row));
+                            if (P.best_write)
+                                P.best_io[row] = b2;  // a later query group's launch finishes the row
+                            else
+                                emit_score(P, x.l, row, ex2(b2 * P.c2), s_coarse);
+                        }
                         ++tcount;
                     } else {
                         named_bar_sync(2 + quarter, 64);
@@ -858,6 +873,18 @@ static int smem_bytes(const TcParams& P, int mode) {
            (2 * P.kstages + 2 * kMaxQRes + 8) * 8 + 16 + (P.runs + 1) * 4;
 }
 
+// SCORE launch of query group g (chunks [g kMaxQRes, ...)): its query rows
+// (64-row units) split evenly over <= 256-row MMA jobs (384 -> 2 x 192).
+static void p2_group_jobs(TcParams* P, int g) {
+    P->qg0 = g * kMaxQRes;
+    P->qgn = P->qgroups <= 1 ? P->NQ : std::min(kMaxQRes, P->NQ - P->qg0);
+    const int rows = std::min(P->Gp - P->qg0 * kChunk, P->qgn * kChunk);
+    const int R = (rows + 63) / 64 * 64;
+    P->sj = (R + 255) / 256;
+    P->sj_n0 = (R / 64 + P->sj - 1) / P->sj * 64;
+    P->sj_nl = R - (P->sj - 1) * P->sj_n0;
+}
+
 // A tensor-core scoring launch plan.  P1 and P2 run per layer range [l0, l1)
 // (a step's layer group): P1 of a range, then P2 of the same range, so the
 // range's K tiles are re-read from L2 and a finished group's selection /
@@ -867,6 +894,7 @@ struct TcPlan {
     CUtensorMap tm_k, tm_q, tm_kp;
     int smem1, smem2;
     int grid;  // persistent CTAs of both passes
+    float* best_buf;  // P2 in query groups: the running max per cache row
     void (*stats_fn)(TcParams, CUtensorMap, CUtensorMap, CUtensorMap);
     void (*score_fn)(TcParams, CUtensorMap, CUtensorMap, CUtensorMap);
     const void* q;
@@ -908,6 +936,10 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.ptiles = (p + 127) / 128;
     P.hk_base = 0;
     P.run_hk_base = 0;
+    P.qgroups = 1;
+    P.qg0 = P.qgn = 0;
+    P.best_io = nullptr;
+    P.best_read = P.best_write = 0;
     const int grid = score_grid(ctx);  // persistent: one CTA per SM, tile-balanced ranges
 
     using KernelFn = void (*)(TcParams, CUtensorMap, CUtensorMap, CUtensorMap);
@@ -976,7 +1008,10 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.slots = kStatGroups * grid;
     const int64_t rows = int64_t(P.L) * H * P.NQ * kChunk;
     const int64_t pre_n = int64_t(P.L) * (int64_t(H) * P.cgroups + 1) + 1;
-    rc = ws_require(ctx, 2 * rows * P.slots * 4 + pre_n * 4 + rows * kBiasRowB + 4096);
+    const int64_t cache_rows = c->layer_base[c->layers];
+    const bool multi_group = P.NQ > kMaxQRes && agg_max;  // P2 in query groups: a running max per cache row
+    rc = ws_require(ctx, 2 * rows * P.slots * 4 + pre_n * 4 + rows * kBiasRowB + 4096 +
+                             (multi_group ? cache_rows * 4 + 256 : 0));
     if (rc) return rc;
     WsCarver carve(ctx->ws);
     P.prow = rows;
@@ -985,6 +1020,7 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     P.p1_pre = carve.take<int32_t>(pre_n);
     P.bias_out = carve.take<uint8_t>(rows * kBiasRowB);
     P.bias = P.bias_out;
+    float* best_buf = multi_group ? carve.take<float>(cache_rows) : nullptr;
     out->p1_pre_all = P.p1_pre;
     out->grid = grid;
     T.P1 = P;
@@ -999,13 +1035,18 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     // stay P1's (the merge maps query rows to P1 runs).
     P.krows = 128;
     P.runs = P.L * H;
-    P.resident = P.NQ <= kMaxQRes;
-    P.qcap = P.resident ? P.NQ * kChunk : 4 * kChunk;
-    if (P.resident) {  // query rows (64-row units) split evenly over <= 256-row MMA jobs: 384 -> 2 x 192
-        const int R = (P.Gp + 63) / 64 * 64;
-        P.sj = (R + 255) / 256;
-        P.sj_n0 = (R / 64 + P.sj - 1) / P.sj * 64;
-        P.sj_nl = R - (P.sj - 1) * P.sj_n0;
+    // more query chunks than fit: Max runs one launch per query group of <=
+    // kMaxQRes resident chunks (K streamed once per group, the running max
+    // carried in best_io); Avg streams chunk pairs through two slots per K tile
+    P.qgroups = P.NQ <= kMaxQRes ? 1 : (agg_max ? (P.NQ + kMaxQRes - 1) / kMaxQRes : 0);
+    P.resident = P.qgroups > 0;
+    P.qg0 = 0;
+    P.qgn = P.NQ;
+    P.best_io = nullptr;
+    P.best_read = P.best_write = 0;
+    P.qcap = P.NQ <= kMaxQRes ? P.NQ * kChunk : 4 * kChunk;
+    if (P.resident) {
+        p2_group_jobs(&P, 0);
     } else {  // streamed chunk pairs
         P.sj = (P.NQ + 1) / 2;
         P.sj_n0 = 256;
@@ -1024,6 +1065,7 @@ static int tc_plan(epk_ctx* ctx, const epk_cache_desc* c, const void* q, const v
     }
     if (P.kstages < 2) P.kstages = 2;  // over the co-residency budget: use the whole opt-in limit
     if (smem_bytes(P, MODE_SCORE) > limit) return fail(EPK_ERR_UNSUPPORTED, "score(tensor core): shared memory");
+    T.best_buf = best_buf;
     T.P2 = P;
     T.smem2 = smem_bytes(P, MODE_SCORE);
     T.score_fn = score_fn;
@@ -1102,10 +1144,19 @@ static int tc_launch_p2(epk_ctx* ctx, const TcPlan& T, int l0, int l1, int p0, i
     EPK_CUDA_CHECK(launch_pdl(tc_bias_kernel, dim3(unsigned(P.L * P.H)), dim3(unsigned(std::min(P.NQ * kChunk, 1024))), 0, ctx->stream,
                               P));
     EPK_LAUNCH_CHECK(ctx);
-    EPK_PROF(ctx, "p2_colscore");
-    EPK_CUDA_CHECK(launch_pdl(T.score_fn, dim3(T.grid), dim3(kThreads), T.smem2, ctx->stream, P, T.tm_k, tm_q,
-                              T.tm_kp));
-    EPK_LAUNCH_CHECK(ctx);
+    const int groups = std::max(1, P.qgroups);
+    for (int g = 0; g < groups; ++g) {
+        if (P.qgroups > 1) {
+            p2_group_jobs(&P, g);
+            P.best_io = T.best_buf;
+            P.best_read = g > 0;
+            P.best_write = g + 1 < groups;
+        }
+        EPK_PROF(ctx, "p2_colscore");
+        EPK_CUDA_CHECK(launch_pdl(T.score_fn, dim3(T.grid), dim3(kThreads), T.smem2, ctx->stream, P, T.tm_k, tm_q,
+                                  T.tm_kp));
+        EPK_LAUNCH_CHECK(ctx);
+    }
     return EPK_OK;
 }
 
