@@ -138,8 +138,9 @@ __device__ __forceinline__ uint64_t exp2_poly3x2(uint64_t t2) {
 
 // STATS epilogue on W columns of one query row, `lim` of them valid:
 // online (max, sum 2^(x c2 - max)) update of (m, z).  Pairs of columns go
-// through FFMA2/FADD2, every exp2 through MUFU.EX2 (the bound of this pass;
-// moving a share of them to an FMA-pipe polynomial measured slower).
+// through FFMA2/FADD2; the exp2 of EPK_P1_POLY3 of every EPK_P1_POLY3_OF pairs
+// through exp2_poly3x2 on the FMA pipe, the rest through MUFU.EX2 (the bound
+// of this pass; 3/16 measured best, profiles/p1_variants_r02c.txt).
 template <int W>
 __device__ __forceinline__ void stats_cols(float (&v)[W], int lim, float c2, float& m, float& z) {
     float mx = -INFINITY;
