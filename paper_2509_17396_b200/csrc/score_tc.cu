@@ -10,19 +10,23 @@
 // grid never exists in memory; K is streamed twice (P1, P2), Q stays in
 // shared memory.
 //
-// One persistent kernel template, two modes; every MMA is 128 x 256 x 128
-// (the shape that keeps tcgen05 near its issue peak -- 128 x 128 tiles
-// saturate shared-memory operand bandwidth):
-//   STATS (P1): A = 128-row query chunk (resident), B = 256-row K tile,
-//               D[query row][cache col] -> epilogue lanes own a query row and
-//               keep an online (max, sum exp2) per chunk -> one partial (m, Z)
-//               per (row, CTA segment, column half).
-//   SCORE (P2): A = 128-row K tile, B = two query chunks (256 query rows),
-//               D[cache row][query row] -> epilogue lanes own a cache row and
-//               reduce max_r (x c2 - lse2[r]) -> one exp2 per cache row.  The
-//               P1 partials of a head are folded into lse2 = log2 sum 2^(x-m)+m
-//               by the epilogue warps when a CTA reaches the head (no separate
-//               merge launch).
+// One persistent kernel template, two modes, 128-row K tiles:
+//   STATS (P1): A = 128-row query chunk (resident), B = K tile, MMA 128 x 128
+//               x 128 per (tile, chunk) job, D[query row][cache col] ->
+//               epilogue lanes own a query row and keep an online (max, sum
+//               exp2) per chunk (13/16 of the exp2 on MUFU, 3/16 as an FMA-pipe
+//               polynomial) -> one partial (m, Z) per (row, CTA segment,
+//               epilogue group).  P1 is bound by the exp2 rate, not the MMA.
+//   merge       tc_bias_kernel, one CTA per head: each query row's lse2 from
+//               its partials, written as P2's bias operand row.
+//   SCORE (P2): A = K tile, B = the head's query rows (<= 512 resident, as
+//               MMA jobs of N <= 256, 384 -> 2 x 192), D[cache row][query
+//               row]; the lse subtraction rides in the MMA as one extra
+//               16-wide K-step (bias rows), so the epilogue lanes (a cache row
+//               each) reduce a bare max over query rows -> one exp2 per cache
+//               row.  More query chunks than fit: Max runs one launch per
+//               resident query group carrying each row's running max; Avg
+//               streams chunk pairs through two slots per K tile.
 //
 // Work partition (tile-balanced): a mode's work is the sequence of RUNS
 // (STATS: (layer, kv-head, query-chunk group); SCORE: (layer, kv-head)), each
@@ -34,11 +38,11 @@
 // makespan is within one tile of the mean for any layer group and any
 // per-head raggedness.
 //
-// Shared memory keeps Q as [d-half][all query rows] (128-byte swizzled rows,
-// 8-row groups 1024 B apart) so any two consecutive 128-row chunks form one
-// 256-row B operand.  TMEM (512 columns): STATS three 128-column accumulator
-// slots, each owned by one epilogue group and one MMA warp (job j -> slot
-// j mod 3); SCORE two 256-column slots.
+// Shared memory keeps Q as [d-half][resident query rows] (128-byte swizzled
+// rows, 8-row groups 1024 B apart) so consecutive 128-row chunks form one
+// B operand of up to 256 rows.  TMEM (512 columns): STATS three 128-column
+// accumulator slots, each owned by one epilogue group and one MMA warp (job
+// j -> slot j mod 3); SCORE two 256-column slots.
 // Warp roles: warp 0 TMA producer; STATS (512 threads): warps 1-3 MMA issuers
 // (one per slot), warps 4-15 epilogue in three groups of four; SCORE (352
 // threads): warps 1-2 MMA issuers (alternate jobs), warps 3-10 epilogue
