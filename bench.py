@@ -352,7 +352,10 @@ def run_ours(args, c, rank, world, device, torch, dist):
 
     energy_costs = None
     if sustained is not None and not args.no_power_roofline and meter.mj() is not None:
-        energy_costs = calibrate_energy(torch, device, meter)
+        try:  # 4 GiB of scratch: a GPU short of memory skips the power roofline, not the bench
+            energy_costs = calibrate_energy(torch, device, meter)
+        except torch.cuda.OutOfMemoryError:
+            torch.cuda.empty_cache()
 
     if args.timeline:  # one profiled step's launch timeline (start, duration, stream)
         ctx.profile(True)

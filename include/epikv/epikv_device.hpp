@@ -74,6 +74,21 @@ class DeviceEpisode {
         device_detail::cuda(cudaSetDevice(device_), "cudaSetDevice");
         device_detail::check(epk_ctx_create(device_, stream, &ctx_), "epk_ctx_create");
         stream_ = stream;
+        try {
+            allocate();
+        } catch (...) {
+            release();  // a constructor that throws runs no destructor
+            throw;
+        }
+    }
+
+    DeviceEpisode(const DeviceEpisode&) = delete;
+    DeviceEpisode& operator=(const DeviceEpisode&) = delete;
+
+    ~DeviceEpisode() { release(); }
+
+  private:
+    void allocate() {
         const std::size_t rows = std::size_t(base_[L_]);
         for (Buf& b : buf_) {
             device_detail::cuda(cudaMalloc(&b.k, rows * d_ * 2), "cudaMalloc(k)");
@@ -91,28 +106,30 @@ class DeviceEpisode {
         device_detail::cuda(cudaMemcpy(buf_[0].len, len.data(), len.size() * 4, cudaMemcpyHostToDevice), "H2D");
     }
 
-    DeviceEpisode(const DeviceEpisode&) = delete;
-    DeviceEpisode& operator=(const DeviceEpisode&) = delete;
-
-    ~DeviceEpisode() {
-        if (ctx_) {
-            cudaSetDevice(device_);
-            epk_ctx_synchronize(ctx_);
-            for (Buf& b : buf_) {
-                cudaFree(b.k);
-                cudaFree(b.v);
-                cudaFree(b.pos);
-                cudaFree(b.off);
-                cudaFree(b.len);
-            }
-            cudaFree(kept_);
-            epk_ctx_destroy(ctx_);
+    void release() noexcept {
+        if (!ctx_) return;
+        cudaSetDevice(device_);
+        epk_ctx_synchronize(ctx_);
+        for (Buf& b : buf_) {
+            cudaFree(b.k);  // cudaFree(nullptr) is a no-op
+            cudaFree(b.v);
+            cudaFree(b.pos);
+            cudaFree(b.off);
+            cudaFree(b.len);
+            b = Buf{};
         }
+        cudaFree(kept_);
+        kept_ = nullptr;
+        epk_ctx_destroy(ctx_);
+        ctx_ = nullptr;
     }
 
+  public:
+
     /// append_to_cache: k, v [dev] bf16 [layers][kv_heads][len][head_dim],
-    /// positions [dev] int32 [len] (the block's token positions, ascending
-    /// after every live position).  len <= block.
+    /// positions [dev] int32 [len] (the block's token positions; the caller
+    /// keeps them ascending and after every live position, as the reference's
+    /// block loop does -- not re-checked on the device).  len <= block.
     void append(const void* k, const void* v, const std::int32_t* positions, std::size_t len) {
         const epk_cache_desc c = desc();
         device_detail::check(epk_append(ctx_, &c, k, v, positions, std::int32_t(len), std::int32_t(block_)),
