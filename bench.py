@@ -229,11 +229,11 @@ def cpu_model():
     return platform.processor() or "unknown"
 
 
-def make_inputs(epk, torch, c, R, device, seed, dtype=None):
+def make_inputs(epk, torch, c, R, device, seed, dtype=None, budgets=None):
     """R steady-state input caches (n_l = M_l + block live rows per head of
     layer l, dense) and R prompt sets, resident in HBM (bf16 by default)."""
     dtype = dtype or torch.bfloat16
-    bud = layer_budgets(c)
+    bud = budgets if budgets is not None else layer_budgets(c)
     L, H, d, p, Hq = c["L"], c["H"], c["d"], c["p"], c["Hq"]
     nl = [b + c["block"] for b in bud]
     cap = [H * n for n in nl]
@@ -267,12 +267,20 @@ def run_ours(args, c, rank, world, device, torch, dist):
     n_h, live, keep = step_sizes(c)
     # this rank's episodes (episodes round-robin over the GPUs)
     n_ep = len(range(rank, c.get("E", 1), world)) if not args.total_live else 1
-    R = max(1, -(-3 // max(1, n_ep)))  # >= 3 distinct input caches per GPU: every step reads cold K/V
-    eps = []
-    for e in range(n_ep):
-        caches, qs, kps, out = make_inputs(epk, torch, c, R, device, 1234 + 97 * rank + e)
-        eps.append((caches, qs, kps, out))
+    # several episodes on this GPU: one step over all of them -- their layers
+    # concatenated in one cache (the C ABI is layer-agnostic and every layer
+    # keeps its own budget), so the episodes share the step's launches
+    batch = n_ep > 1 and not args.no_batch_episodes and n_ep * c["L"] <= 128
     budgets = layer_budgets(c)
+    eps = []
+    if batch:
+        R = 3
+        budgets = budgets * n_ep
+        eps.append(make_inputs(epk, torch, dict(c, L=n_ep * c["L"]), R, device, 1234 + 97 * rank, budgets=budgets))
+    else:
+        R = max(1, -(-3 // max(1, n_ep)))  # >= 3 distinct input caches per GPU: every step reads cold K/V
+        for e in range(n_ep):
+            eps.append(make_inputs(epk, torch, c, R, device, 1234 + 97 * rank + e))
     plans = [[StepPlan(cs[r], out, budgets) for r in range(R)] for cs, _, _, out in eps]
 
     def step(i):
@@ -373,7 +381,8 @@ def run_ours(args, c, rank, world, device, torch, dist):
     e2e = run_e2e(args, c, epk, torch, device, ctx, dist) if not args.no_e2e else None
     phase_a = run_phase_a(c, epk, torch, device) if c.get("E", 1) > 1 and rank == 0 else None
     return dict(ms=ms_max, launches=launches, clocks=clk, kernels=kernels, e2e=e2e, live=live * n_ep, keep=keep,
-                sustained=sustained, exact=exact, phase_a=phase_a, episodes=n_ep, energy_costs=energy_costs)
+                sustained=sustained, exact=exact, phase_a=phase_a, episodes=n_ep, energy_costs=energy_costs,
+                batched=batch)
 
 
 def calibrate_energy(torch, device, meter, secs=1.5):
@@ -726,6 +735,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--no-batch-episodes", action="store_true",
+                    help="several episodes per GPU: one step call per episode instead of one over all")
     ap.add_argument("--no-power-roofline", action="store_true",
                     help="skip the copy / GEMM energy calibration behind the power roofline")
     ap.add_argument("--sustained-steps", type=int, default=1000,
@@ -855,6 +866,7 @@ def main():
             "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": config, "score_mode": "tc_bf16", "episodes_per_gpu": n_ep,
+            "episodes_batched": r["batched"],
             "roofline": roof, "step_roofline": step_roof, "power_roofline": power_roof, "kernels": kernels, "cpu_baseline": cpu,
             "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
             "sustained": sus, "exact_f32": r["exact"], "phase_a": r["phase_a"],
