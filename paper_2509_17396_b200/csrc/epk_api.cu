@@ -573,8 +573,10 @@ int epk_evict_step(epk_ctx* ctx, const epk_cache_desc* in, const epk_cache_desc*
             EPK_CUDA_CHECK(cudaStreamWaitEvent(ctx->hi, ctx->ev_hi, 0));
             ctx->stream = ctx->hi;
         }
+        // the fused selection works from the keys: the fp32 scores are written
+        // only when the caller asked for them
         rc = launch_step_tc_grouped(ctx, in, out, q, kp, q_heads, prompt_len, aggregation == EPK_AGG_MAX, budgets, G,
-                                    overlap ? ctx->side : nullptr, ctx->ev_fork, out_slack, scores, keep, fs_all, thr,
+                                    overlap ? ctx->side : nullptr, ctx->ev_fork, out_slack, scores_ws, keep, fs_all, thr,
                                     kept, launch_select_threshold, launch_compact, layer_view);
         ctx->stream = main;
         if (rc) return rc;

@@ -246,7 +246,7 @@ __device__ __forceinline__ Seg seg_at(const TcParams& P, const int32_t* s_pre, i
 // histogram counts.
 __device__ __forceinline__ void emit_score(const TcParams& P, int layer, int64_t row, float sc, uint32_t* s_coarse) {
     if (sc != sc) atomicCAS(P.err_flag, 0, EPK_ERR_NAN);  // non-finite inputs: the selection has no order for NaN
-    P.scores[row] = sc;
+    if (P.scores) P.scores[row] = sc;  // null: a fused step whose caller wants no scores (the keys carry them)
     if (P.keys) {
         P.keys[row] = desc_key(sc);
         const uint32_t b = min(__float_as_uint(sc) >> 14, 65535u);
