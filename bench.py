@@ -666,16 +666,20 @@ def cpu_cores():
 
 
 def cpu_baseline(c):
-    """The reference CPU path on this box's host cores, bounded: one whole
-    steady-state step (every layer) on all host threads, and a 2-layer sample
-    on one thread."""
+    """The reference CPU path on this box's host cores, bounded: two whole
+    steady-state steps (every layer; BASELINE.md section 3 asks for >= 2) on all
+    host threads, and a 2-layer sample on one thread."""
     cores = cpu_cores()
     L = c["L"]
-    tok_n, sec_n, kind = ref_units(c, [(l, l) for l in range(L)], cores)
+    tok_n = sec_n = 0
+    for st in range(2):  # one step's inputs in host memory at a time
+        tk, sc, kind = ref_units(c, [(l, st * L + l) for l in range(L)], cores)
+        tok_n += tk
+        sec_n += sc
     tok_1, sec_1, _ = ref_units(c, [(0, 0), (1 % L, 1)], 1)
     return {"value": tok_n / sec_n, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
             "value_1_thread": tok_1 / sec_1,
-            "sample": f"{cores} threads: one whole steady-state step ({L} layers x {c['H']} heads, "
+            "sample": f"{cores} threads: two whole steady-state steps ({L} layers x {c['H']} heads, "
                       f"p={c['p']}) in {sec_n:.1f} s; 1 thread: 2 of {L} layer-steps in {sec_1:.1f} s "
                       "(per-step throughput, the metric's unit; whole runs not timed): restated fp64 attention -> "
                       "epikv::score_with_prompt -> epikv::evict_to_budget (oracle/_ref)"}
