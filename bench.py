@@ -589,7 +589,9 @@ def run_e2e(args, c, epk, torch, device, ctx, dist):
             "d2h_bytes_per_step": int(d2h), "steps": steps,
             "ms_per_step": 1000.0 * float(tt.item()) / steps,
             "path": "paper_2509_17396_b200.append_to_cache + step.evict_step (C ABI epk_append/epk_evict_step), "
-                    "pinned host buffers, H2D of step i+1 overlapped with step i on a copy stream"}
+                    "pinned host buffers, H2D of step i+1 overlapped with step i on a copy stream"
+                    + ("" if c.get("E", 1) == 1 and not c.get("adaptive") else
+                       "; one episode per GPU with uniform budgets M (the config's own per-episode shape)")}
 
 
 # ---------------------------------------------------------------------------
